@@ -1,0 +1,209 @@
+/*
+ * gdx.h -- C ABI of the B200 GraNNDis hot-path engine (libgdx.so).
+ *
+ * The reference (/root/reference/proj) exposes its hot path only as C++
+ * free functions in namespace granndis; it has no FFI.  This
+ * header is the thin extern "C" layer those functions are re-implemented on:
+ * plain pointers and sizes, caller-allocated DEVICE buffers (unless a name
+ * says host), stream-ordered, no allocation inside per-layer calls, no
+ * exceptions.  Each entry point cites the reference code it replaces.
+ *
+ * Status codes mirror the reference error taxonomy (errors.hpp:11-44):
+ *   GDX_OK 0, GDX_INPUT 1 (InputError), GDX_CAPACITY 2 (CapacityError),
+ *   GDX_CONTRACT 3 (ContractError), GDX_INTERNAL 4 (InternalError / CUDA).
+ * gdx_last_error() returns the thread-local message of the last failure.
+ *
+ * Layouts: CSR row_ptr u64[rows+1] (absolute offsets) + col u32[nnz]
+ * (graph.hpp:21-60).  Dense matrices are row-major fp32 with a row pitch in
+ * elements.  GEMM operands are "split bf16": x = hi + lo with
+ * hi = bf16(x), lo = bf16(x - hi), stored as two uint16 arrays.
+ */
+#ifndef GDX_H
+#define GDX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* gdx_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+enum { GDX_OK = 0, GDX_INPUT = 1, GDX_CAPACITY = 2, GDX_CONTRACT = 3, GDX_INTERNAL = 4 };
+#define GDX_UNSEEN 0xFFFFFFFFu
+#define GDX_UNLIMITED_FANOUT 0xFFFFFFFFu
+
+const char* gdx_last_error(void);
+int gdx_version(void);
+/* Number of GPU kernel launches issued by this library in this process. */
+uint64_t gdx_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * Host preprocessing (C++, OpenMP).  Bit-identical to the reference.
+ * ---------------------------------------------------------------------- */
+/* gen_random_graph (graph.cpp:137-154, assemble_undirected :116-132).
+ * Pass 1 fills row_offsets[n+1] and returns nnz; pass 2 fills cols[nnz]. */
+uint64_t gdx_host_gen_random_graph_count(uint32_t n, double avg_degree, uint64_t seed,
+                                         uint64_t* row_offsets);
+int gdx_host_gen_random_graph_fill(uint32_t n, double avg_degree, uint64_t seed,
+                                   const uint64_t* row_offsets, uint32_t* cols);
+/* partition_random (partition.cpp:51-61). */
+int gdx_host_partition_random(uint32_t n, uint32_t parts, uint64_t seed, uint32_t* assignment);
+
+/* ------------------------------------------------------------------------
+ * K7 initialisation: make_features / make_layer_weights (reference_gnn.cpp:11-32)
+ * out[r*ld + c] = float(lo + (hi-lo)*next_double()) of stream (seed,k1,k2) at draw
+ * index first_draw + r*cols + c (SplitMix64 jump-ahead; bit-exact double math).
+ * ---------------------------------------------------------------------- */
+int gdx_init_uniform(uint64_t seed, uint64_t k1, uint64_t k2, uint64_t first_draw,
+                     uint32_t rows, uint32_t cols, double lo, double hi, float* out,
+                     uint64_t ld, gdx_stream stream);
+/* Same stream, written as fp64 (the reference Matrix element type). */
+int gdx_init_uniform_f64(uint64_t seed, uint64_t k1, uint64_t k2, uint64_t first_draw,
+                         uint32_t rows, uint32_t cols, double lo, double hi, double* out,
+                         uint64_t ld, gdx_stream stream);
+/* Builder-defined labels: KeyedRng(seed, base+v, "labl").next_below(classes). */
+int gdx_init_labels(uint64_t seed, uint64_t base, uint32_t rows, uint32_t classes,
+                    int32_t* out, gdx_stream stream);
+
+/* ------------------------------------------------------------------------
+ * K1/K3 aggregation: the forward_full inner loop (reference_gnn.cpp:76-83),
+ * forward_server_local's masked loop (:123-134) and the transposed backward.
+ *   out[v] = act( post_scale[v] * (self_coef * src[self_base+v]
+ *                                  + sum_{e in [row_ptr[v], row_end[v])} src[col[e]])
+ *                 + add[v] )
+ * ---------------------------------------------------------------------- */
+typedef struct gdx_aggregate_args {
+    const uint64_t* row_ptr;  /* [rows+1] */
+    const uint64_t* row_end;  /* nullable: per-row end (hop masking), else row_ptr[v+1] */
+    const uint32_t* col;
+    uint32_t rows;
+    uint32_t width;           /* feature width F (any; fast paths for F % 4 == 0) */
+    const float* src;         /* gathered matrix, row pitch ld_src (16 B aligned rows) */
+    uint64_t ld_src;
+    float self_coef;          /* 1: reference self term, 0: none (SAGE mean) */
+    uint64_t self_base;       /* src row of destination 0 (owned-row offset) */
+    const float* post_scale;  /* nullable, [rows] */
+    const float* add;         /* nullable, [rows x ld_add] (SAGE self path) */
+    uint64_t ld_add;
+    int relu;
+    float* out;               /* nullable fp32 [rows x ld_out] */
+    uint64_t ld_out;
+    uint16_t* out_hi;         /* nullable split-bf16 copy [rows x ld_split] */
+    uint16_t* out_lo;
+    uint64_t ld_split;
+} gdx_aggregate_args;
+int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream);
+
+/* ------------------------------------------------------------------------
+ * K2 dense transform on tcgen05 (apply_layer, reference_gnn.cpp:53-60), TN:
+ *   C[m][n] = sum_k (A_hi+A_lo)[m][k] * (B_hi+B_lo)[n][k]   (3 bf16 MMAs, fp32 TMEM acc)
+ * Epilogue: C *= row_scale[m]; relu; columns [0,split) -> c0, [split,n) -> c1;
+ * optional split-bf16 copy.  split_k > 1 writes raw partials to
+ * c0 + z*m*ldc0 (z < split_k) for gdx_splitk_reduce.
+ * Constraints: lda, ldb multiples of 8 elements; device pointers 16 B aligned.
+ * ---------------------------------------------------------------------- */
+typedef struct gdx_gemm_args {
+    const uint16_t* a_hi; const uint16_t* a_lo; uint64_t lda;
+    const uint16_t* b_hi; const uint16_t* b_lo; uint64_t ldb;
+    uint32_t m, n, k;
+    float* c0; uint64_t ldc0;
+    float* c1; uint64_t ldc1;
+    uint32_t split;           /* == n when c1 unused */
+    const float* row_scale;   /* nullable */
+    int relu;
+    uint16_t* out_hi; uint16_t* out_lo; uint64_t ld_split;   /* nullable */
+    uint32_t split_k;         /* 0/1: none */
+} gdx_gemm_args;
+int gdx_gemm_tn(const gdx_gemm_args* g, gdx_stream stream);
+/* Reference-precision SIMT fallback of the same contract, for tests only. */
+int gdx_gemm_tn_simt(const gdx_gemm_args* g, gdx_stream stream);
+/* out[i] = sum_z ws[z*stride + i] for i < rows*cols (pitch ld); then optional SGD:
+ * if w: w[i] -= lr * out[i] and (w_hi,w_lo) split copies are refreshed. */
+int gdx_splitk_reduce(const float* ws, uint32_t split_k, uint64_t stride, uint32_t rows,
+                      uint32_t cols, uint64_t ld, float* out, float* w, float lr,
+                      uint16_t* w_hi, uint16_t* w_lo, gdx_stream stream);
+
+/* ------------------------------------------------------------------------
+ * Layout / elementwise helpers of the training extension (no reference code).
+ * ---------------------------------------------------------------------- */
+/* dst (rows x cols, pitch ld_dst) = split(src); transpose=1 writes dst[c][r]. */
+int gdx_split_bf16(const float* src, uint64_t ld_src, uint32_t rows, uint32_t cols,
+                   uint16_t* hi, uint16_t* lo, uint64_t ld_dst, int transpose, gdx_stream stream);
+/* Transpose a split-bf16 pair: dst[c][r] = src[r][c]. */
+int gdx_transpose_split(const uint16_t* src_hi, const uint16_t* src_lo, uint64_t ld_src,
+                        uint32_t rows, uint32_t cols, uint16_t* dst_hi, uint16_t* dst_lo,
+                        uint64_t ld_dst, gdx_stream stream);
+/* Backward through act and the aggregation's destination scale:
+ *   g = dH * (mask ? (H > 0) : 1)          -> g_hi/g_lo (split, pitch ld_g) and g_out (fp32, nullable)
+ *   gs = g * dst_scale[v]                  -> gs (fp32, nullable; the rows to gather) */
+int gdx_grad_prepare(const float* dH, uint64_t ld_dh, const float* H, uint64_t ld_h,
+                     uint32_t rows, uint32_t width, const float* dst_scale,
+                     float* g_out, uint64_t ld_gout, float* gs, uint64_t ld_gs,
+                     uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g, gdx_stream stream);
+/* Softmax cross-entropy over rows: dlogits = (softmax - onehot) * inv_count,
+ * loss_sum[0] += sum of per-row losses (fp64 atomics). */
+int gdx_softmax_xent(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
+                     const int32_t* labels, float inv_count, float* dlogits, uint64_t ld_d,
+                     double* loss_sum, gdx_stream stream);
+/* Per-vertex scales from CSR degrees: kind 0 -> 1/deg (0 if deg=0), 1 -> (deg+1)^-1/2. */
+int gdx_degree_scale(const uint64_t* row_ptr, uint32_t rows, int kind, float* out,
+                     gdx_stream stream);
+
+/* ------------------------------------------------------------------------
+ * K4/K5 sampling and closure (integer, bit-exact).  Host-synchronising:
+ * frontier sizes are read back once per hop.
+ * ---------------------------------------------------------------------- */
+/* Shared hop loop of extract_sampled (extract.cpp:135-182) and batch_closure
+ * (batch_plan.cpp:28-70).  mark[n] in: 0 for excluded (inner / targets) vertices,
+ * GDX_UNSEEN otherwise; out: hop label of every vertex taken.  allowed (nullable)
+ * restricts candidates (the batch universe).  fanout GDX_UNLIMITED_FANOUT gives the
+ * unsampled closure (extract_full, extract.cpp:87-113).  work: >= 2*n + 64 u32. */
+int gdx_sampled_growth(const uint64_t* row_ptr, const uint32_t* col, uint32_t n,
+                       const uint8_t* excluded, const uint8_t* allowed, uint32_t max_hop,
+                       uint32_t fanout, uint64_t seed, uint32_t* mark, uint32_t* work,
+                       gdx_stream stream);
+/* count_induced_edges (extract.cpp:49-58): sum over v with mark[v] != UNSEEN of
+ * |{u in N(v): mark[u] != UNSEEN}|.  result: host pointer. work >= 1 u64. */
+int gdx_induced_count(const uint64_t* row_ptr, const uint32_t* col, uint32_t n,
+                      const uint32_t* mark, unsigned long long* work, uint64_t* result,
+                      gdx_stream stream);
+/* peel_mfg (batch_plan.cpp:75-101): counts[layers+1] (host) of the back-peeled
+ * MFG sets.  in_batch[n] u8; targets[nt]; work >= 3*n + 64 u32. */
+int gdx_peel_mfg(const uint64_t* row_ptr, const uint32_t* col, uint32_t n,
+                 const uint8_t* in_batch, const uint32_t* targets, uint64_t nt, uint32_t layers,
+                 uint32_t* work, uint64_t* counts, gdx_stream stream);
+/* split_batch (sim.cpp:81-102): share_of[i] for sorted batch_vertices[i]; inner
+ * vertices to their home GPU, halo vertices (ascending) to the least-loaded GPU,
+ * computed in closed form (greedy == (level, gpu)-ordered slot filling).
+ * work >= 5*nb + 2*gpus + 8 u32. */
+int gdx_split_batch(const uint32_t* batch_vertices, uint64_t nb, const uint32_t* server_assign,
+                    const uint32_t* gpu_assign, uint32_t server, uint32_t gpus,
+                    uint32_t* share_of, uint32_t* work, gdx_stream stream);
+/* Local numbering of a dependency subgraph for forward_server_local
+ * (reference_gnn.cpp:103-116): vertices with hop[v] != UNSEEN ordered by
+ * (hop, id), so the rows valid at layer l are a prefix.  Writes
+ * local_to_global[local_n], local_of[n] (UNSEEN outside), hop_start[max_hop+2]
+ * (host: first local id of each hop class) and returns local_n via *local_n. */
+int gdx_order_by_hop(const uint32_t* hop, uint32_t n, uint32_t max_hop, uint32_t* local_to_global,
+                     uint32_t* local_of, uint64_t* hop_start, uint32_t* local_n, gdx_stream stream);
+/* Induced local CSR over that numbering (reference_gnn.cpp:125-131): row i lists
+ * the in-subgraph neighbours of local_to_global[i] as local ids, in the global
+ * row's (ascending-id) order, so a row whose neighbours are all present reduces
+ * in exactly the same order as in the whole graph.
+ * Pass 1 (lptr == NULL): counts[i] = in-subgraph degree of local vertex i.
+ * Pass 2: writes the row at lptr[i]. */
+int gdx_local_csr(const uint64_t* row_ptr, const uint32_t* col, const uint32_t* local_to_global,
+                  uint32_t local_n, const uint32_t* local_of, uint64_t* counts, const uint64_t* lptr,
+                  uint32_t* lcol, gdx_stream stream);
+/* Exclusive prefix sum of counts[n] into out[n+1] (out[n] = total, also in *total). */
+int gdx_exclusive_scan_u64(const uint64_t* counts, uint64_t n, uint64_t* out, uint64_t* total,
+                           gdx_stream stream);
+/* out[i*ld_out + c] = src[idx[i]*ld_src + c] for i < rows, c < cols (row gather). */
+int gdx_gather_rows(const float* src, uint64_t ld_src, const uint32_t* idx, uint32_t rows,
+                    uint32_t cols, float* out, uint64_t ld_out, gdx_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GDX_H */

@@ -1,0 +1,182 @@
+"""Cooperative batching on the device -- the reference's batch_plan.hpp API and
+the simulator's split_batch (sim.cpp:81-102), re-exported.
+
+batch_closure (batch_plan.cpp:28-70) is the same device hop loop as EAS with
+the batch universe as the candidate mask; peel_mfg (:75-101) is a
+level-synchronous device BFS; split_batch is a closed-form device kernel.
+Target splitting (split_targets_mincut, :114-126) is host min-cut (C++).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call
+from .device import require_cuda, stream_handle
+from .errors import CapacityError, InputError
+from .extract import DependencySubgraph, SamplingConfig, sampled_growth_device, _Work
+from .graph import Graph, Partition
+
+kBytesPerScalar = 4
+kUnlimitedMemory = (1 << 64) - 1
+
+
+@dataclass
+class ModelSpec:
+    """cost_model.hpp ModelSpec."""
+    layers: int = 1
+    hidden_dim: int = 64
+    feature_dim: int = 64
+    expansion_factor: float = 1.5
+
+
+@dataclass
+class Batch:
+    """batch_plan.hpp:20-25."""
+    target_vertices: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    vertices: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    mfg_vertices_per_layer: list = field(default_factory=list)
+    est_memory_bytes: int = 0
+
+
+@dataclass
+class BatchPlan:
+    worker_id: int = 0
+    strategy: str = "fetch_then_split"
+    layers: int = 0
+    batches: list = field(default_factory=list)
+
+    def batch_count(self) -> int:
+        return len(self.batches)
+
+
+def estimate_batch_memory(b: Batch, model: ModelSpec) -> int:
+    """batch_plan.cpp:13-20."""
+    total = 0
+    for l, cnt in enumerate(b.mfg_vertices_per_layer):
+        width = model.feature_dim if l == 0 else model.hidden_dim
+        total += int(cnt) * width * kBytesPerScalar
+    return total
+
+
+def _mask(n: int, vertices, dev) -> torch.Tensor:
+    m = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+    if len(vertices):
+        m[torch.from_numpy(np.asarray(vertices, np.int64)).to(dev)] = 1
+    return m
+
+
+def batch_closure(g: Graph, universe: np.ndarray, targets: np.ndarray, cfg: SamplingConfig) -> np.ndarray:
+    """Sampled closure of ``targets`` inside ``universe`` (u8 mask over all vertices)."""
+    require_cuda()
+    dev = g.device().row_ptr.device
+    tmask = _mask(g.num_vertices(), targets, dev)
+    allowed = torch.from_numpy(np.ascontiguousarray(universe, np.uint8)).to(dev)
+    mark = sampled_growth_device(g, tmask, allowed, cfg.max_hop, cfg.fanout, cfg.seed)
+    hop = mark.cpu().numpy().view(np.uint32)
+    return np.nonzero(hop != 0xFFFFFFFF)[0].astype(np.uint32)
+
+
+def peel_mfg(g: Graph, batch_vertices: np.ndarray, targets: np.ndarray, layers: int) -> list:
+    require_cuda()
+    dg = g.device()
+    dev = dg.row_ptr.device
+    n = g.num_vertices()
+    in_batch = _mask(n, batch_vertices, dev)
+    t = torch.from_numpy(np.ascontiguousarray(targets, np.uint32).view(np.int32)).to(dev)
+    work = _Work.get(n, dev)
+    counts = np.zeros(layers + 1, np.uint64)
+    call("gdx_peel_mfg", dg.row_ptr.data_ptr(), dg.col.data_ptr(), n, in_batch.data_ptr(),
+         t.data_ptr(), len(targets), layers, work.data_ptr(), counts.ctypes.data, stream_handle())
+    return [int(c) for c in counts]
+
+
+def make_batch(g: Graph, universe: np.ndarray, targets: np.ndarray, layers: int,
+               cfg: SamplingConfig, model: ModelSpec) -> Batch:
+    """batch_plan.cpp:103-112."""
+    b = Batch(np.asarray(targets, np.uint32))
+    b.vertices = batch_closure(g, universe, b.target_vertices, cfg)
+    b.mfg_vertices_per_layer = peel_mfg(g, b.vertices, b.target_vertices, layers)
+    b.est_memory_bytes = estimate_batch_memory(b, model)
+    return b
+
+
+def split_targets_mincut(g: Graph, targets: np.ndarray, r: int, seed: int) -> list:
+    """batch_plan.cpp:114-126: min-cut split of the targets' induced subgraph (host C++)."""
+    if r <= 1 or len(targets) <= 1:
+        return [np.asarray(targets, np.uint32)]
+    from .partition_host import induced_subgraph, partition_mincut
+    sub, gids = induced_subgraph(g, targets)
+    p = partition_mincut(sub, r, seed)
+    return [np.sort(gids[p.assignment == k]).astype(np.uint32) for k in range(r)]
+
+
+def _build_cobatch(sub: DependencySubgraph, g: Graph, layers: int, cfg: SamplingConfig, r: int,
+                   model: ModelSpec) -> BatchPlan:
+    universe = np.zeros(g.num_vertices(), np.uint8)
+    universe[sub.inner_vertices] = 1
+    universe[sub.halo_vertices] = 1
+    plan = BatchPlan(sub.server_id, "fetch_then_split", layers)
+    for group in split_targets_mincut(g, sub.inner_vertices, r, cfg.seed):
+        plan.batches.append(make_batch(g, universe, group, layers, cfg, model))
+    return plan
+
+
+def plan_cobatch_fixed_r(sub: DependencySubgraph, g: Graph, layers: int, cfg: SamplingConfig,
+                         r: int, model: ModelSpec) -> BatchPlan:
+    """batch_plan.cpp:146-153."""
+    if r == 0:
+        raise InputError("plan_cobatch: batch count must be >= 1")
+    capped = min(r, max(1, len(sub.inner_vertices)))
+    return _build_cobatch(sub, g, layers, cfg, capped, model)
+
+
+def plan_cobatch(sub: DependencySubgraph, g: Graph, layers: int, cfg: SamplingConfig,
+                 mem_budget: int, model: ModelSpec) -> BatchPlan:
+    """batch_plan.cpp:155-180: smallest R whose batches all fit the budget (linear scan)."""
+    if mem_budget == 0:
+        raise InputError("plan_cobatch: mem_budget must be > 0")
+    max_r = max(1, len(sub.inner_vertices))
+    plan = None
+    for r in range(1, max_r + 1):
+        plan = _build_cobatch(sub, g, layers, cfg, r, model)
+        if max(b.est_memory_bytes for b in plan.batches) <= mem_budget:
+            return plan
+    worst = max(plan.batches, key=lambda b: b.est_memory_bytes)
+    first = int(worst.target_vertices[0]) if len(worst.target_vertices) else 0
+    raise CapacityError(f"single-target batch for vertex {first} needs {worst.est_memory_bytes} "
+                        f"bytes, budget is {mem_budget}")
+
+
+def split_batch(batch_vertices: np.ndarray, server_partition: Partition, gpu_partition: Partition,
+                server: int, gpus: int) -> list:
+    """sim.cpp:81-102 on the device: inner vertices to their home GPU, halo vertices
+    (ascending) to the least-loaded GPU (ties -> lowest).  Returns sorted shares."""
+    require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    bv = np.ascontiguousarray(batch_vertices, np.uint32)
+    nb = len(bv)
+    if nb == 0:
+        return [np.zeros(0, np.uint32) for _ in range(gpus)]
+    tb = torch.from_numpy(bv.view(np.int32)).to(dev)
+    sp = torch.from_numpy(server_partition.assignment.view(np.int32)).to(dev)
+    gp = torch.from_numpy(gpu_partition.assignment.view(np.int32)).to(dev)
+    share = torch.empty(nb, dtype=torch.int32, device=dev)
+    work = torch.empty(5 * nb + 2 * gpus + 8, dtype=torch.int32, device=dev)
+    call("gdx_split_batch", tb.data_ptr(), nb, sp.data_ptr(), gp.data_ptr(), server, gpus,
+         share.data_ptr(), work.data_ptr(), stream_handle())
+    s = share.cpu().numpy()
+    return [bv[s == w] for w in range(gpus)]
+
+
+def split_batch_owner(batch_vertices, server_partition, gpu_partition, server, gpus) -> np.ndarray:
+    """Per-vertex local GPU of split_batch (same kernel, un-grouped)."""
+    shares = split_batch(batch_vertices, server_partition, gpu_partition, server, gpus)
+    bv = np.asarray(batch_vertices, np.uint32)
+    out = np.zeros(len(bv), np.uint32)
+    for w, s in enumerate(shares):
+        out[np.searchsorted(bv, s)] = w
+    return out

@@ -1,0 +1,226 @@
+// aggregate.cu -- K1/K3: CSR gather-reduce aggregation on sm_100a.
+//
+// Replaces the reference's per-vertex loop (reference_gnn.cpp:76-83, masked
+// variant :123-134) and serves the transposed backward (A is symmetric,
+// graph.hpp:14-18, so A^T g is the same pull over the same CSR).
+//
+// Design (HBM/L2-bound gather, no tensor-core work):
+//  * one warp per destination row; the row's column indices are read once,
+//    coalesced, with an evict-first streaming hint and broadcast by shuffle;
+//  * a gathered row of F fp32 is read with 128-bit loads by LPE = pow2(F/4)
+//    lanes, so 32/LPE neighbour rows are in flight per warp step, unrolled 4x
+//    for memory-level parallelism;
+//  * partial sums of the lane groups are combined with xor-shuffles and the
+//    whole epilogue (self term, destination scale, SAGE self path, ReLU,
+//    fp32 and split-bf16 stores) is fused, so the output is written once.
+#include "gdx_common.cuh"
+
+namespace gdx {
+namespace {
+
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ float4 ld_row4(const float* p) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+}
+
+struct AggParams {
+    const uint64_t* row_ptr;
+    const uint64_t* row_end;
+    const uint32_t* col;
+    uint32_t rows;
+    uint32_t c4;  // width / 4
+    const float* src;
+    uint64_t ld_src;
+    float self_coef;
+    uint64_t self_base;
+    const float* post_scale;
+    const float* add;
+    uint64_t ld_add;
+    int relu;
+    float* out;
+    uint64_t ld_out;
+    uint16_t* out_hi;
+    uint16_t* out_lo;
+    uint64_t ld_split;
+};
+
+template <int LPE, int NCH>
+__global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
+    constexpr int EPW = 32 / LPE;  // neighbour rows per warp step
+    constexpr int UNROLL = 4;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / LPE;
+    const int lin = lane % LPE;
+    const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < p.rows;
+         row += warps_total) {
+        const uint64_t beg = p.row_ptr[row];
+        const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
+        float4 acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+        for (uint64_t e0 = beg; e0 < end; e0 += 32) {
+            const uint32_t cnt = static_cast<uint32_t>((end - e0) < 32 ? (end - e0) : 32);
+            const uint32_t my = lane < cnt ? ld_stream_u32(p.col + e0 + lane) : 0u;
+            for (uint32_t j = 0; j < cnt; j += EPW * UNROLL) {
+                float4 v[UNROLL][NCH];
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    const uint32_t slot = j + u * EPW + sub;
+                    const uint32_t nb = __shfl_sync(0xffffffffu, my, slot & 31);
+                    const bool ok = slot < cnt;
+                    const float* rowp = p.src + static_cast<uint64_t>(nb) * p.ld_src;
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        const uint32_t ch = lin + c * LPE;
+                        v[u][c] = (ok && ch < p.c4) ? ld_row4(rowp + 4 * ch)
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) add4(acc[c], v[u][c]);
+            }
+        }
+        // combine the EPW lane groups
+#pragma unroll
+        for (int off = LPE; off < 32; off <<= 1) {
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, off);
+                acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, off);
+                acc[c].z += __shfl_xor_sync(0xffffffffu, acc[c].z, off);
+                acc[c].w += __shfl_xor_sync(0xffffffffu, acc[c].w, off);
+            }
+        }
+        const float scale = (sub == 0 && p.post_scale) ? p.post_scale[row] : 1.f;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const uint32_t ch = lin + c * LPE;
+            if (sub != 0 || ch >= p.c4) continue;
+            float4 r = acc[c];
+            if (p.self_coef != 0.f) {
+                const float4 s = ld_row4(p.src + (p.self_base + row) * p.ld_src + 4 * ch);
+                r.x += p.self_coef * s.x;
+                r.y += p.self_coef * s.y;
+                r.z += p.self_coef * s.z;
+                r.w += p.self_coef * s.w;
+            }
+            r.x *= scale;
+            r.y *= scale;
+            r.z *= scale;
+            r.w *= scale;
+            if (p.add) add4(r, ld_row4(p.add + row * p.ld_add + 4 * ch));
+            if (p.relu) {
+                r.x = fmaxf(r.x, 0.f);
+                r.y = fmaxf(r.y, 0.f);
+                r.z = fmaxf(r.z, 0.f);
+                r.w = fmaxf(r.w, 0.f);
+            }
+            if (p.out) *reinterpret_cast<float4*>(p.out + row * p.ld_out + 4 * ch) = r;
+            if (p.out_hi) {
+                ushort4 h, l;
+                split_bf16(r.x, h.x, l.x);
+                split_bf16(r.y, h.y, l.y);
+                split_bf16(r.z, h.z, l.z);
+                split_bf16(r.w, h.w, l.w);
+                *reinterpret_cast<ushort4*>(p.out_hi + row * p.ld_split + 4 * ch) = h;
+                *reinterpret_cast<ushort4*>(p.out_lo + row * p.ld_split + 4 * ch) = l;
+            }
+        }
+    }
+}
+
+// Any width / alignment: one warp per row, lanes stride over columns.
+__global__ void __launch_bounds__(256) aggregate_scalar(const AggParams p, uint32_t width) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < p.rows;
+         row += warps_total) {
+        const uint64_t beg = p.row_ptr[row];
+        const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
+        const float scale = p.post_scale ? p.post_scale[row] : 1.f;
+        for (uint32_t c = lane; c < width; c += 32) {
+            float acc = p.self_coef != 0.f ? p.self_coef * p.src[(p.self_base + row) * p.ld_src + c]
+                                           : 0.f;
+            for (uint64_t e = beg; e < end; ++e)
+                acc += p.src[static_cast<uint64_t>(p.col[e]) * p.ld_src + c];
+            acc *= scale;
+            if (p.add) acc += p.add[row * p.ld_add + c];
+            if (p.relu) acc = fmaxf(acc, 0.f);
+            if (p.out) p.out[row * p.ld_out + c] = acc;
+            if (p.out_hi) split_bf16(acc, p.out_hi[row * p.ld_split + c], p.out_lo[row * p.ld_split + c]);
+        }
+    }
+}
+
+template <int LPE, int NCH>
+void launch_vec(const AggParams& p, cudaStream_t s) {
+    const uint32_t warps_per_block = 8;
+    uint64_t blocks = (static_cast<uint64_t>(p.rows) + warps_per_block - 1) / warps_per_block;
+    if (blocks > 65535ull * 64) blocks = 65535ull * 64;
+    aggregate_vec4<LPE, NCH><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
+}
+
+int pick_and_launch(const AggParams& p, cudaStream_t s) {
+    const uint32_t c4 = p.c4;
+    if (c4 <= 1) launch_vec<1, 1>(p, s);
+    else if (c4 <= 2) launch_vec<2, 1>(p, s);
+    else if (c4 <= 4) launch_vec<4, 1>(p, s);
+    else if (c4 <= 8) launch_vec<8, 1>(p, s);
+    else if (c4 <= 16) launch_vec<16, 1>(p, s);
+    else if (c4 <= 32) launch_vec<32, 1>(p, s);
+    else if (c4 <= 64) launch_vec<32, 2>(p, s);
+    else if (c4 <= 128) launch_vec<32, 4>(p, s);
+    else launch_vec<32, 8>(p, s);
+    return 0;
+}
+
+bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; }
+
+}  // namespace
+}  // namespace gdx
+
+extern "C" int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream) {
+    using namespace gdx;
+    GDX_REQUIRE(a != nullptr, GDX_INPUT, "gdx_aggregate: null args");
+    GDX_REQUIRE(a->rows == 0 || (a->row_ptr && a->col && a->src), GDX_INPUT,
+                "gdx_aggregate: null CSR or source");
+    GDX_REQUIRE(a->width > 0, GDX_INPUT, "gdx_aggregate: width must be >= 1");
+    GDX_REQUIRE(a->ld_src >= a->width, GDX_INPUT, "gdx_aggregate: ld_src < width");
+    GDX_REQUIRE(!a->out || a->ld_out >= a->width, GDX_INPUT, "gdx_aggregate: ld_out < width");
+    GDX_REQUIRE(!a->out_hi == !a->out_lo, GDX_INPUT, "gdx_aggregate: out_hi/out_lo must pair");
+    if (a->rows == 0) return GDX_OK;
+    AggParams p{a->row_ptr, a->row_end, a->col, a->rows, a->width / 4, a->src, a->ld_src,
+                a->self_coef, a->self_base, a->post_scale, a->add, a->ld_add, a->relu, a->out,
+                a->ld_out, a->out_hi, a->out_lo, a->ld_split};
+    const bool vec = a->width % 4 == 0 && a->ld_src % 4 == 0 && aligned16(a->src) && a->width <= 4096 &&
+                     (!a->add || (a->ld_add % 4 == 0 && aligned16(a->add))) &&
+                     (!a->out || (a->ld_out % 4 == 0 && aligned16(a->out))) &&
+                     (!a->out_hi || (a->ld_split % 4 == 0 && (reinterpret_cast<uintptr_t>(a->out_hi) & 7) == 0 &&
+                                     (reinterpret_cast<uintptr_t>(a->out_lo) & 7) == 0));
+    cudaStream_t s = as_cuda(stream);
+    if (vec) {
+        pick_and_launch(p, s);
+    } else {
+        uint64_t blocks = (static_cast<uint64_t>(a->rows) + 7) / 8;
+        if (blocks > 65535ull * 64) blocks = 65535ull * 64;
+        aggregate_scalar<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, a->width);
+    }
+    note_launch();
+    return check_launch("gdx_aggregate");
+}

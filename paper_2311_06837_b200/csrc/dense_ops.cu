@@ -1,0 +1,280 @@
+// dense_ops.cu -- initialisation (K7), layout and elementwise kernels of the
+// training extension (K8): split-bf16 conversion/transposes, ReLU/scale
+// backward prep, softmax cross-entropy, degree scales, split-K reduce + SGD.
+#include "gdx_common.cuh"
+
+namespace gdx {
+namespace {
+
+// make_features / make_layer_weights (reference_gnn.cpp:11-32): draw index
+// first + r*cols + c of stream (seed,k1,k2), uniform(lo,hi) in double, then fp32.
+__global__ void init_uniform_kernel(uint64_t s0, uint64_t first, uint32_t rows, uint32_t cols,
+                                    double lo, double hi, float* out, uint64_t ld) {
+    const uint64_t total = static_cast<uint64_t>(rows) * cols;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / cols, c = i % cols;
+        const double u = to_unit(draw_at(s0, first + i));
+        out[r * ld + c] = static_cast<float>(lo + (hi - lo) * u);
+    }
+}
+
+__global__ void init_uniform_f64_kernel(uint64_t s0, uint64_t first, uint32_t rows, uint32_t cols,
+                                        double lo, double hi, double* out, uint64_t ld) {
+    const uint64_t total = static_cast<uint64_t>(rows) * cols;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / cols, c = i % cols;
+        out[r * ld + c] = lo + (hi - lo) * to_unit(draw_at(s0, first + i));
+    }
+}
+
+__global__ void init_labels_kernel(uint64_t seed, uint64_t base, uint32_t rows, uint32_t classes,
+                                   int32_t* out) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < rows; v += gridDim.x * blockDim.x) {
+        const uint64_t s = keyed_state(seed, base + v, 0x6c61626cULL);  // "labl"
+        out[v] = static_cast<int32_t>(below(draw_at(s, 0), classes));
+    }
+}
+
+__global__ void split_kernel(const float* src, uint64_t ld_src, uint32_t rows, uint32_t cols,
+                             uint16_t* hi, uint16_t* lo, uint64_t ld_dst) {
+    const uint64_t total = static_cast<uint64_t>(rows) * cols;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / cols, c = i % cols;
+        split_bf16(src[r * ld_src + c], hi[r * ld_dst + c], lo[r * ld_dst + c]);
+    }
+}
+
+// 32x32 tiles through shared memory so both the read and the write are coalesced.
+__global__ void split_transpose_kernel(const float* src, uint64_t ld_src, uint32_t rows,
+                                       uint32_t cols, uint16_t* hi, uint16_t* lo, uint64_t ld_dst) {
+    __shared__ float tile[32][33];
+    const uint32_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const uint32_t r = r0 + j, c = c0 + threadIdx.x;
+        tile[j][threadIdx.x] = (r < rows && c < cols) ? src[static_cast<uint64_t>(r) * ld_src + c] : 0.f;
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const uint32_t c = c0 + j, r = r0 + threadIdx.x;  // dst[c][r]
+        if (c < cols && r < rows)
+            split_bf16(tile[threadIdx.x][j], hi[static_cast<uint64_t>(c) * ld_dst + r],
+                       lo[static_cast<uint64_t>(c) * ld_dst + r]);
+    }
+}
+
+__global__ void transpose_split_kernel(const uint16_t* shi, const uint16_t* slo, uint64_t ld_src,
+                                       uint32_t rows, uint32_t cols, uint16_t* dhi, uint16_t* dlo,
+                                       uint64_t ld_dst) {
+    __shared__ uint16_t th[32][34];
+    __shared__ uint16_t tl[32][34];
+    const uint32_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const uint32_t r = r0 + j, c = c0 + threadIdx.x;
+        const bool ok = r < rows && c < cols;
+        th[j][threadIdx.x] = ok ? shi[static_cast<uint64_t>(r) * ld_src + c] : 0;
+        tl[j][threadIdx.x] = ok ? slo[static_cast<uint64_t>(r) * ld_src + c] : 0;
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const uint32_t c = c0 + j, r = r0 + threadIdx.x;
+        if (c < cols && r < rows) {
+            dhi[static_cast<uint64_t>(c) * ld_dst + r] = th[threadIdx.x][j];
+            dlo[static_cast<uint64_t>(c) * ld_dst + r] = tl[threadIdx.x][j];
+        }
+    }
+}
+
+__global__ void grad_prepare_kernel(const float* dH, uint64_t ld_dh, const float* H, uint64_t ld_h,
+                                    uint32_t rows, uint32_t width, const float* dst_scale,
+                                    float* g_out, uint64_t ld_gout, float* gs, uint64_t ld_gs,
+                                    uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g) {
+    const uint64_t total = static_cast<uint64_t>(rows) * width;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / width, c = i % width;
+        float g = dH[r * ld_dh + c];
+        if (H && !(H[r * ld_h + c] > 0.f)) g = 0.f;
+        if (g_out) g_out[r * ld_gout + c] = g;
+        if (gs) gs[r * ld_gs + c] = dst_scale ? g * dst_scale[r] : g;
+        if (g_hi) split_bf16(g, g_hi[r * ld_g + c], g_lo[r * ld_g + c]);
+    }
+}
+
+// One warp per row; classes <= 32*8.
+__global__ void softmax_xent_kernel(const float* logits, uint64_t ld, uint32_t rows,
+                                    uint32_t classes, const int32_t* labels, float inv_count,
+                                    float* dlogits, uint64_t ld_d, double* loss_sum) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    double local = 0.0;
+    for (uint32_t r = warp; r < rows; r += nwarps) {
+        const float* z = logits + static_cast<uint64_t>(r) * ld;
+        float mx = -INFINITY;
+        for (uint32_t c = lane; c < classes; c += 32) mx = fmaxf(mx, z[c]);
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float sum = 0.f;
+        for (uint32_t c = lane; c < classes; c += 32) sum += expf(z[c] - mx);
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const float lse = mx + logf(sum);
+        const int32_t y = labels[r];
+        for (uint32_t c = lane; c < classes; c += 32) {
+            const float p = expf(z[c] - lse);
+            dlogits[static_cast<uint64_t>(r) * ld_d + c] = (p - (static_cast<int32_t>(c) == y ? 1.f : 0.f)) * inv_count;
+        }
+        if (lane == 0) local += static_cast<double>(lse - z[y]);
+    }
+    if (lane == 0 && local != 0.0) atomicAdd(loss_sum, local);
+}
+
+__global__ void degree_scale_kernel(const uint64_t* row_ptr, uint32_t rows, int kind, float* out) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < rows; v += gridDim.x * blockDim.x) {
+        const double d = static_cast<double>(row_ptr[v + 1] - row_ptr[v]);
+        out[v] = kind == 0 ? (d > 0 ? static_cast<float>(1.0 / d) : 0.f)
+                           : static_cast<float>(1.0 / sqrt(d + 1.0));
+    }
+}
+
+__global__ void splitk_reduce_kernel(const float* ws, uint32_t split_k, uint64_t stride,
+                                     uint32_t rows, uint32_t cols, uint64_t ld, float* out,
+                                     float* w, float lr, uint16_t* w_hi, uint16_t* w_lo) {
+    const uint64_t total = static_cast<uint64_t>(rows) * cols;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / cols, c = i % cols, o = r * ld + c;
+        float acc = 0.f;
+        for (uint32_t z = 0; z < split_k; ++z) acc += ws[z * stride + o];
+        if (out) out[o] = acc;
+        if (w) {
+            const float nw = w[o] - lr * acc;
+            w[o] = nw;
+            if (w_hi) split_bf16(nw, w_hi[o], w_lo[o]);
+        }
+    }
+}
+
+unsigned grid_for(uint64_t total, unsigned block = 256) {
+    uint64_t b = (total + block - 1) / block;
+    const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 16;
+    if (b > cap) b = cap;
+    return static_cast<unsigned>(b ? b : 1);
+}
+
+}  // namespace
+}  // namespace gdx
+
+using namespace gdx;
+
+extern "C" int gdx_init_uniform(uint64_t seed, uint64_t k1, uint64_t k2, uint64_t first_draw,
+                                uint32_t rows, uint32_t cols, double lo, double hi, float* out,
+                                uint64_t ld, gdx_stream stream) {
+    GDX_REQUIRE(out || rows * static_cast<uint64_t>(cols) == 0, GDX_INPUT, "gdx_init_uniform: null out");
+    GDX_REQUIRE(ld >= cols, GDX_INPUT, "gdx_init_uniform: ld < cols");
+    if (!rows || !cols) return GDX_OK;
+    init_uniform_kernel<<<grid_for(static_cast<uint64_t>(rows) * cols), 256, 0, as_cuda(stream)>>>(
+        keyed_state(seed, k1, k2), first_draw, rows, cols, lo, hi, out, ld);
+    note_launch();
+    return check_launch("gdx_init_uniform");
+}
+
+extern "C" int gdx_init_uniform_f64(uint64_t seed, uint64_t k1, uint64_t k2, uint64_t first_draw,
+                                    uint32_t rows, uint32_t cols, double lo, double hi, double* out,
+                                    uint64_t ld, gdx_stream stream) {
+    GDX_REQUIRE(out || rows * static_cast<uint64_t>(cols) == 0, GDX_INPUT, "gdx_init_uniform_f64: null out");
+    GDX_REQUIRE(ld >= cols, GDX_INPUT, "gdx_init_uniform_f64: ld < cols");
+    if (!rows || !cols) return GDX_OK;
+    init_uniform_f64_kernel<<<grid_for(static_cast<uint64_t>(rows) * cols), 256, 0, as_cuda(stream)>>>(
+        keyed_state(seed, k1, k2), first_draw, rows, cols, lo, hi, out, ld);
+    note_launch();
+    return check_launch("gdx_init_uniform_f64");
+}
+
+extern "C" int gdx_init_labels(uint64_t seed, uint64_t base, uint32_t rows, uint32_t classes,
+                               int32_t* out, gdx_stream stream) {
+    GDX_REQUIRE(classes > 0, GDX_INPUT, "gdx_init_labels: classes must be >= 1");
+    if (!rows) return GDX_OK;
+    init_labels_kernel<<<grid_for(rows), 256, 0, as_cuda(stream)>>>(seed, base, rows, classes, out);
+    note_launch();
+    return check_launch("gdx_init_labels");
+}
+
+extern "C" int gdx_split_bf16(const float* src, uint64_t ld_src, uint32_t rows, uint32_t cols,
+                              uint16_t* hi, uint16_t* lo, uint64_t ld_dst, int transpose,
+                              gdx_stream stream) {
+    GDX_REQUIRE(src && hi && lo, GDX_INPUT, "gdx_split_bf16: null pointer");
+    GDX_REQUIRE(ld_src >= cols && ld_dst >= (transpose ? rows : cols), GDX_INPUT,
+                "gdx_split_bf16: leading dimension too small");
+    if (!rows || !cols) return GDX_OK;
+    if (transpose) {
+        dim3 blk(32, 8), grid((cols + 31) / 32, (rows + 31) / 32);
+        split_transpose_kernel<<<grid, blk, 0, as_cuda(stream)>>>(src, ld_src, rows, cols, hi, lo, ld_dst);
+    } else {
+        split_kernel<<<grid_for(static_cast<uint64_t>(rows) * cols), 256, 0, as_cuda(stream)>>>(
+            src, ld_src, rows, cols, hi, lo, ld_dst);
+    }
+    note_launch();
+    return check_launch("gdx_split_bf16");
+}
+
+extern "C" int gdx_transpose_split(const uint16_t* src_hi, const uint16_t* src_lo, uint64_t ld_src,
+                                   uint32_t rows, uint32_t cols, uint16_t* dst_hi, uint16_t* dst_lo,
+                                   uint64_t ld_dst, gdx_stream stream) {
+    GDX_REQUIRE(src_hi && src_lo && dst_hi && dst_lo, GDX_INPUT, "gdx_transpose_split: null pointer");
+    GDX_REQUIRE(ld_src >= cols && ld_dst >= rows, GDX_INPUT, "gdx_transpose_split: leading dimension too small");
+    if (!rows || !cols) return GDX_OK;
+    dim3 blk(32, 8), grid((cols + 31) / 32, (rows + 31) / 32);
+    transpose_split_kernel<<<grid, blk, 0, as_cuda(stream)>>>(src_hi, src_lo, ld_src, rows, cols,
+                                                               dst_hi, dst_lo, ld_dst);
+    note_launch();
+    return check_launch("gdx_transpose_split");
+}
+
+extern "C" int gdx_grad_prepare(const float* dH, uint64_t ld_dh, const float* H, uint64_t ld_h,
+                                uint32_t rows, uint32_t width, const float* dst_scale, float* g_out,
+                                uint64_t ld_gout, float* gs, uint64_t ld_gs, uint16_t* g_hi,
+                                uint16_t* g_lo, uint64_t ld_g, gdx_stream stream) {
+    GDX_REQUIRE(dH, GDX_INPUT, "gdx_grad_prepare: null dH");
+    GDX_REQUIRE(!g_hi == !g_lo, GDX_INPUT, "gdx_grad_prepare: g_hi/g_lo must pair");
+    if (!rows || !width) return GDX_OK;
+    grad_prepare_kernel<<<grid_for(static_cast<uint64_t>(rows) * width), 256, 0, as_cuda(stream)>>>(
+        dH, ld_dh, H, ld_h, rows, width, dst_scale, g_out, ld_gout, gs, ld_gs, g_hi, g_lo, ld_g);
+    note_launch();
+    return check_launch("gdx_grad_prepare");
+}
+
+extern "C" int gdx_softmax_xent(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
+                                const int32_t* labels, float inv_count, float* dlogits,
+                                uint64_t ld_d, double* loss_sum, gdx_stream stream) {
+    GDX_REQUIRE(logits && labels && dlogits && loss_sum, GDX_INPUT, "gdx_softmax_xent: null pointer");
+    GDX_REQUIRE(classes >= 1, GDX_INPUT, "gdx_softmax_xent: classes must be >= 1");
+    if (!rows) return GDX_OK;
+    const uint64_t threads = static_cast<uint64_t>(rows) * 32;
+    softmax_xent_kernel<<<grid_for(threads), 256, 0, as_cuda(stream)>>>(
+        logits, ld, rows, classes, labels, inv_count, dlogits, ld_d, loss_sum);
+    note_launch();
+    return check_launch("gdx_softmax_xent");
+}
+
+extern "C" int gdx_degree_scale(const uint64_t* row_ptr, uint32_t rows, int kind, float* out,
+                                gdx_stream stream) {
+    GDX_REQUIRE(row_ptr && out, GDX_INPUT, "gdx_degree_scale: null pointer");
+    if (!rows) return GDX_OK;
+    degree_scale_kernel<<<grid_for(rows), 256, 0, as_cuda(stream)>>>(row_ptr, rows, kind, out);
+    note_launch();
+    return check_launch("gdx_degree_scale");
+}
+
+extern "C" int gdx_splitk_reduce(const float* ws, uint32_t split_k, uint64_t stride, uint32_t rows,
+                                 uint32_t cols, uint64_t ld, float* out, float* w, float lr,
+                                 uint16_t* w_hi, uint16_t* w_lo, gdx_stream stream) {
+    GDX_REQUIRE(ws && split_k >= 1, GDX_INPUT, "gdx_splitk_reduce: bad workspace");
+    GDX_REQUIRE(!w_hi == !w_lo, GDX_INPUT, "gdx_splitk_reduce: w_hi/w_lo must pair");
+    if (!rows || !cols) return GDX_OK;
+    splitk_reduce_kernel<<<grid_for(static_cast<uint64_t>(rows) * cols), 256, 0, as_cuda(stream)>>>(
+        ws, split_k, stride, rows, cols, ld, out, w, lr, w_hi, w_lo);
+    note_launch();
+    return check_launch("gdx_splitk_reduce");
+}

@@ -1,0 +1,163 @@
+// host.cpp -- host-side C++ of libgdx: error plumbing, launch accounting and
+// the host preprocessing that stays on the CPU: the
+// G(n,p) generator and the random partition, parallelised with OpenMP and
+// bit-identical to the reference.
+//
+// gen_random_graph (graph.cpp:137-154) keys every vertex's stream by
+// (seed, u), so vertices can be sampled in any order.  assemble_undirected
+// (graph.cpp:116-132) produces rows sorted ascending without a sort pass; the
+// parallel fill appends with atomic cursors and then sorts each row, which
+// yields the identical CSR because every row is a set of distinct ids.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "gdx.h"
+
+namespace gdx {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
+inline uint64_t fin(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+inline uint64_t mix64(uint64_t x) { return fin(x + kGamma); }
+
+// rng.hpp:18-52 KeyedRng
+struct Stream {
+    uint64_t s;
+    Stream(uint64_t seed, uint64_t k1, uint64_t k2) {
+        s = mix64(seed);
+        s = mix64(s ^ (k1 + kGamma));
+        s = mix64(s ^ (k2 + 0xc2b2ae3d27d4eb4fULL));
+    }
+    uint64_t next() {
+        s += kGamma;
+        return fin(s);
+    }
+    double unit() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+    uint64_t below(uint64_t n) {
+        return static_cast<uint64_t>((static_cast<unsigned __int128>(next()) * n) >> 64);
+    }
+};
+
+// graph.cpp:86-94
+inline uint64_t geometric_skip(Stream& r, double p, double log1mp) {
+    if (p >= 1.0) return 0;
+    double u = r.unit();
+    if (u <= 0.0) u = 0x1.0p-53;
+    double skip = std::floor(std::log(u) / log1mp);
+    if (skip < 0.0) skip = 0.0;
+    if (skip > 1e18) skip = 1e18;
+    return static_cast<uint64_t>(skip);
+}
+
+// graph.cpp:99-111, for one u
+template <class Emit>
+void sample_range(uint64_t seed, uint32_t u, uint32_t start, uint32_t limit, double p, Emit&& emit) {
+    if (p <= 0.0 || start >= limit) return;
+    Stream r(seed, u, 0);
+    const double log1mp = (p < 1.0) ? std::log1p(-p) : 0.0;
+    uint64_t v = start + geometric_skip(r, p, log1mp);
+    while (v < limit) {
+        emit(static_cast<uint32_t>(v));
+        v += 1 + geometric_skip(r, p, log1mp);
+    }
+}
+
+double edge_probability(uint32_t n, double d) {
+    double p = d / static_cast<double>(n - 1);
+    return p > 1.0 ? 1.0 : p;
+}
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(GDX_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
+    return GDX_OK;
+}
+
+}  // namespace gdx
+
+using namespace gdx;
+
+extern "C" const char* gdx_last_error(void) { return g_last_error.c_str(); }
+extern "C" int gdx_version(void) { return 1; }
+extern "C" uint64_t gdx_launch_count(void) { return g_launches.load(); }
+
+extern "C" uint64_t gdx_host_gen_random_graph_count(uint32_t n, double d, uint64_t seed,
+                                                    uint64_t* ro) {
+    if (n == 0 || d < 0.0 || d >= static_cast<double>(n) || !ro) {
+        fail(GDX_INPUT, "gen_random_graph: need n >= 1 and 0 <= avg_degree < n");
+        return ~0ull;
+    }
+    std::memset(ro, 0, sizeof(uint64_t) * (static_cast<size_t>(n) + 1));
+    if (n == 1 || d == 0.0) return 0;
+    const double p = edge_probability(n, d);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t uu = 0; uu < static_cast<int64_t>(n) - 1; ++uu) {
+        const uint32_t u = static_cast<uint32_t>(uu);
+        uint64_t mine = 0;
+        sample_range(seed, u, u + 1, n, p, [&](uint32_t v) {
+            ++mine;
+            __atomic_fetch_add(&ro[v + 1], 1, __ATOMIC_RELAXED);
+        });
+        __atomic_fetch_add(&ro[u + 1], mine, __ATOMIC_RELAXED);
+    }
+    for (uint32_t i = 0; i < n; ++i) ro[i + 1] += ro[i];
+    return ro[n];
+}
+
+extern "C" int gdx_host_gen_random_graph_fill(uint32_t n, double d, uint64_t seed,
+                                              const uint64_t* ro, uint32_t* cols) {
+    if (n == 0 || d < 0.0 || d >= static_cast<double>(n) || !ro)
+        return fail(GDX_INPUT, "gen_random_graph: need n >= 1 and 0 <= avg_degree < n");
+    if (n == 1 || d == 0.0 || ro[n] == 0) return GDX_OK;
+    const double p = edge_probability(n, d);
+    std::vector<uint64_t> cursor(ro, ro + n);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t uu = 0; uu < static_cast<int64_t>(n) - 1; ++uu) {
+        const uint32_t u = static_cast<uint32_t>(uu);
+        sample_range(seed, u, u + 1, n, p, [&](uint32_t v) {
+            cols[__atomic_fetch_add(&cursor[u], 1, __ATOMIC_RELAXED)] = v;
+            cols[__atomic_fetch_add(&cursor[v], 1, __ATOMIC_RELAXED)] = u;
+        });
+    }
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t v = 0; v < static_cast<int64_t>(n); ++v) std::sort(cols + ro[v], cols + ro[v + 1]);
+    return GDX_OK;
+}
+
+// partition.cpp:51-61
+extern "C" int gdx_host_partition_random(uint32_t n, uint32_t parts, uint64_t seed,
+                                         uint32_t* assignment) {
+    if (parts == 0) return fail(GDX_INPUT, "partition: parts must be >= 1");
+    if (parts > n)
+        return fail(GDX_INPUT, "partition: parts (" + std::to_string(parts) +
+                                   ") exceeds vertex count (" + std::to_string(n) + ")");
+    std::vector<uint32_t> perm(n);
+    std::iota(perm.begin(), perm.end(), 0u);
+    Stream r(seed, 0x7061727469ULL, 0);
+    for (uint64_t i = n; i > 1; --i) std::swap(perm[i - 1], perm[r.below(i)]);
+    for (uint32_t i = 0; i < n; ++i) assignment[perm[i]] = i % parts;
+    return GDX_OK;
+}

@@ -1,0 +1,148 @@
+"""Device-side data layout and thin wrappers over the libgdx kernels.
+
+PyTorch is used only as the device allocator / stream provider: tensors are
+raw HBM buffers whose pointers are handed to the C ABI.  Layout rules:
+
+* CSR: row_ptr int64[rows+1] (u64 offsets), col int32[nnz] (u32 ids);
+* fp32 dense matrices: row pitch padded to a multiple of 4 (16-byte rows);
+* split-bf16 GEMM operands: hi/lo int16 arrays, row pitch padded to a
+  multiple of 8 (16-byte TMA pitch), zero-filled padding.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import AggregateArgs, GemmArgs, call, ptr
+from .errors import InternalError
+
+
+def pad4(x: int) -> int:
+    return (x + 3) // 4 * 4
+
+
+def pad8(x: int) -> int:
+    return (x + 7) // 8 * 8
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise InternalError("no CUDA device visible: the B200 engine has no CPU fallback")
+
+
+def stream_handle(stream=None) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+@dataclass
+class DeviceCSR:
+    row_ptr: torch.Tensor  # int64 [rows+1]
+    col: torch.Tensor      # int32 [nnz]
+    rows: int
+
+    @staticmethod
+    def upload(ro: np.ndarray, ci: np.ndarray, device) -> "DeviceCSR":
+        require_cuda()
+        rp = torch.from_numpy(np.ascontiguousarray(ro).view(np.int64)).to(device, non_blocking=False)
+        c = torch.from_numpy(np.ascontiguousarray(ci).view(np.int32) if len(ci) else
+                             np.zeros(1, np.int32)).to(device)
+        return DeviceCSR(rp, c, len(ro) - 1)
+
+    def slice_rows(self, lo: int, hi: int) -> "DeviceCSR":
+        """Rows [lo, hi): offsets stay absolute into the same col array."""
+        return DeviceCSR(self.row_ptr[lo:hi + 1], self.col, hi - lo)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1].item() - self.row_ptr[0].item())
+
+
+class Split:
+    """Split-bf16 matrix (x = hi + lo) with rows x cols logical shape, pitch ld."""
+
+    def __init__(self, rows: int, cols: int, device, ld: int | None = None):
+        self.rows, self.cols = rows, cols
+        self.ld = pad8(cols) if ld is None else ld
+        self.hi = torch.zeros(max(rows, 1) * self.ld, dtype=torch.int16, device=device)
+        self.lo = torch.zeros(max(rows, 1) * self.ld, dtype=torch.int16, device=device)
+
+    def to_float(self) -> torch.Tensor:
+        """fp32 value (for tests): hi + lo."""
+        def f(t):
+            return (t.view(self.rows if self.rows else 1, self.ld)[:self.rows, :self.cols]
+                    .to(torch.int32).bitwise_left_shift(16).view(torch.float32))
+        return f(self.hi) + f(self.lo)
+
+    def fill_from(self, x: torch.Tensor, ld_x: int, transpose: bool = False, stream=None):
+        """hi/lo := split(x) (x: fp32, logical rows x cols if not transpose, else cols x rows)."""
+        if transpose:
+            call("gdx_split_bf16", x.data_ptr(), ld_x, self.cols, self.rows, self.hi.data_ptr(),
+                 self.lo.data_ptr(), self.ld, 1, stream_handle(stream))
+        else:
+            call("gdx_split_bf16", x.data_ptr(), ld_x, self.rows, self.cols, self.hi.data_ptr(),
+                 self.lo.data_ptr(), self.ld, 0, stream_handle(stream))
+        return self
+
+
+def dense(rows: int, cols: int, device, zero: bool = True) -> torch.Tensor:
+    """fp32 matrix storage with a 16-byte row pitch; returns a [rows, pad4(cols)] tensor."""
+    f = torch.zeros if zero else torch.empty
+    return f((max(rows, 1), pad4(cols)), dtype=torch.float32, device=device)
+
+
+def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_split: Split | None = None,
+              self_coef: float = 0.0, self_base: int = 0, post_scale=None, add=None, relu=False,
+              row_end=None, stream=None):
+    """K1/K3 (see include/gdx.h gdx_aggregate)."""
+    a = AggregateArgs()
+    a.row_ptr = g.row_ptr.data_ptr()
+    a.row_end = ptr(row_end)
+    a.col = g.col.data_ptr()
+    a.rows = g.rows
+    a.width = width
+    a.src = src.data_ptr()
+    a.ld_src = src.shape[-1] if src.dim() == 2 else width
+    a.self_coef = self_coef
+    a.self_base = self_base
+    a.post_scale = ptr(post_scale)
+    a.add = ptr(add)
+    a.ld_add = add.shape[-1] if add is not None else 0
+    a.relu = int(relu)
+    a.out = ptr(out)
+    a.ld_out = out.shape[-1] if out is not None else 0
+    if out_split is not None:
+        a.out_hi, a.out_lo, a.ld_split = out_split.hi.data_ptr(), out_split.lo.data_ptr(), out_split.ld
+    call("gdx_aggregate", _lib.C.byref(a), stream_handle(stream))
+
+
+def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None, relu=False,
+            out_split: Split | None = None, split_k: int = 1, m=None, simt=False, stream=None):
+    """K2: C = A . B^T over the shared k = A.cols (see gdx_gemm_tn)."""
+    assert A.cols == B.cols, (A.cols, B.cols)
+    g = GemmArgs()
+    g.a_hi, g.a_lo, g.lda = A.hi.data_ptr(), A.lo.data_ptr(), A.ld
+    g.b_hi, g.b_lo, g.ldb = B.hi.data_ptr(), B.lo.data_ptr(), B.ld
+    g.m = A.rows if m is None else m
+    g.n = B.rows
+    g.k = A.cols
+    g.c0 = ptr(c0)
+    g.ldc0 = c0.shape[-1] if c0 is not None else 0
+    g.c1 = ptr(c1)
+    g.ldc1 = c1.shape[-1] if c1 is not None else 0
+    g.split = B.rows if split is None else split
+    g.row_scale = ptr(row_scale)
+    g.relu = int(relu)
+    if out_split is not None:
+        g.out_hi, g.out_lo, g.ld_split = out_split.hi.data_ptr(), out_split.lo.data_ptr(), out_split.ld
+    g.split_k = split_k
+    call("gdx_gemm_tn_simt" if simt else "gdx_gemm_tn", _lib.C.byref(g), stream_handle(stream))
+
+
+def degree_scale(g: DeviceCSR, kind: int, device) -> torch.Tensor:
+    out = torch.empty(max(g.rows, 1), dtype=torch.float32, device=device)
+    call("gdx_degree_scale", g.row_ptr.data_ptr(), g.rows, kind, out.data_ptr(), stream_handle())
+    return out

@@ -1,0 +1,93 @@
+"""CPU-only checks of the drop-in boundary: libgdx.so loads and exports every
+entry point include/gdx.h declares; host preprocessing entry points are
+bit-identical to the reference; error codes map to the reference taxonomy."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "gdx.h")).read()
+    return sorted(set(re.findall(r"\b(gdx_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2311_06837_b200 import _lib
+    L = _lib.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+    bound = set(_lib._SIGS)
+    assert set(syms) <= bound, sorted(set(syms) - bound)
+
+
+def test_version_and_error_channel():
+    from paper_2311_06837_b200 import _lib
+    from paper_2311_06837_b200.errors import InputError
+    assert _lib.lib().gdx_version() >= 1
+    with pytest.raises(InputError):
+        _lib.call("gdx_host_partition_random", 3, 0, 1, None)
+    assert b"parts must be >= 1" in _lib.lib().gdx_last_error()
+
+
+@pytest.mark.parametrize("n,d,seed", [(1, 0.0, 1), (2, 1.0, 3), (50, 5.0, 71), (10000, 10.0, 7),
+                                      (3000, 250.0, 11)])
+def test_host_generator_bit_exact(n, d, seed):
+    import oracle as O
+    import paper_2311_06837_b200 as G
+    g = G.gen_random_graph(n, d, seed)
+    c = O.gen_random_graph(n, d, seed)
+    assert np.array_equal(g.row_offsets(), c.row_offsets)
+    assert np.array_equal(g.col_indices(), c.cols)
+
+
+def test_host_generator_errors():
+    import paper_2311_06837_b200 as G
+    with pytest.raises(G.InputError):
+        G.gen_random_graph(0, 1.0, 1)
+    with pytest.raises(G.InputError):
+        G.gen_random_graph(10, 10.0, 1)
+
+
+@pytest.mark.parametrize("n,parts,seed", [(10, 3, 1), (1000, 8, 5), (7, 7, 2)])
+def test_host_partition_random_bit_exact(n, parts, seed):
+    import oracle as O
+    import paper_2311_06837_b200 as G
+    g = G.Graph(n, np.zeros(n + 1, np.uint64), np.zeros(0, np.uint32))
+    assert np.array_equal(G.partition_random(g, parts, seed).assignment, O.partition_random(n, parts, seed))
+
+
+def test_from_edges_matches_reference_rules():
+    import oracle as O
+    import paper_2311_06837_b200 as G
+    edges = [(0, 1), (1, 0), (2, 2), (3, 1), (0, 1), (4, 2)]
+    g = G.Graph.from_edges(edges, 5)
+    c = O.from_edges(edges, 5)
+    assert np.array_equal(g.row_offsets(), c.row_offsets) and np.array_equal(g.col_indices(), c.cols)
+    with pytest.raises(G.InputError):
+        G.Graph.from_edges([(0, 9)], 5)
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2311_06837_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "granndis_oracle" not in src, f
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    from paper_2311_06837_b200 import _lib
+    from paper_2311_06837_b200.errors import InternalError
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "nope.so"))
+    with pytest.raises(InternalError):
+        _lib.lib()

@@ -1,0 +1,159 @@
+"""GPU parity of the individual kernels through the C ABI (K1 aggregate, K2 tcgen05
+GEMM, K7 init) against fp64 / exact references.  Tolerance: |a-b| <= 1e-4 (|b| + rms(b))."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def close(a, b, tol=TOL):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    rms = float(np.sqrt(np.mean(b * b))) if b.size else 0.0
+    err = np.abs(a - b) - tol * (np.abs(b) + rms)
+    worst = float(err.max()) if err.size else -1.0
+    assert worst <= 0.0, f"max excess {worst:.3e} (rms {rms:.3e})"
+
+
+@pytest.fixture(scope="module")
+def gdx(cuda):
+    import torch
+    from paper_2311_06837_b200 import device as D
+    torch.manual_seed(0)
+    return D
+
+
+def _split(D, x, cuda):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(cuda)
+    s = D.Split(x.shape[0], x.shape[1], cuda)
+    return s.fill_from(t, x.shape[1])
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 8, 16), (128, 64, 64), (300, 128, 602), (1000, 41, 64),
+                                   (257, 96, 128), (64, 608, 200), (4000, 128, 608), (129, 256, 1000)])
+def test_gemm_tcgen05_matches_fp64(gdx, cuda, m, n, k):
+    import torch
+    rng = np.random.default_rng(m * 7 + n + k)
+    a = rng.uniform(-0.5, 0.5, (m, k))
+    b = rng.uniform(-0.5, 0.5, (n, k))
+    A, B = _split(gdx, a, cuda), _split(gdx, b, cuda)
+    c = gdx.dense(m, n, cuda)
+    gdx.gemm_tn(A, B, c0=c)
+    torch.cuda.synchronize()
+    ref = a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T
+    close(c[:m, :n].double().cpu().numpy(), ref)
+
+
+def test_gemm_epilogue_split_scale_relu(gdx, cuda):
+    import torch
+    rng = np.random.default_rng(5)
+    m, n, k = 333, 128, 96
+    a = rng.uniform(-1, 1, (m, k))
+    b = rng.uniform(-1, 1, (n, k))
+    scale = rng.uniform(0.1, 2.0, m).astype(np.float32)
+    A, B = _split(gdx, a, cuda), _split(gdx, b, cuda)
+    c0, c1 = gdx.dense(m, 64, cuda), gdx.dense(m, 64, cuda)
+    sp = gdx.Split(m, n, cuda)
+    sc = torch.from_numpy(scale).to(cuda)
+    gdx.gemm_tn(A, B, c0=c0, c1=c1, split=64, row_scale=sc, relu=True, out_split=sp)
+    torch.cuda.synchronize()
+    ref = np.maximum((a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T)
+                     * scale[:, None], 0)
+    close(c0[:m, :64].double().cpu().numpy(), ref[:, :64])
+    close(c1[:m, :64].double().cpu().numpy(), ref[:, 64:])
+    close(sp.to_float().double().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("split_k", [2, 7])
+def test_gemm_splitk_reduce(gdx, cuda, split_k):
+    import torch
+    from paper_2311_06837_b200._lib import call
+    rng = np.random.default_rng(split_k)
+    m, n, k = 128, 64, 5000
+    a = rng.uniform(-1, 1, (m, k))
+    b = rng.uniform(-1, 1, (n, k))
+    A, B = _split(gdx, a, cuda), _split(gdx, b, cuda)
+    ws = torch.zeros(split_k * m * 64, dtype=torch.float32, device=cuda).view(split_k * m, 64)
+    gdx.gemm_tn(A, B, c0=ws, split_k=split_k)
+    out = gdx.dense(m, n, cuda)
+    call("gdx_splitk_reduce", ws.data_ptr(), split_k, m * 64, m, n, 64, out.data_ptr(), None, 0.0,
+         None, None, gdx.stream_handle())
+    torch.cuda.synchronize()
+    ref = a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T
+    close(out[:m, :n].double().cpu().numpy(), ref)
+
+
+def _rand_csr(n, deg, seed):
+    import oracle as O
+    return O.gen_random_graph(n, deg, seed)
+
+
+@pytest.mark.parametrize("width", [1, 3, 4, 8, 12, 41, 44, 64, 128, 130, 256, 602])
+def test_aggregate_widths(gdx, cuda, width):
+    import torch
+    from paper_2311_06837_b200.device import DeviceCSR
+    g = _rand_csr(700, 9.0, width)
+    rng = np.random.default_rng(width)
+    x = rng.uniform(-1, 1, (g.n, width)).astype(np.float32)
+    add = rng.uniform(-1, 1, (g.n, width)).astype(np.float32)
+    scale = rng.uniform(0.5, 1.5, g.n).astype(np.float32)
+    dg = DeviceCSR.upload(g.row_offsets, g.cols, cuda)
+    X = gdx.dense(g.n, width, cuda)
+    X[:, :width] = torch.from_numpy(x).to(cuda)
+    Add = gdx.dense(g.n, width, cuda)
+    Add[:, :width] = torch.from_numpy(add).to(cuda)
+    out = gdx.dense(g.n, width, cuda)
+    sp = gdx.Split(g.n, width, cuda)
+    gdx.aggregate(dg, X, width, out=out, out_split=sp, self_coef=1.0,
+                  post_scale=torch.from_numpy(scale).to(cuda), add=Add, relu=True)
+    torch.cuda.synchronize()
+    ro, ci = g.row_offsets.astype(np.int64), g.cols.astype(np.int64)
+    xd = x.astype(np.float64)
+    ref = xd.copy()
+    for v in range(g.n):
+        ref[v] += xd[ci[ro[v]:ro[v + 1]]].sum(0)
+    ref = np.maximum(ref * scale[:, None] + add, 0)
+    close(out[:, :width].double().cpu().numpy(), ref)
+    close(sp.to_float().double().cpu().numpy(), ref)
+
+
+def test_aggregate_slice_and_self_base(gdx, cuda):
+    """Owned-row slice [lo, hi) with the self term taken at self_base + row (multi-GPU layout)."""
+    import torch
+    from paper_2311_06837_b200.device import DeviceCSR
+    g = _rand_csr(500, 12.0, 3)
+    x = np.random.default_rng(1).uniform(-1, 1, (g.n, 64)).astype(np.float32)
+    dg = DeviceCSR.upload(g.row_offsets, g.cols, cuda)
+    X = torch.from_numpy(x).to(cuda)
+    lo, hi = 123, 377
+    out = gdx.dense(hi - lo, 64, cuda)
+    gdx.aggregate(dg.slice_rows(lo, hi), X, 64, out=out, self_coef=1.0, self_base=lo)
+    torch.cuda.synchronize()
+    ro, ci = g.row_offsets.astype(np.int64), g.cols.astype(np.int64)
+    ref = np.stack([x[v].astype(np.float64) + x[ci[ro[v]:ro[v + 1]]].astype(np.float64).sum(0)
+                    for v in range(lo, hi)])
+    close(out[:, :64].double().cpu().numpy(), ref)
+
+
+def test_init_streams_bit_exact(cuda):
+    import oracle as O
+    from paper_2311_06837_b200 import make_features, make_layer_weights
+    assert np.array_equal(make_features(313, 7, 9), O.make_features(313, 7, 9))
+    ws = make_layer_weights(3, 5, 4, 77)
+    wo = O.make_layer_weights(3, 5, 4, 77)
+    for a, b in zip(ws, wo):
+        assert np.array_equal(a, b)
+
+
+def test_labels_bit_exact(cuda):
+    import torch
+    import oracle as O
+    from paper_2311_06837_b200._lib import call
+    from paper_2311_06837_b200.device import stream_handle
+    out = torch.empty(5000, dtype=torch.int32, device=cuda)
+    call("gdx_init_labels", 11, 0, 5000, 41, out.data_ptr(), stream_handle())
+    assert np.array_equal(out.cpu().numpy(), O.make_labels(5000, 41, 11))
