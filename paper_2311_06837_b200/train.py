@@ -1,0 +1,386 @@
+"""Full-graph GNN training on the B200 engine (the training extension of the
+reference's layer model).
+
+One process per GPU.  Rank r owns the contiguous row block [lo, hi) of the
+vertex set (the graph's rows, its labels and its input features); every
+layer is
+
+  forward   Z_loc = H_loc W^T            (K2 tcgen05 GEMM; GCN row scale fused)
+            all-gather Z -> Z_full        (NCCL over NVLink; the a13 exchange)
+            H'_loc = act(agg(Z_full))     (K1; self term, degree scale, SAGE self
+                                           path, ReLU and the split-bf16 copy fused)
+  backward  g = dH * relu'(H') -> split G, gs = scaled g   (elementwise)
+            all-gather gs -> gs_full
+            dZ_loc = agg^T(gs_full)       (K3 = K1 on the symmetric CSR)
+            dH_loc = G W                  (K2)
+            dW = G^T H (split-K over rows) (K2) -> all-reduce -> SGD (fused reduce)
+
+Models (no bias; dims[0] = features, dims[-1] = classes, ReLU between layers):
+  'sum'  : P = W (H_v + sum_u H_u)                  (reference_gnn.cpp:64-89)
+  'gcn'  : P = W s_v (s_v H_v + sum_u s_u H_u), s = (deg+1)^-1/2
+  'sage' : P = W_s H_v + W_n mean_u H_u             (GraphSAGE-mean)
+Loss: mean softmax cross-entropy over all vertices; SGD.  Parity is against the
+fp64 oracle restatement (parity unpinned: no reference implementation exists).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call
+from .device import DeviceCSR, Split, aggregate, dense, gemm_tn, pad4, pad8, require_cuda, stream_handle
+from .errors import InputError
+from .gnn import FEAT_TAG, WEIG_TAG
+from .graph import Graph, partition_contiguous
+
+LABEL_SEED_DEFAULT = 0x6c61626c
+
+
+@dataclass
+class ModelConfig:
+    kind: str = "sage"              # 'sage' | 'gcn' | 'sum'
+    dims: list = field(default_factory=lambda: [602, 64, 64, 41])
+    lr: float = 0.1
+
+    @property
+    def layers(self) -> int:
+        return len(self.dims) - 1
+
+    @property
+    def classes(self) -> int:
+        return self.dims[-1]
+
+    def weight_shapes(self):
+        """Reference-order weight list: per layer W (sum/gcn) or W_self, W_neigh (sage)."""
+        out = []
+        for l in range(self.layers):
+            out.append((self.dims[l + 1], self.dims[l]))
+            if self.kind == "sage":
+                out.append((self.dims[l + 1], self.dims[l]))
+        return out
+
+
+def init_weights(cfg: ModelConfig, seed: int) -> list:
+    """Consecutive U(-.5,.5) draws of stream (seed, "weig") in weight_shapes order
+    (the make_layer_weights stream, reference_gnn.cpp:18-32, extended to SAGE)."""
+    require_cuda()
+    d = torch.device("cuda", torch.cuda.current_device())
+    ws, first = [], 0
+    for (o, i) in cfg.weight_shapes():
+        t = torch.empty(o * i, dtype=torch.float64, device=d)
+        call("gdx_init_uniform_f64", seed, WEIG_TAG, 0, first, o, i, -0.5, 0.5, t.data_ptr(), i,
+             stream_handle())
+        ws.append(t.cpu().numpy().reshape(o, i))
+        first += o * i
+    return ws
+
+
+class _Layer:
+    """Device state of one layer: W_cat (fp32 master + split copies), buffers."""
+
+    def __init__(self, kind, fin, fout, nloc, nfull, d, splitk_target, first):
+        self.kind, self.fin, self.fout = kind, fin, fout
+        self.k = fin if first else pad4(fin)      # GEMM K: the input operand's logical width
+        self.w = pad4(fout)                       # aggregation width (16 B rows)
+        self.nz = 2 * self.w if kind == "sage" else self.w   # GEMM N (W_cat rows)
+        self.fin_ld = pad8(fin)
+        # master weights, row pitch == split pitch so the fused SGD can index both
+        self.W = torch.zeros((self.nz, self.fin_ld), dtype=torch.float32, device=d)
+        self.Wsp = Split(self.nz, self.k, d, ld=self.fin_ld)  # forward B   (nz x k)
+        self.WTsp = Split(fin, self.nz, d)                    # backward B  (fin x nz)
+        self.dW = torch.zeros((self.nz, self.fin_ld), dtype=torch.float32, device=d)
+        kb = max(1, math.ceil(nloc / 64))
+        ntiles = max(1, math.ceil(fin / (256 if fin > 128 else (128 if fin > 64 else 64))))
+        self.split_k = max(1, min(kb, splitk_target // ntiles))
+        self.ws = torch.zeros((self.split_k * self.nz, self.fin_ld), dtype=torch.float32, device=d)
+        # activations
+        self.S = dense(nloc, self.w, d) if kind == "sage" else None     # SAGE self path
+        self.Zfull = dense(nfull, self.w, d)                             # gathered rows
+        self.Hout = dense(nloc, self.w, d)                               # act output fp32
+        self.Hsp = Split(nloc, self.w, d)                                # next layer's A
+        self.G = Split(nloc, self.nz, d)                                 # [dP | dZn] or dZ
+        self.GT = Split(self.nz, nloc, d)
+        self.dfull = dense(nfull, self.w, d)                             # gathered grads
+
+    def set_weights(self, mats):
+        """mats: [W] or [W_self, W_neigh] (fout x fin each), fp64 numpy."""
+        self.W.zero_()
+        if self.kind == "sage":
+            ws, wn = mats
+            self.W[:self.fout, :self.fin] = torch.from_numpy(ws.astype(np.float32))
+            self.W[self.w:self.w + self.fout, :self.fin] = torch.from_numpy(wn.astype(np.float32))
+        else:
+            self.W[:self.fout, :self.fin] = torch.from_numpy(mats[0].astype(np.float32))
+        self.refresh_splits()
+
+    def refresh_splits(self):
+        self.Wsp.fill_from(self.W, self.fin_ld)
+        self.WTsp.fill_from(self.W, self.fin_ld, transpose=True)
+
+    def get_weights(self):
+        W = self.W.double().cpu().numpy()
+        if self.kind == "sage":
+            return [W[:self.fout, :self.fin].copy(), W[self.w:self.w + self.fout, :self.fin].copy()]
+        return [W[:self.fout, :self.fin].copy()]
+
+
+class FullGraphTrainer:
+    """Data-parallel-over-rows full-graph trainer (one instance per rank/GPU).
+
+    pg: torch.distributed process group (None for a single GPU).  The graph is
+    host-resident on every rank (generation is deterministic); each rank uploads
+    only its own rows.
+    """
+
+    def __init__(self, g: Graph, cfg: ModelConfig, *, rank: int = 0, world: int = 1,
+                 feature_seed: int = 1, label_seed: int = 2, weights=None, weight_seed: int = 3,
+                 pg=None, device=None):
+        require_cuda()
+        if cfg.kind not in ("sage", "gcn", "sum"):
+            raise InputError(f"unknown model kind {cfg.kind!r}")
+        if cfg.classes > 256:
+            raise InputError("classes must be <= 256")
+        self.g, self.cfg, self.rank, self.world, self.pg = g, cfg, rank, world, pg
+        self.d = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        d = self.d
+        n = g.num_vertices()
+        part = partition_contiguous(n, world)
+        sizes = part.part_sizes.astype(np.int64)
+        self.offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        self.lo, self.hi = int(self.offsets[rank]), int(self.offsets[rank + 1])
+        self.nloc = self.hi - self.lo
+        self.n = n
+        self.equal_blocks = bool(np.all(sizes == sizes[0]))
+        # local CSR rows [lo, hi) with global column ids
+        ro = g.row_offsets()
+        base = int(ro[self.lo])
+        lro = (ro[self.lo:self.hi + 1] - np.uint64(base)).astype(np.uint64)
+        lci = g.col_indices()[base:int(ro[self.hi])]
+        self.csr = DeviceCSR.upload(lro, lci, d)
+        self.nnz_local = len(lci)
+        deg = np.diff(lro).astype(np.float64)
+        self.inv_deg = torch.from_numpy(np.where(deg > 0, 1.0 / np.maximum(deg, 1), 0.0)
+                                        .astype(np.float32)).to(d)
+        self.gcn_s = torch.from_numpy((1.0 / np.sqrt(deg + 1.0)).astype(np.float32)).to(d)
+        # inputs: features of owned rows (stream (feature_seed, "feat") row-major over all
+        # vertices, so row v starts at draw v*F), labels of owned rows
+        F = cfg.dims[0]
+        self.F = F
+        self.X = dense(self.nloc, F, d)
+        call("gdx_init_uniform", feature_seed, FEAT_TAG, 0, self.lo * F, self.nloc, F, -0.5, 0.5,
+             self.X.data_ptr(), self.X.shape[1], stream_handle())
+        self.labels = torch.empty(max(self.nloc, 1), dtype=torch.int32, device=d)
+        call("gdx_init_labels", label_seed, self.lo, self.nloc, cfg.classes, self.labels.data_ptr(),
+             stream_handle())
+        self.Xsp = Split(self.nloc, F, d)
+        self.XTsp = Split(F, self.nloc, d)
+        self._refresh_input_splits()
+        # layers
+        sm = torch.cuda.get_device_properties(d).multi_processor_count
+        self.layers = []
+        for l in range(cfg.layers):
+            self.layers.append(_Layer(cfg.kind, cfg.dims[l], cfg.dims[l + 1], self.nloc, n, d, 2 * sm,
+                                      l == 0))
+        if weights is None:
+            weights = init_weights(cfg, weight_seed)
+        self.set_weights(weights)
+        self.dlogits = dense(self.nloc, self.layers[-1].w, d)
+        self.dH = [dense(self.nloc, pad4(cfg.dims[l]), d) for l in range(cfg.layers)]
+        self.loss_acc = torch.zeros(1, dtype=torch.float64, device=d)
+        self.keep_activations = False
+        self.activations = []
+        torch.cuda.synchronize(d)
+
+    # ---- state ----
+    def _refresh_input_splits(self):
+        self.Xsp.fill_from(self.X, self.X.shape[1])
+        self.XTsp.fill_from(self.X, self.X.shape[1], transpose=True)
+
+    def set_weights(self, weights):
+        k = 2 if self.cfg.kind == "sage" else 1
+        for l, layer in enumerate(self.layers):
+            layer.set_weights(weights[k * l:k * l + k])
+
+    def get_weights(self):
+        out = []
+        for layer in self.layers:
+            out.extend(layer.get_weights())
+        return out
+
+    def load_features(self, x_host: torch.Tensor, labels_host: torch.Tensor | None = None):
+        """H2D of this rank's feature rows (pinned host fp32, nloc x F) and labels."""
+        self.X[:self.nloc, :self.F].copy_(x_host, non_blocking=True)
+        if labels_host is not None:
+            self.labels[:self.nloc].copy_(labels_host, non_blocking=True)
+        self._refresh_input_splits()
+
+    # ---- kernel instrumentation (bench roofline) ----
+    def enable_kernel_events(self, on: bool):
+        self._events = [] if on else None
+
+    def _agg(self, csr, src, width, **kw):
+        ev = getattr(self, "_events", None)
+        if ev is None:
+            return aggregate(csr, src, width, **kw)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        aggregate(csr, src, width, **kw)
+        b.record()
+        nnz, rows = self.nnz_local, csr.rows
+        ev.append((a, b, 4 * nnz + 8 * (rows + 1) + 4 * width * nnz + 4 * width * rows))
+
+    def kernel_event_summary(self):
+        """(total ms, launches, algorithmic bytes) of the instrumented aggregations."""
+        torch.cuda.synchronize()
+        ev = getattr(self, "_events", None) or []
+        return (sum(a.elapsed_time(b) for a, b, _ in ev), len(ev), sum(x for _, _, x in ev))
+
+    # ---- collectives ----
+    def _allgather_rows(self, full: torch.Tensor):
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        if self.equal_blocks:
+            local = full[self.lo:self.hi]
+            dist.all_gather_into_tensor(full[:self.n], local, group=self.pg)
+        else:
+            chunks = [full[int(self.offsets[r]):int(self.offsets[r + 1])] for r in range(self.world)]
+            dist.all_gather(chunks, chunks[self.rank].clone(), group=self.pg)
+
+    def _allreduce(self, t: torch.Tensor):
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        dist.all_reduce(t, group=self.pg)
+
+    # ---- one epoch ----
+    def forward(self):
+        cfg = self.cfg
+        A = self.Xsp
+        acts = []
+        for l, L in enumerate(self.layers):
+            relu = l + 1 < cfg.layers
+            own = L.Zfull[self.lo:self.hi]
+            if cfg.kind == "sage":
+                gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w)
+            elif cfg.kind == "gcn":
+                gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s)
+            else:
+                gemm_tn(A, L.Wsp, c0=own)
+            self._allgather_rows(L.Zfull)
+            if cfg.kind == "sage":
+                self._agg(self.csr, L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=0.0,
+                          self_base=self.lo, post_scale=self.inv_deg, add=L.S, relu=relu)
+            elif cfg.kind == "gcn":
+                self._agg(self.csr, L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=1.0,
+                          self_base=self.lo, post_scale=self.gcn_s, relu=relu)
+            else:
+                self._agg(self.csr, L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=1.0,
+                          self_base=self.lo, relu=relu)
+            A = L.Hsp
+            if self.keep_activations:
+                acts.append(L.Hout[:self.nloc, :L.fout].clone())
+        self.activations = acts
+        return self.layers[-1].Hout
+
+    def backward_and_step(self):
+        cfg = self.cfg
+        nL = cfg.layers
+        dH = self.dlogits
+        for l in range(nL - 1, -1, -1):
+            L = self.layers[l]
+            relu = l + 1 < nL
+            own = L.dfull[self.lo:self.hi]
+            mask = L.Hout if relu else None
+            if cfg.kind == "sage":
+                call("gdx_grad_prepare", dH.data_ptr(), dH.shape[1], _lib.ptr(mask), L.Hout.shape[1],
+                     self.nloc, L.w, self.inv_deg.data_ptr(), None, 0, own.data_ptr(), own.shape[1],
+                     L.G.hi.data_ptr(), L.G.lo.data_ptr(), L.G.ld, stream_handle())
+            else:
+                scale = self.gcn_s if cfg.kind == "gcn" else None
+                call("gdx_grad_prepare", dH.data_ptr(), dH.shape[1], _lib.ptr(mask), L.Hout.shape[1],
+                     self.nloc, L.w, _lib.ptr(scale), None, 0, own.data_ptr(), own.shape[1],
+                     None, None, 0, stream_handle())
+            self._allgather_rows(L.dfull)
+            # dZ = agg^T(gs): SAGE -> G[:, w:2w]; GCN/SUM -> G (all columns)
+            if cfg.kind == "sage":
+                Gn = _SplitView(L.G, L.w)
+                self._agg(self.csr, L.dfull, L.w, out_split=Gn, self_coef=0.0, self_base=self.lo)
+            elif cfg.kind == "gcn":
+                self._agg(self.csr, L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo,
+                          post_scale=self.gcn_s)
+            else:
+                self._agg(self.csr, L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo)
+            # dH_{l} = G W_cat  (before this layer's update)
+            if l > 0:
+                dprev = self.dH[l]
+                gemm_tn(L.G, L.WTsp, c0=dprev)
+            # dW = G^T H_in (split-K over the local rows)
+            A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
+            AT = self.XTsp if l == 0 else _transpose(A_in, self.layers[l - 1])
+            call("gdx_transpose_split", L.G.hi.data_ptr(), L.G.lo.data_ptr(), L.G.ld, self.nloc, L.nz,
+                 L.GT.hi.data_ptr(), L.GT.lo.data_ptr(), L.GT.ld, stream_handle())
+            gemm_tn(L.GT, AT, c0=L.ws, split_k=L.split_k)
+            if self.world == 1:
+                call("gdx_splitk_reduce", L.ws.data_ptr(), L.split_k, L.nz * L.fin_ld, L.nz, L.fin,
+                     L.fin_ld, L.dW.data_ptr(), L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(),
+                     L.Wsp.lo.data_ptr(), stream_handle())
+            else:
+                call("gdx_splitk_reduce", L.ws.data_ptr(), L.split_k, L.nz * L.fin_ld, L.nz, L.fin,
+                     L.fin_ld, L.dW.data_ptr(), None, 0.0, None, None, stream_handle())
+                self._allreduce(L.dW)
+                call("gdx_splitk_reduce", L.dW.data_ptr(), 1, 0, L.nz, L.fin, L.fin_ld, None,
+                     L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(), L.Wsp.lo.data_ptr(), stream_handle())
+            L.WTsp.fill_from(L.W, L.fin_ld, transpose=True)
+            if l > 0:
+                dH = self.dH[l]
+
+    def train_epoch(self, sync_loss: bool = True):
+        """Forward, loss, backward, SGD.  Returns the loss (host float) if sync_loss."""
+        self.loss_acc.zero_()
+        logits = self.forward()
+        Lz = self.layers[-1]
+        call("gdx_softmax_xent", logits.data_ptr(), logits.shape[1], self.nloc, self.cfg.classes,
+             self.labels.data_ptr(), 1.0 / self.n, self.dlogits.data_ptr(), self.dlogits.shape[1],
+             self.loss_acc.data_ptr(), stream_handle())
+        self._allreduce(self.loss_acc)
+        self.backward_and_step()
+        if sync_loss:
+            return float(self.loss_acc.item()) / self.n
+        return None
+
+    def aggregation_edges_per_epoch(self) -> int:
+        """Edges aggregated by this rank in one epoch: L forward + L backward passes."""
+        return 2 * self.cfg.layers * self.nnz_local
+
+
+class _SplitView:
+    """Column-offset view of a Split (writes into columns [off, ...))."""
+
+    def __init__(self, s: Split, off: int):
+        self.ld = s.ld
+        self.hi = _Ptr(s.hi.data_ptr() + 2 * off)
+        self.lo = _Ptr(s.lo.data_ptr() + 2 * off)
+
+
+class _Ptr:
+    def __init__(self, p):
+        self.p = p
+
+    def data_ptr(self):
+        return self.p
+
+
+def _transpose(A: Split, layer: _Layer) -> Split:
+    """H^T of a layer output (fin x nloc) into a per-layer cached buffer."""
+    buf = getattr(layer, "_HT", None)
+    if buf is None:
+        buf = Split(A.cols, A.rows, A.hi.device)
+        layer._HT = buf
+    call("gdx_transpose_split", A.hi.data_ptr(), A.lo.data_ptr(), A.ld, A.rows, A.cols, buf.hi.data_ptr(),
+         buf.lo.data_ptr(), buf.ld, stream_handle())
+    return buf
