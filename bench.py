@@ -57,92 +57,90 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------------
-def cpu_epoch_sample(n, degree, seed, dims, rows, threads):
-    """The oracle port's fp64 epoch restricted to destination rows < rows, timed;
-    returns (seconds, rows)."""
+def cpu_baseline_record(args, steps=1, warmup=0):
+    """The oracle port's fp64 SAGE epoch (forward, loss, backward, SGD) on all host
+    threads, restricted to destination rows < rows (default: all rows), timed and
+    extrapolated linearly to the whole epoch."""
     import oracle as O
 
-    g = O.gen_random_graph(n, degree, seed)
-    x = O.make_features(n, dims[0], 1)
-    labels = O.make_labels(n, dims[-1], 2)
+    threads = os.cpu_count() or 1
+    rows = min(args.n, args.cpu_sample_rows or args.n)
+    dims = REDDIT["dims"]
+    g = O.gen_random_graph(args.n, args.degree, REDDIT["seed"])
+    x = O.make_features(args.n, dims[0], 1)
+    labels = O.make_labels(args.n, dims[-1], 2)
     model = O.Model(O.SAGE, dims)
     w = np.random.default_rng(0).uniform(-0.5, 0.5, model.weight_count())
-    t = time.perf_counter()
-    O.train_epoch(g, x, labels, model, w, 0.1, row_limit=rows, nthreads=threads)
-    return time.perf_counter() - t
-
-
-def cpu_baseline_record(args, steps=1, warmup=0):
-    threads = os.cpu_count() or 1
-    rows = args.cpu_sample_rows or max(2000, min(args.n, 6000 * threads))
     times = []
     for i in range(warmup + steps):
-        t = cpu_epoch_sample(args.n, args.degree, REDDIT["seed"], REDDIT["dims"], rows, threads)
+        t = time.perf_counter()
+        O.train_epoch(g, x, labels, model, w, 0.1, row_limit=rows, nthreads=threads)
         if i >= warmup:
-            times.append(t)
+            times.append(time.perf_counter() - t)
     sec = statistics.median(times)
     epoch_ms = sec * 1e3 * args.n / rows
     return {
         "value": round(epoch_ms, 1), "unit": "ms", "cores": threads, "kind": "port",
-        "sample": (f"oracle port (fp64 C restatement, OpenMP {threads} threads) of one SAGE epoch "
-                   f"restricted to the first {rows} of {args.n} destination rows per phase, "
-                   f"{sec:.2f} s measured, extrapolated x{args.n / rows:.2f}; the reference has no "
-                   f"training path (SPEC.md:9) and its forward_full is single-threaded"),
+        "sample": (f"oracle port (fp64 C restatement of the reference loops, OpenMP {threads} "
+                   f"threads): one SAGE epoch over {rows} of {args.n} destination rows, median of "
+                   f"{steps} ({sec:.2f} s), x{args.n / rows:.2f} to a full epoch; the reference has "
+                   f"no training path (SPEC.md:9), so its own code cannot run this epoch"),
     }
 
 
 # ---------------------------------------------------------------------------------
 class ClockSampler:
+    """Samples SM clock and throttle reasons every 5 ms on a thread (NVML) while the
+    timed region runs; falls back to nvidia-smi polling when NVML is unavailable."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
-        self.path = os.path.join(HERE, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        self.samples = []
+        self.max_mhz = None
+        self._stop = None
 
     def __enter__(self):
-        os.makedirs(os.path.dirname(self.path), exist_ok=True)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
         try:
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis else self.gpu
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            return self
+        self._stop = threading.Event()
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, rs))
+                except Exception:
+                    pass
+                self._stop.wait(0.005)
+
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
         return self
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-            self.fh.close()
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
 
     def summary(self):
-        res = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        try:
-            rows = [l.split(",") for l in open(self.path).read().strip().splitlines() if l.strip()]
-        except Exception:
-            return res
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            r = [x.strip() for x in r]
-            try:
-                sm.append(float(r[1]))
-                mx.append(float(r[2]))
-            except (ValueError, IndexError):
-                continue
-            for i, nm in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
-                    reasons.add(nm)
-        if sm:
-            res.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons),
-                       samples=len(sm))
-        return res
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({k for _, r in self.samples for k, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "source": "nvml 5 ms polling during the timed region"}
 
 
 def load_peaks():
@@ -232,9 +230,9 @@ def main():
         e1.record()
         barrier()
     launches = _lib.launch_count() - launches0
-    tr.enable_kernel_events(False)
     ms = e0.elapsed_time(e1) / args.steps
     agg_ms_total, agg_launches, agg_bytes = tr.kernel_event_summary()
+    tr.enable_kernel_events(False)
     loss = tr.train_epoch(sync_loss=True)
 
     t_ms = torch.tensor([ms, agg_ms_total / args.steps], dtype=torch.float64, device=dev)
