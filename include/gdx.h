@@ -94,6 +94,8 @@ typedef struct gdx_aggregate_args {
     uint64_t ld_split;
 } gdx_aggregate_args;
 int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream);
+/* Tuning hook (benchmarks only): forces a kernel variant (unroll depth 4 or 8). */
+int gdx_aggregate_variant(const gdx_aggregate_args* a, int variant, gdx_stream stream);
 
 /* ------------------------------------------------------------------------
  * K2 dense transform on tcgen05 (apply_layer, reference_gnn.cpp:53-60), TN:

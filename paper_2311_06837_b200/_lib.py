@@ -49,6 +49,7 @@ _SIGS = {
     "gdx_init_uniform_f64": (C.c_int, [u64, u64, u64, u64, u32, u32, C.c_double, C.c_double, vp, u64, vp]),
     "gdx_init_labels": (C.c_int, [u64, u64, u32, u32, vp, vp]),
     "gdx_aggregate": (C.c_int, [C.POINTER(AggregateArgs), vp]),
+    "gdx_aggregate_variant": (C.c_int, [C.POINTER(AggregateArgs), C.c_int, vp]),
     "gdx_gemm_tn": (C.c_int, [C.POINTER(GemmArgs), vp]),
     "gdx_gemm_tn_simt": (C.c_int, [C.POINTER(GemmArgs), vp]),
     "gdx_splitk_reduce": (C.c_int, [vp, u32, u64, u32, u32, u64, vp, vp, C.c_float, vp, vp, vp]),

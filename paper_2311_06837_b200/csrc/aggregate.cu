@@ -18,21 +18,48 @@
 namespace gdx {
 namespace {
 
-__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
     uint32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v)
+                 : "l"(p), "l"(pol));
     return v;
 }
 
-__device__ __forceinline__ float4 ld_row4(const float* p) {
+// 16-byte gather of a neighbour row chunk: skip L1 (no reuse on structure-free
+// graphs) and keep the gathered matrix resident in L2 against the index stream.
+__device__ __forceinline__ float4 ld_row4(const void* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+// row address = base + nb * ld_bytes in one IMAD.WIDE.U32
+__device__ __forceinline__ const char* row_addr(uint64_t base, uint32_t nb, uint32_t ldb) {
+    uint64_t r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(nb), "r"(ldb), "l"(base));
+    return reinterpret_cast<const char*>(r);
+}
+
+__device__ __forceinline__ float4 ld_plain4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
+// Packed fp32 adds (FADD2 on sm_100): two lanes of a float4 per instruction.
 __device__ __forceinline__ void add4(float4& a, const float4& b) {
-    a.x += b.x;
-    a.y += b.y;
-    a.z += b.z;
-    a.w += b.w;
+    unsigned long long lo, hi;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(lo)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a.x)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&b.x)));
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(hi)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a.z)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&b.z)));
+    *reinterpret_cast<unsigned long long*>(&a.x) = lo;
+    *reinterpret_cast<unsigned long long*>(&a.z) = hi;
 }
 
 struct AggParams {
@@ -40,9 +67,10 @@ struct AggParams {
     const uint64_t* row_end;
     const uint32_t* col;
     uint32_t rows;
-    uint32_t c4;  // width / 4
+    uint32_t c4;        // width / 4
     const float* src;
-    uint64_t ld_src;
+    uint64_t ld_src;    // elements
+    uint32_t ld_bytes;  // ld_src * 4 (fits: checked on the host)
     float self_coef;
     uint64_t self_base;
     const float* post_scale;
@@ -56,13 +84,27 @@ struct AggParams {
     uint64_t ld_split;
 };
 
-template <int LPE, int NCH>
+constexpr int pow2_floor(int x) { return x >= 32 ? 32 : x >= 16 ? 16 : x >= 8 ? 8 : x >= 4 ? 4 : x >= 2 ? 2 : 1; }
+
+// LPE lanes cover one neighbour row (NCH float4 chunks each); EPW = pow2 rows per
+// warp step; EXACT: c4 == LPE*NCH (no column masks).
+template <int LPE, int NCH, bool EXACT, int UNROLL>
 __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
-    constexpr int EPW = 32 / LPE;  // neighbour rows per warp step
-    constexpr int UNROLL = 4;
+    constexpr int EPW = pow2_floor(32 / LPE);
+    constexpr int STEP = EPW * UNROLL;
     const int lane = threadIdx.x & 31;
     const int sub = lane / LPE;
-    const int lin = lane % LPE;
+    const int lin = lane - sub * LPE;
+    const bool lane_on = sub < EPW;
+    uint64_t pol_keep, pol_stream;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const uint64_t base = reinterpret_cast<uint64_t>(p.src) + 16 * lin;
+    const uint32_t ldb = p.ld_bytes;
+    bool chan_on[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) chan_on[c] = EXACT || (lin + c * LPE) < p.c4;
+
     const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < p.rows;
          row += warps_total) {
@@ -72,49 +114,62 @@ __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
 
+        // index chunks of 32 are software-pipelined: chunk k+1's column ids are in
+        // flight while chunk k's rows are gathered.
+        uint32_t my = (beg + lane < end) ? ld_stream_u32(p.col + beg + lane, pol_stream) : 0u;
         for (uint64_t e0 = beg; e0 < end; e0 += 32) {
             const uint32_t cnt = static_cast<uint32_t>((end - e0) < 32 ? (end - e0) : 32);
-            const uint32_t my = lane < cnt ? ld_stream_u32(p.col + e0 + lane) : 0u;
-            for (uint32_t j = 0; j < cnt; j += EPW * UNROLL) {
+            const uint64_t e1 = e0 + 32;
+            const uint32_t nxt = (e1 + lane < end) ? ld_stream_u32(p.col + e1 + lane, pol_stream) : 0u;
+            uint32_t j = 0;
+            // full steps: no per-edge predicates, UNROLL gathers in flight per lane
+            for (; j + STEP <= cnt; j += STEP) {
                 float4 v[UNROLL][NCH];
 #pragma unroll
                 for (int u = 0; u < UNROLL; ++u) {
-                    const uint32_t slot = j + u * EPW + sub;
-                    const uint32_t nb = __shfl_sync(0xffffffffu, my, slot & 31);
-                    const bool ok = slot < cnt;
-                    const float* rowp = p.src + static_cast<uint64_t>(nb) * p.ld_src;
+                    const uint32_t nb = __shfl_sync(0xffffffffu, my, (j + u * EPW + sub) & 31);
+                    const char* rp = row_addr(base, nb, ldb);
 #pragma unroll
-                    for (int c = 0; c < NCH; ++c) {
-                        const uint32_t ch = lin + c * LPE;
-                        v[u][c] = (ok && ch < p.c4) ? ld_row4(rowp + 4 * ch)
-                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
+                    for (int c = 0; c < NCH; ++c)
+                        v[u][c] = (lane_on && chan_on[c]) ? ld_row4(rp + 16 * LPE * c, pol_keep)
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
                 for (int u = 0; u < UNROLL; ++u)
 #pragma unroll
                     for (int c = 0; c < NCH; ++c) add4(acc[c], v[u][c]);
             }
-        }
-        // combine the EPW lane groups
+            // tail
+            for (; j < cnt; j += EPW) {
+                const uint32_t slot = j + sub;
+                const uint32_t nb = __shfl_sync(0xffffffffu, my, slot & 31);
+                const char* rp = row_addr(base, nb, ldb);
 #pragma unroll
-        for (int off = LPE; off < 32; off <<= 1) {
+                for (int c = 0; c < NCH; ++c)
+                    if (lane_on && chan_on[c] && slot < cnt) add4(acc[c], ld_row4(rp + 16 * LPE * c, pol_keep));
+            }
+            my = nxt;
+        }
+        // combine the EPW lane groups into group 0
+#pragma unroll
+        for (int k = EPW / 2; k >= 1; k >>= 1) {
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-                acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, off);
-                acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, off);
-                acc[c].z += __shfl_xor_sync(0xffffffffu, acc[c].z, off);
-                acc[c].w += __shfl_xor_sync(0xffffffffu, acc[c].w, off);
+                acc[c].x += __shfl_down_sync(0xffffffffu, acc[c].x, k * LPE);
+                acc[c].y += __shfl_down_sync(0xffffffffu, acc[c].y, k * LPE);
+                acc[c].z += __shfl_down_sync(0xffffffffu, acc[c].z, k * LPE);
+                acc[c].w += __shfl_down_sync(0xffffffffu, acc[c].w, k * LPE);
             }
         }
-        const float scale = (sub == 0 && p.post_scale) ? p.post_scale[row] : 1.f;
+        if (sub != 0) continue;
+        const float scale = p.post_scale ? p.post_scale[row] : 1.f;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
             const uint32_t ch = lin + c * LPE;
-            if (sub != 0 || ch >= p.c4) continue;
+            if (!chan_on[c]) continue;
             float4 r = acc[c];
             if (p.self_coef != 0.f) {
-                const float4 s = ld_row4(p.src + (p.self_base + row) * p.ld_src + 4 * ch);
+                const float4 s = ld_plain4(p.src + (p.self_base + row) * p.ld_src + 4 * ch);
                 r.x += p.self_coef * s.x;
                 r.y += p.self_coef * s.y;
                 r.z += p.self_coef * s.z;
@@ -124,7 +179,13 @@ __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
             r.y *= scale;
             r.z *= scale;
             r.w *= scale;
-            if (p.add) add4(r, ld_row4(p.add + row * p.ld_add + 4 * ch));
+            if (p.add) {
+                const float4 q = ld_plain4(p.add + row * p.ld_add + 4 * ch);
+                r.x += q.x;
+                r.y += q.y;
+                r.z += q.z;
+                r.w += q.w;
+            }
             if (p.relu) {
                 r.x = fmaxf(r.x, 0.f);
                 r.y = fmaxf(r.y, 0.f);
@@ -168,25 +229,54 @@ __global__ void __launch_bounds__(256) aggregate_scalar(const AggParams p, uint3
     }
 }
 
-template <int LPE, int NCH>
+template <int LPE, int NCH, bool EXACT, int UNROLL = 4>
 void launch_vec(const AggParams& p, cudaStream_t s) {
     const uint32_t warps_per_block = 8;
     uint64_t blocks = (static_cast<uint64_t>(p.rows) + warps_per_block - 1) / warps_per_block;
     if (blocks > 65535ull * 64) blocks = 65535ull * 64;
-    aggregate_vec4<LPE, NCH><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
+    aggregate_vec4<LPE, NCH, EXACT, UNROLL><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
 }
 
+// Exact instantiations for the widths the engine uses (8/16/32/48/64/128/256),
+// masked power-of-two fallbacks for the rest.
 int pick_and_launch(const AggParams& p, cudaStream_t s) {
+    switch (p.c4) {
+        case 1: launch_vec<1, 1, true>(p, s); return 0;
+        case 2: launch_vec<2, 1, true>(p, s); return 0;
+        case 4: launch_vec<4, 1, true>(p, s); return 0;
+        case 8: launch_vec<8, 1, true>(p, s); return 0;
+        case 12: launch_vec<12, 1, true>(p, s); return 0;
+        case 16: launch_vec<16, 1, true>(p, s); return 0;
+        case 32: launch_vec<32, 1, true>(p, s); return 0;
+        case 64: launch_vec<32, 2, true>(p, s); return 0;
+        default: break;
+    }
     const uint32_t c4 = p.c4;
-    if (c4 <= 1) launch_vec<1, 1>(p, s);
-    else if (c4 <= 2) launch_vec<2, 1>(p, s);
-    else if (c4 <= 4) launch_vec<4, 1>(p, s);
-    else if (c4 <= 8) launch_vec<8, 1>(p, s);
-    else if (c4 <= 16) launch_vec<16, 1>(p, s);
-    else if (c4 <= 32) launch_vec<32, 1>(p, s);
-    else if (c4 <= 64) launch_vec<32, 2>(p, s);
-    else if (c4 <= 128) launch_vec<32, 4>(p, s);
-    else launch_vec<32, 8>(p, s);
+    if (c4 <= 4) launch_vec<4, 1, false>(p, s);
+    else if (c4 <= 8) launch_vec<8, 1, false>(p, s);
+    else if (c4 <= 16) launch_vec<16, 1, false>(p, s);
+    else if (c4 <= 32) launch_vec<32, 1, false>(p, s);
+    else if (c4 <= 64) launch_vec<32, 2, false>(p, s);
+    else if (c4 <= 128) launch_vec<32, 4, false>(p, s);
+    else launch_vec<32, 8, false>(p, s);
+    return 0;
+}
+
+// Tuning hook: variant = unroll depth (4 or 8) for the exact 12/16-lane kernels.
+int launch_variant(const AggParams& p, int variant, cudaStream_t s) {
+    const bool u8 = variant == 8;
+    if (p.c4 == 16) {
+        if (u8) launch_vec<16, 1, true, 8>(p, s);
+        else launch_vec<16, 1, true, 4>(p, s);
+    } else if (p.c4 == 12) {
+        if (u8) launch_vec<12, 1, true, 8>(p, s);
+        else launch_vec<12, 1, true, 4>(p, s);
+    } else if (p.c4 == 8) {
+        if (u8) launch_vec<8, 1, true, 8>(p, s);
+        else launch_vec<8, 1, true, 4>(p, s);
+    } else {
+        return pick_and_launch(p, s);
+    }
     return 0;
 }
 
@@ -195,8 +285,9 @@ bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) ==
 }  // namespace
 }  // namespace gdx
 
-extern "C" int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream) {
-    using namespace gdx;
+namespace gdx {
+namespace {
+int aggregate_impl(const gdx_aggregate_args* a, int variant, gdx_stream stream) {
     GDX_REQUIRE(a != nullptr, GDX_INPUT, "gdx_aggregate: null args");
     GDX_REQUIRE(a->rows == 0 || (a->row_ptr && a->col && a->src), GDX_INPUT,
                 "gdx_aggregate: null CSR or source");
@@ -206,16 +297,18 @@ extern "C" int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream) {
     GDX_REQUIRE(!a->out_hi == !a->out_lo, GDX_INPUT, "gdx_aggregate: out_hi/out_lo must pair");
     if (a->rows == 0) return GDX_OK;
     AggParams p{a->row_ptr, a->row_end, a->col, a->rows, a->width / 4, a->src, a->ld_src,
-                a->self_coef, a->self_base, a->post_scale, a->add, a->ld_add, a->relu, a->out,
-                a->ld_out, a->out_hi, a->out_lo, a->ld_split};
+                static_cast<uint32_t>(a->ld_src * 4), a->self_coef, a->self_base, a->post_scale,
+                a->add, a->ld_add, a->relu, a->out, a->ld_out, a->out_hi, a->out_lo, a->ld_split};
     const bool vec = a->width % 4 == 0 && a->ld_src % 4 == 0 && aligned16(a->src) && a->width <= 4096 &&
+                     a->ld_src * 4 < (1ull << 32) &&
                      (!a->add || (a->ld_add % 4 == 0 && aligned16(a->add))) &&
                      (!a->out || (a->ld_out % 4 == 0 && aligned16(a->out))) &&
                      (!a->out_hi || (a->ld_split % 4 == 0 && (reinterpret_cast<uintptr_t>(a->out_hi) & 7) == 0 &&
                                      (reinterpret_cast<uintptr_t>(a->out_lo) & 7) == 0));
     cudaStream_t s = as_cuda(stream);
     if (vec) {
-        pick_and_launch(p, s);
+        if (variant) launch_variant(p, variant, s);
+        else pick_and_launch(p, s);
     } else {
         uint64_t blocks = (static_cast<uint64_t>(a->rows) + 7) / 8;
         if (blocks > 65535ull * 64) blocks = 65535ull * 64;
@@ -223,4 +316,14 @@ extern "C" int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream) {
     }
     note_launch();
     return check_launch("gdx_aggregate");
+}
+}  // namespace
+}  // namespace gdx
+
+extern "C" int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream) {
+    return gdx::aggregate_impl(a, 0, stream);
+}
+
+extern "C" int gdx_aggregate_variant(const gdx_aggregate_args* a, int variant, gdx_stream stream) {
+    return gdx::aggregate_impl(a, variant, stream);
 }

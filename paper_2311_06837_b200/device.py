@@ -96,7 +96,7 @@ def dense(rows: int, cols: int, device, zero: bool = True) -> torch.Tensor:
 
 def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_split: Split | None = None,
               self_coef: float = 0.0, self_base: int = 0, post_scale=None, add=None, relu=False,
-              row_end=None, stream=None):
+              row_end=None, stream=None, variant: int = 0):
     """K1/K3 (see include/gdx.h gdx_aggregate)."""
     a = AggregateArgs()
     a.row_ptr = g.row_ptr.data_ptr()
@@ -116,7 +116,10 @@ def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_spli
     a.ld_out = out.shape[-1] if out is not None else 0
     if out_split is not None:
         a.out_hi, a.out_lo, a.ld_split = out_split.hi.data_ptr(), out_split.lo.data_ptr(), out_split.ld
-    call("gdx_aggregate", _lib.C.byref(a), stream_handle(stream))
+    if variant:
+        call("gdx_aggregate_variant", _lib.C.byref(a), variant, stream_handle(stream))
+    else:
+        call("gdx_aggregate", _lib.C.byref(a), stream_handle(stream))
 
 
 def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None, relu=False,

@@ -84,8 +84,8 @@ class _Layer:
 
     def __init__(self, kind, fin, fout, nloc, nfull, d, splitk_target, first):
         self.kind, self.fin, self.fout = kind, fin, fout
-        self.k = fin if first else pad4(fin)      # GEMM K: the input operand's logical width
-        self.w = pad4(fout)                       # aggregation width (16 B rows)
+        self.k = fin if first else pad8(fin)      # GEMM K: the input operand's logical width
+        self.w = pad8(fout)                       # aggregation width (32 B sectors)
         self.nz = 2 * self.w if kind == "sage" else self.w   # GEMM N (W_cat rows)
         self.fin_ld = pad8(fin)
         # master weights, row pitch == split pitch so the fused SGD can index both
@@ -189,7 +189,7 @@ class FullGraphTrainer:
             weights = init_weights(cfg, weight_seed)
         self.set_weights(weights)
         self.dlogits = dense(self.nloc, self.layers[-1].w, d)
-        self.dH = [dense(self.nloc, pad4(cfg.dims[l]), d) for l in range(cfg.layers)]
+        self.dH = [dense(self.nloc, pad8(cfg.dims[l]), d) for l in range(cfg.layers)]
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=d)
         self.keep_activations = False
         self.activations = []

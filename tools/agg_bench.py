@@ -1,0 +1,85 @@
+"""Microbenchmark of the aggregation kernel (K1) alone on the Reddit-shape graph.
+
+    python tools/agg_bench.py [--widths 64,48] [--reps 20]
+
+Times gdx_aggregate with CUDA events on the launching stream (after warm-up) and
+prints ms, edges/s and algorithmic GB/s (SURVEY §8d formula) per width.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--widths", default="32,48,64,128")
+    ap.add_argument("--variants", default="4,8")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--n", type=int, default=232965)
+    ap.add_argument("--degree", type=float, default=491.99)
+    args = ap.parse_args()
+    import torch
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.device import aggregate, dense, Split
+
+    d = torch.device("cuda", 0)
+    g = G.gen_random_graph(args.n, args.degree, 11)
+    dg = g.device(d)
+    nnz, n = g.num_edges(), g.num_vertices()
+    res = []
+    for w in [int(x) for x in args.widths.split(",")]:
+        src = torch.randn(n, w, device=d)
+        out = dense(n, w, d)
+        for variant in [int(v) for v in args.variants.split(",")]:
+            kw = dict(out=out, self_coef=1.0, variant=variant)
+            for _ in range(3):
+                aggregate(dg, src, w, **kw)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.reps):
+                aggregate(dg, src, w, **kw)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.reps
+            alg = 4 * nnz + 8 * (n + 1) + 4 * w * nnz + 4 * w * n
+            res.append({"width": w, "unroll": variant, "ms": round(ms, 4),
+                        "gedges_per_s": round(nnz / ms / 1e6, 2),
+                        "alg_GBps": round(alg / ms / 1e6, 1)})
+    # L2-resident streaming read ceiling (library reduction over a 60 MB tensor)
+    for mb in (30, 60):
+        t = torch.randn(mb * 262144, device=d)
+        for _ in range(3):
+            t.sum()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(50):
+            t.sum()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 50
+        res.append({"l2_stream_read_MB": mb, "ms": round(ms, 4), "GBps": round(mb * 1.048576e6 / ms / 1e6, 1)})
+    # library gather for comparison: index_select of 64-wide rows
+    src = torch.randn(n, 64, device=d)
+    idx = dg.col[:20_000_000].long()
+    for _ in range(2):
+        torch.index_select(src, 0, idx)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        torch.index_select(src, 0, idx)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    res.append({"torch_index_select_rows": 20_000_000, "ms": round(ms, 3),
+                "gather_GBps": round(20e6 * 256 / ms / 1e6, 1)})
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
