@@ -148,13 +148,16 @@ class FullGraphTrainer:
         self.d = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         d = self.d
         n = g.num_vertices()
-        part = partition_contiguous(n, world)
-        sizes = part.part_sizes.astype(np.int64)
-        self.offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        # ceil-sized contiguous row blocks: rank r owns [r*B, min((r+1)*B, n)); the
+        # gathered buffers hold world*B rows so every all-gather block is B rows.
+        B = -(-n // world)
+        self.block = B
+        self.offsets = np.minimum(np.arange(world + 1, dtype=np.int64) * B, n)
         self.lo, self.hi = int(self.offsets[rank]), int(self.offsets[rank + 1])
         self.nloc = self.hi - self.lo
         self.n = n
-        self.equal_blocks = bool(np.all(sizes == sizes[0]))
+        self.nrows_gather = world * B
+        self.exchange = RowExchange(np.arange(world + 1, dtype=np.int64) * B, rank, world, pg)
         # local CSR rows [lo, hi) with global column ids
         ro = g.row_offsets()
         base = int(ro[self.lo])
@@ -183,8 +186,8 @@ class FullGraphTrainer:
         sm = torch.cuda.get_device_properties(d).multi_processor_count
         self.layers = []
         for l in range(cfg.layers):
-            self.layers.append(_Layer(cfg.kind, cfg.dims[l], cfg.dims[l + 1], self.nloc, n, d, 2 * sm,
-                                      l == 0))
+            self.layers.append(_Layer(cfg.kind, cfg.dims[l], cfg.dims[l + 1], self.nloc,
+                                      self.nrows_gather, d, 2 * sm, l == 0))
         if weights is None:
             weights = init_weights(cfg, weight_seed)
         self.set_weights(weights)
@@ -241,21 +244,10 @@ class FullGraphTrainer:
 
     # ---- collectives ----
     def _allgather_rows(self, full: torch.Tensor):
-        if self.world == 1:
-            return
-        import torch.distributed as dist
-        if self.equal_blocks:
-            local = full[self.lo:self.hi]
-            dist.all_gather_into_tensor(full[:self.n], local, group=self.pg)
-        else:
-            chunks = [full[int(self.offsets[r]):int(self.offsets[r + 1])] for r in range(self.world)]
-            dist.all_gather(chunks, chunks[self.rank].clone(), group=self.pg)
+        self.exchange.allgather_rows(full)
 
     def _allreduce(self, t: torch.Tensor):
-        if self.world == 1:
-            return
-        import torch.distributed as dist
-        dist.all_reduce(t, group=self.pg)
+        self.exchange.allreduce(t)
 
     # ---- one epoch ----
     def forward(self):
@@ -356,6 +348,49 @@ class FullGraphTrainer:
     def aggregation_edges_per_epoch(self) -> int:
         """Edges aggregated by this rank in one epoch: L forward + L backward passes."""
         return 2 * self.cfg.layers * self.nnz_local
+
+
+class RowExchange:
+    """The per-layer exchange of a row-partitioned full graph:
+    every rank owns the contiguous row block offsets[r]:offsets[r+1] of a
+    [n, w] matrix and receives everybody else's block (all-gather); weight
+    gradients are summed (all-reduce).  NCCL on GPUs; any torch.distributed
+    backend works, which is how the CPU tests drive it with gloo."""
+
+    def __init__(self, offsets, rank: int, world: int, pg=None):
+        self.offsets = np.asarray(offsets, np.int64)
+        self.rank, self.world, self.pg = rank, world, pg
+        sizes = np.diff(self.offsets)
+        self.equal_blocks = bool(np.all(sizes == sizes[0]))
+
+    def allgather_rows(self, full: torch.Tensor):
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        n = int(self.offsets[-1])
+        lo, hi = int(self.offsets[self.rank]), int(self.offsets[self.rank + 1])
+        if self.equal_blocks:
+            dist.all_gather_into_tensor(full[:n], full[lo:hi].clone() if full.device.type == "cpu"
+                                        else full[lo:hi], group=self.pg)
+        else:
+            # unequal blocks: gather padded blocks, then scatter them into place
+            sizes = np.diff(self.offsets)
+            mb = int(sizes.max())
+            send = torch.zeros((mb,) + tuple(full.shape[1:]), dtype=full.dtype, device=full.device)
+            send[:hi - lo] = full[lo:hi]
+            recv = torch.empty((self.world * mb,) + tuple(full.shape[1:]), dtype=full.dtype,
+                               device=full.device)
+            dist.all_gather_into_tensor(recv, send, group=self.pg)
+            for r in range(self.world):
+                if r != self.rank:
+                    a, b = int(self.offsets[r]), int(self.offsets[r + 1])
+                    full[a:b].copy_(recv[r * mb:r * mb + (b - a)])
+
+    def allreduce(self, t: torch.Tensor):
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        dist.all_reduce(t, group=self.pg)
 
 
 class _SplitView:
