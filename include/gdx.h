@@ -148,6 +148,11 @@ int gdx_grad_prepare(const float* dH, uint64_t ld_dh, const float* H, uint64_t l
 int gdx_softmax_xent(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
                      const int32_t* labels, float inv_count, float* dlogits, uint64_t ld_d,
                      double* loss_sum, gdx_stream stream);
+/* Bandwidth probe for roofline denominators: reads `bytes` of buf `reps` times,
+ * mode 0 = coalesced stream, mode 1 = random 256 B row gathers (bytes moved =
+ * reps * bytes in both modes).  Time it with events on `stream`. */
+int gdx_probe_bandwidth(const float* buf, uint64_t bytes, uint32_t reps, int mode, float* sink,
+                        gdx_stream stream);
 /* Per-vertex scales from CSR degrees: kind 0 -> 1/deg (0 if deg=0), 1 -> (deg+1)^-1/2. */
 int gdx_degree_scale(const uint64_t* row_ptr, uint32_t rows, int kind, float* out,
                      gdx_stream stream);

@@ -156,6 +156,47 @@ __global__ void splitk_reduce_kernel(const float* ws, uint32_t split_k, uint64_t
     }
 }
 
+// Bandwidth probe (roofline denominators): mode 0 streams the buffer with 16 B
+// loads (coalesced), mode 1 gathers random 256 B rows (the aggregation's access
+// pattern without the CSR).  The buffer is L2-resident when it fits.
+__global__ void __launch_bounds__(256) probe_kernel(const float4* __restrict__ buf, uint64_t n4,
+                                                    uint32_t reps, int mode, float* sink) {
+    constexpr int U = 8;  // independent 16 B loads in flight per thread
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    if (mode == 0) {
+        for (uint32_t r = 0; r < reps; ++r)
+            for (uint64_t i = tid; i + (U - 1) * nthreads < n4; i += U * nthreads) {
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = __ldcg(buf + i + u * nthreads);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+                }
+            }
+    } else {
+        const uint64_t rows = n4 / 16;  // 256-byte rows, 16 lanes per row
+        const int lane16 = threadIdx.x & 15;
+        uint64_t h = (tid >> 4) * 0x9e3779b97f4a7c15ULL + 1;
+        const uint64_t steps = reps * (n4 / nthreads) / U;
+        for (uint64_t k = 0; k < steps; ++k) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                h = h * 6364136223846793005ULL + 1442695040888963407ULL;
+                v[u] = __ldcg(buf + ((h >> 33) % rows) * 16 + lane16);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+            }
+        }
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 12345.678f) sink[0] = acc.x;
+}
+
 unsigned grid_for(uint64_t total, unsigned block = 256) {
     uint64_t b = (total + block - 1) / block;
     const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 16;
@@ -277,4 +318,14 @@ extern "C" int gdx_splitk_reduce(const float* ws, uint32_t split_k, uint64_t str
         ws, split_k, stride, rows, cols, ld, out, w, lr, w_hi, w_lo);
     note_launch();
     return check_launch("gdx_splitk_reduce");
+}
+
+extern "C" int gdx_probe_bandwidth(const float* buf, uint64_t bytes, uint32_t reps, int mode,
+                                   float* sink, gdx_stream stream) {
+    GDX_REQUIRE(buf && sink && bytes >= 4096 && (bytes % 4096) == 0, GDX_INPUT,
+                "gdx_probe_bandwidth: need a 4 KiB-multiple buffer");
+    probe_kernel<<<kNumSMs * 8, 256, 0, as_cuda(stream)>>>(reinterpret_cast<const float4*>(buf), bytes / 16,
+                                                           reps, mode, sink);
+    note_launch();
+    return check_launch("gdx_probe_bandwidth");
 }

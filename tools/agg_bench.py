@@ -49,20 +49,25 @@ def main():
             res.append({"width": w, "unroll": variant, "ms": round(ms, 4),
                         "gedges_per_s": round(nnz / ms / 1e6, 2),
                         "alg_GBps": round(alg / ms / 1e6, 1)})
-    # L2-resident streaming read ceiling (library reduction over a 60 MB tensor)
-    for mb in (30, 60):
-        t = torch.randn(mb * 262144, device=d)
-        for _ in range(3):
-            t.sum()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(50):
-            t.sum()
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 50
-        res.append({"l2_stream_read_MB": mb, "ms": round(ms, 4), "GBps": round(mb * 1.048576e6 / ms / 1e6, 1)})
+    # bandwidth ceilings with the library's probe kernel: L2-resident (60 MB) and
+    # HBM-resident (4 GB) buffers, coalesced stream and random 256 B row gathers
+    from paper_2311_06837_b200._lib import call
+    from paper_2311_06837_b200.device import stream_handle
+    sink = torch.zeros(4, device=d)
+    for mb, reps in ((60, 40), (4096, 2)):
+        buf = torch.randn(mb * 262144, device=d)
+        for mode in (0, 1):
+            call("gdx_probe_bandwidth", buf.data_ptr(), buf.numel() * 4, reps, mode, sink.data_ptr(), stream_handle())
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            call("gdx_probe_bandwidth", buf.data_ptr(), buf.numel() * 4, reps, mode, sink.data_ptr(), stream_handle())
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            res.append({"probe_MB": mb, "mode": ["stream", "gather256"][mode], "ms": round(ms, 3),
+                        "GBps": round(reps * buf.numel() * 4 / ms / 1e6, 1)})
+        del buf
     # library gather for comparison: index_select of 64-wide rows
     src = torch.randn(n, 64, device=d)
     idx = dg.col[:20_000_000].long()
