@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
     ap.add_argument("--n", type=int, default=REDDIT["n"])
     ap.add_argument("--degree", type=float, default=REDDIT["degree"])
@@ -152,6 +153,17 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def launches_per_epoch(tr) -> int:
+    """libgdx kernel launches in one eager epoch (graph replays issue the same kernels)."""
+    import torch
+    from paper_2311_06837_b200 import _lib
+    torch.cuda.synchronize()
+    a = _lib.launch_count()
+    tr.train_epoch(sync_loss=False)
+    torch.cuda.synchronize()
+    return _lib.launch_count() - a
+
+
 def probe_l2_peak(torch, dev):
     """Live L2 read ceiling: the library's coalesced-stream probe over a 60 MB
     (L2-resident) buffer, best of 3, GB/s."""
@@ -235,8 +247,25 @@ def main():
         tr.train_epoch(sync_loss=False)
     barrier()
 
-    # ---- timed region (device events, aggregation launches instrumented) ----
+    # ---- kernel-level roofline: the aggregation launches of K eager epochs, timed
+    # with CUDA events on the launching stream ----
     tr.enable_kernel_events(True)
+    barrier()
+    for _ in range(args.steps):
+        tr.train_epoch(sync_loss=False)
+    barrier()
+    agg_ms_total, agg_launches, agg_bytes = tr.kernel_event_summary()
+    tr.enable_kernel_events(False)
+    eager_epoch_events = None
+
+    # ---- timed region: K epochs (CUDA-graph replays unless --eager) ----
+    use_graph = not args.eager
+    if use_graph:
+        tr.capture(warmup=1)
+        for _ in range(2):
+            tr.replay()
+    step = tr.replay if use_graph else (lambda: tr.train_epoch(sync_loss=False))
+    barrier()
     launches0 = _lib.launch_count()
     with ClockSampler(local) as clk:
         barrier()
@@ -244,13 +273,13 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            tr.train_epoch(sync_loss=False)
+            step()
         e1.record()
         barrier()
     launches = _lib.launch_count() - launches0
+    if use_graph:
+        launches = launches_per_epoch(tr) * args.steps
     ms = e0.elapsed_time(e1) / args.steps
-    agg_ms_total, agg_launches, agg_bytes = tr.kernel_event_summary()
-    tr.enable_kernel_events(False)
     loss = tr.train_epoch(sync_loss=True)
 
     t_ms = torch.tensor([ms, agg_ms_total / args.steps], dtype=torch.float64, device=dev)
@@ -270,7 +299,7 @@ def main():
         s0.record()
         for _ in range(args.steps):
             tr.load_features(xh, lh)
-            tr.train_epoch(sync_loss=True)
+            tr.train_epoch(sync_loss=True) if not use_graph else tr.replay(sync_loss=True)
         s1.record()
         barrier()
         e2e_ms = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device=dev)
@@ -338,12 +367,16 @@ def main():
                                       "60 MB L2-resident buffer (best of 4)"},
             },
             "gpu_launches": int(launches),
+            "cuda_graph": use_graph,
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "setup_s": {"graph_generation": round(t_gen, 2)},
         }
         print(json.dumps(out), flush=True)
+    # release the captured graph (it references the NCCL communicator) before teardown
+    tr.graph = None
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

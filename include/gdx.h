@@ -98,16 +98,21 @@ int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream);
 int gdx_aggregate_variant(const gdx_aggregate_args* a, int variant, gdx_stream stream);
 
 /* ------------------------------------------------------------------------
- * K2 dense transform on tcgen05 (apply_layer, reference_gnn.cpp:53-60), TN:
- *   C[m][n] = sum_k (A_hi+A_lo)[m][k] * (B_hi+B_lo)[n][k]   (3 bf16 MMAs, fp32 TMEM acc)
+ * K2 dense transform on tcgen05 (apply_layer, reference_gnn.cpp:53-60):
+ *   C[m][n] = sum_k (A_hi+A_lo)(m,k) * (B_hi+B_lo)(n,k)   (3 bf16 MMAs, fp32 TMEM acc)
+ * with each operand K-major or MN-major (so G^T H needs no transposes).
+ * Persistent: one CTA per SM, double-buffered TMEM accumulator.
  * Epilogue: C *= row_scale[m]; relu; columns [0,split) -> c0, [split,n) -> c1;
  * optional split-bf16 copy.  split_k > 1 writes raw partials to
  * c0 + z*m*ldc0 (z < split_k) for gdx_splitk_reduce.
  * Constraints: lda, ldb multiples of 8 elements; device pointers 16 B aligned.
+ * Note: inputs are read by TMA through tensor maps built per call on the host.
  * ---------------------------------------------------------------------- */
 typedef struct gdx_gemm_args {
     const uint16_t* a_hi; const uint16_t* a_lo; uint64_t lda;
     const uint16_t* b_hi; const uint16_t* b_lo; uint64_t ldb;
+    int a_mn_major;           /* 0: A stored [m][k] (K-major); 1: A stored [k][m] */
+    int b_mn_major;           /* 0: B stored [n][k];           1: B stored [k][n] */
     uint32_t m, n, k;
     float* c0; uint64_t ldc0;
     float* c1; uint64_t ldc1;

@@ -32,6 +32,7 @@ class AggregateArgs(C.Structure):
 class GemmArgs(C.Structure):
     _fields_ = [
         ("a_hi", vp), ("a_lo", vp), ("lda", u64), ("b_hi", vp), ("b_lo", vp), ("ldb", u64),
+        ("a_mn_major", C.c_int), ("b_mn_major", C.c_int),
         ("m", u32), ("n", u32), ("k", u32), ("c0", vp), ("ldc0", u64), ("c1", vp), ("ldc1", u64),
         ("split", u32), ("row_scale", vp), ("relu", C.c_int), ("out_hi", vp), ("out_lo", vp),
         ("ld_split", u64), ("split_k", u32),

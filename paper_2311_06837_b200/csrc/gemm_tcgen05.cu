@@ -1,9 +1,11 @@
 // gemm_tcgen05.cu -- K2: the dense feature transform on 5th-gen tensor cores.
 //
 // Replaces apply_layer (reference_gnn.cpp:53-60) -- out = W * agg for every
-// vertex -- by one TN GEMM over all rows,  C[m][n] = sum_k A[m][k] B[n][k],
+// vertex -- by one GEMM over all rows,  C[m][n] = sum_k A(m,k) B(n,k),
 // and serves the backward GEMMs of the training extension (dW = G^T H with
-// split-K over vertices, dH = G W).
+// split-K over vertices, dH = G W).  A and B are each K-major (A[m][k]) or
+// MN-major (A stored [k][m]); the MN-major forms let dW = G^T H read G and H
+// in place, with no transposes.
 //
 // Precision: the path must stay within 1e-4 (scaled) of an fp64 oracle, which
 // TF32 or plain BF16 cannot.  Operands are stored "split bf16" (x = hi + lo,
@@ -12,12 +14,13 @@
 // accumulator: ~2^-16 relative per product, fp32 accumulation, at 1/3 of the
 // bf16 tensor rate -- the GEMMs here are skinny (N <= 256) and HBM-bound anyway.
 //
-// Structure (one 128 x BN output tile per CTA, 128 threads):
-//   warp 0 / lane 0 : TMA producer  (cp.async.bulk.tensor, 128B swizzle, mbarrier tx)
-//   warp 1 / lane 0 : MMA issuer    (tcgen05.mma, tcgen05.commit -> stage release)
-//   warp 2          : TMEM allocator (tcgen05.alloc / dealloc, BN fp32 columns)
-//   warps 0-3       : epilogue      (tcgen05.ld 32x32b -> scale/ReLU -> fp32 / split stores)
-// Operand stages: {A_hi, A_lo, B_hi, B_lo} x BK=64, S stages deep.
+// Persistent structure: one CTA per SM loops over output tiles (128 x BN, and
+// K ranges for split-K); 192 threads:
+//   warp 0 / lane 0 : TMA producer   (cp.async.bulk.tensor, 128B swizzle, mbarrier tx)
+//   warp 1 / lane 0 : MMA issuer     (tcgen05.mma, tcgen05.commit releases stages / accumulators)
+//   warps 2-5       : epilogue       (tcgen05.ld 32x32b -> scale/ReLU -> vector stores)
+// The accumulator is double-buffered in TMEM (2 x BN fp32 columns) so the
+// epilogue of tile i overlaps the TMA + MMA of tile i+1.
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -29,6 +32,7 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
+constexpr int kThreads = 192;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -42,6 +46,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -66,15 +74,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
-// K-major, 128B-swizzled smem operand descriptor (tcgen05 "matrix descriptor"):
+// 128B-swizzled smem operand descriptor (tcgen05 "matrix descriptor"):
 // start>>4 [0,14) | LBO>>4 [16,30) | SBO>>4 [32,46) | version 1 [46,48) | swizzle 2 [61,64)
-__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+//   K-major : rows of 64 k-elements (128 B), 8-row groups at SBO = 1024 B (LBO unused)
+//   MN-major: 64 mn-elements contiguous, 8 k-rows per 1 KB atom (SBO = 1024 B between
+//             k-groups), 64-wide mn blocks LBO apart
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr, uint32_t lbo) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
-    d |= static_cast<uint64_t>(1) << 16;              // LBO (unused for swizzled K-major)
-    d |= static_cast<uint64_t>(1024 >> 4) << 32;      // SBO: 8 rows x 128 B
-    d |= static_cast<uint64_t>(1) << 46;              // descriptor version (sm_100)
-    d |= static_cast<uint64_t>(2) << 61;              // SWIZZLE_128B
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
     return d;
 }
 
@@ -121,59 +132,74 @@ struct Epi {
     uint16_t* out_lo;
     uint64_t ld_split;
     uint32_t split_k;
-    uint32_t kblocks;  // total k blocks
+    uint32_t kblocks;   // total k blocks
+    uint32_t m_tiles, n_tiles;
 };
 
 template <int BN, int STAGES>
 struct Smem {
-    static constexpr uint32_t kA = BM * BK * 2;  // bytes per A operand tile
+    static constexpr uint32_t kA = BM * BK * 2;  // bytes per A operand tile (hi or lo)
     static constexpr uint32_t kB = BN * BK * 2;
     static constexpr uint32_t kStage = 2 * kA + 2 * kB;
-    static constexpr uint32_t kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr uint32_t kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/;
 };
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(128, 1)
-    gemm_tn_bf16x3(const __grid_constant__ CUtensorMap map_ahi,
-                   const __grid_constant__ CUtensorMap map_alo,
-                   const __grid_constant__ CUtensorMap map_bhi,
-                   const __grid_constant__ CUtensorMap map_blo, const Epi ep) {
+// Load one operand tile (rows x BK of a K-major matrix, or BK x rows of an
+// MN-major one) into smem as the canonical SW128 layout.
+template <int ROWS, bool MN>
+__device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
+                                             int32_t row0, int32_t k0) {
+    if constexpr (!MN) {
+        tma_load_2d(dst, map, bar, k0, row0);  // box {64 k, ROWS rows}
+    } else {
+#pragma unroll
+        for (int b = 0; b < ROWS / 64; ++b)  // box {64 mn, BK k}, 8 KB each
+            tma_load_2d(dst + b * (64 * BK * 2), map, bar, row0 + 64 * b, k0);
+    }
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                const Epi ep) {
     using S = Smem<BN, STAGES>;
+    constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
     uint64_t* empty = full + STAGES;
-    uint64_t* accum = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+    uint64_t* tfull = empty + STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t m0 = blockIdx.x * BM;
-    const uint32_t n0 = blockIdx.y * BN;
-
-    // split-K range of k blocks
+    const uint32_t total = ep.m_tiles * ep.n_tiles * ep.split_k;
     const uint32_t per = (ep.kblocks + ep.split_k - 1) / ep.split_k;
-    const uint32_t kb_begin = blockIdx.z * per;
-    const uint32_t kb_end = min(ep.kblocks, kb_begin + per);
-    const uint32_t nkb = kb_end > kb_begin ? kb_end - kb_begin : 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(accum, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(static_cast<uint32_t>(BN)));
+                     "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -181,115 +207,172 @@ __global__ void __launch_bounds__(128, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0 && lane == 0 && nkb > 0) {
-        // ---------------- TMA producer ----------------
-        for (uint32_t i = 0; i < nkb; ++i) {
-            const int s = i % STAGES;
-            const uint32_t ph = (i / STAGES) & 1;
-            mbar_wait(&empty[s], ph ^ 1);
-            uint8_t* st = smem + s * S::kStage;
-            mbar_expect_tx(&full[s], S::kStage);
-            const int32_t kc = static_cast<int32_t>((kb_begin + i) * BK);
-            tma_load_2d(st, &map_ahi, &full[s], kc, static_cast<int32_t>(m0));
-            tma_load_2d(st + S::kA, &map_alo, &full[s], kc, static_cast<int32_t>(m0));
-            tma_load_2d(st + 2 * S::kA, &map_bhi, &full[s], kc, static_cast<int32_t>(n0));
-            tma_load_2d(st + 2 * S::kA + S::kB, &map_blo, &full[s], kc, static_cast<int32_t>(n0));
-        }
-    } else if (warp == 1 && lane == 0 && nkb > 0) {
-        // ---------------- MMA issuer ----------------
-        // kind::f16: D=f32 (bit 4), A=B=bf16 (bits 7, 10), K-major both, N>>3 @17, M>>4 @24
-        constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
-                                   (static_cast<uint32_t>(BN >> 3) << 17) |
-                                   (static_cast<uint32_t>(BM >> 4) << 24);
-        for (uint32_t i = 0; i < nkb; ++i) {
-            const int s = i % STAGES;
-            const uint32_t ph = (i / STAGES) & 1;
-            mbar_wait(&full[s], ph);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t st = smem_u32(smem + s * S::kStage);
-            const uint32_t a_hi = st, a_lo = st + S::kA, b_hi = st + 2 * S::kA,
-                           b_lo = st + 2 * S::kA + S::kB;
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-                const uint32_t off = kk * 32;  // 16 bf16 along K inside the swizzle row
-                const uint64_t dah = smem_desc_sw128(a_hi + off), dal = smem_desc_sw128(a_lo + off);
-                const uint64_t dbh = smem_desc_sw128(b_hi + off), dbl = smem_desc_sw128(b_lo + off);
-                mma_bf16(tmem, dah, dbh, idesc, (i | kk) != 0);
-                mma_bf16(tmem, dah, dbl, idesc, 1);
-                mma_bf16(tmem, dal, dbh, idesc, 1);
-            }
-            mma_commit(&empty[s]);  // frees the stage once these MMAs retire
-        }
-        mma_commit(accum);
-    }
-    __syncwarp();
+    auto tile_coords = [&](uint32_t t, uint32_t& mt, uint32_t& nt, uint32_t& z) {
+        z = t % ep.split_k;
+        const uint32_t mn = t / ep.split_k;
+        nt = mn % ep.n_tiles;
+        mt = mn / ep.n_tiles;
+    };
 
-    // ---------------- epilogue: TMEM -> registers -> global ----------------
-    if (nkb > 0) {
-        mbar_wait(accum, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-    const uint32_t row = m0 + warp * 32 + lane;
-    const bool row_ok = row < ep.m;
-    const float rs = (row_ok && ep.row_scale && ep.split_k <= 1) ? ep.row_scale[row] : 1.f;
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            uint32_t it = 0;
+            for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+                uint32_t mt, nt, z;
+                tile_coords(t, mt, nt, z);
+                const uint32_t kb0 = z * per, kb1 = min(ep.kblocks, kb0 + per);
+                for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    uint8_t* st = smem + s * S::kStage;
+                    mbar_expect_tx(&full[s], S::kStage);
+                    const int32_t kc = static_cast<int32_t>(kb * BK);
+                    load_operand<BM, A_MN>(st, &map_ahi, &full[s], static_cast<int32_t>(mt * BM), kc);
+                    load_operand<BM, A_MN>(st + S::kA, &map_alo, &full[s], static_cast<int32_t>(mt * BM), kc);
+                    load_operand<BN, B_MN>(st + 2 * S::kA, &map_bhi, &full[s], static_cast<int32_t>(nt * BN), kc);
+                    load_operand<BN, B_MN>(st + 2 * S::kA + S::kB, &map_blo, &full[s],
+                                           static_cast<int32_t>(nt * BN), kc);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer ----------------
+            // kind::f16: D=f32 (bit 4), A=B=bf16 (bits 7, 10), majors (15, 16), N>>3 @17, M>>4 @24
+            constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                                       ((B_MN ? 1u : 0u) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                       (static_cast<uint32_t>(BM >> 4) << 24);
+            // per 16-wide k step: +32 B inside the swizzle row (K-major) or +16 rows (MN-major)
+            constexpr uint32_t a_step = A_MN ? 16 * 128 : 32, b_step = B_MN ? 16 * 128 : 32;
+            constexpr uint32_t a_lbo = A_MN ? 64 * BK * 2 : 16, b_lbo = B_MN ? 64 * BK * 2 : 16;
+            uint32_t it = 0, tl = 0;
+            for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
+                uint32_t mt, nt, z;
+                tile_coords(t, mt, nt, z);
+                const uint32_t kb0 = z * per, kb1 = min(ep.kblocks, kb0 + per);
+                const uint32_t acc = tl & 1;
+                mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d_tmem = tmem + acc * BN;
+                for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t st = smem_u32(smem + s * S::kStage);
+                    const uint32_t ahi = st, alo = st + S::kA, bhi = st + 2 * S::kA, blo = st + 2 * S::kA + S::kB;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const uint64_t dah = smem_desc_sw128(ahi + kk * a_step, a_lbo);
+                        const uint64_t dal = smem_desc_sw128(alo + kk * a_step, a_lbo);
+                        const uint64_t dbh = smem_desc_sw128(bhi + kk * b_step, b_lbo);
+                        const uint64_t dbl = smem_desc_sw128(blo + kk * b_step, b_lbo);
+                        mma_bf16(d_tmem, dah, dbh, idesc, (kb != kb0 || kk) ? 1u : 0u);
+                        mma_bf16(d_tmem, dah, dbl, idesc, 1u);
+                        mma_bf16(d_tmem, dal, dbh, idesc, 1u);
+                    }
+                    mma_commit(&empty[s]);  // frees the stage once these MMAs retire
+                }
+                mma_commit(&tfull[acc]);    // accumulator ready for the epilogue
+            }
+        }
+    } else {
+        // ---------------- epilogue warps 2..5 ----------------
+        const uint32_t lane_base = 32 * (warp & 3);  // TMEM lanes this warp may access
+        uint32_t tl = 0;
+        for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
+            uint32_t mt, nt, z;
+            tile_coords(t, mt, nt, z);
+            const uint32_t acc = tl & 1;
+            const bool has_k = z * per < ep.kblocks;  // an empty split still gets a commit
+            mbar_wait(&tfull[acc], (tl >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t row = mt * BM + lane_base + lane;
+            const bool row_ok = row < ep.m;
+            const float rs = (row_ok && ep.row_scale && ep.split_k <= 1) ? ep.row_scale[row] : 1.f;
 #pragma unroll 1
-    for (int cb = 0; cb < BN; cb += 16) {
-        float v[16];
-        if (nkb > 0) {
-            tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cb, v);
-        } else {
+            for (int cb = 0; cb < BN; cb += 16) {
+                float v[16];
+                if (has_k) {
+                    tmem_ld16(tmem + (lane_base << 16) + acc * BN + cb, v);
+                } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        }
-        if (!row_ok) continue;
-        if (ep.split_k > 1) {
-            float* dst = ep.c0 + static_cast<uint64_t>(blockIdx.z) * ep.m * ep.ldc0 +
-                         static_cast<uint64_t>(row) * ep.ldc0;
+                    for (int j = 0; j < 16; ++j) v[j] = 0.f;
+                }
+                const uint32_t col0 = nt * BN + cb;
+                if (!row_ok || col0 >= ep.n) continue;
+                if (ep.split_k > 1) {
+                    float* dst = ep.c0 + static_cast<uint64_t>(z) * ep.m * ep.ldc0 +
+                                 static_cast<uint64_t>(row) * ep.ldc0 + col0;
+                    if (col0 + 16 <= ep.n && (ep.ldc0 % 4) == 0) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint32_t col = n0 + cb + j;
-                if (col < ep.n) dst[col] = v[j];
-            }
-            continue;
-        }
+                        for (int j = 0; j < 16; j += 4)
+                            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    } else {
+                        for (int j = 0; j < 16 && col0 + j < ep.n; ++j) dst[j] = v[j];
+                    }
+                    continue;
+                }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t col = n0 + cb + j;
-            if (col >= ep.n) continue;
-            float x = v[j] * rs;
-            if (ep.relu) x = fmaxf(x, 0.f);
-            if (col < ep.split) {
-                if (ep.c0) ep.c0[static_cast<uint64_t>(row) * ep.ldc0 + col] = x;
-            } else if (ep.c1) {
-                ep.c1[static_cast<uint64_t>(row) * ep.ldc1 + (col - ep.split)] = x;
+                for (int j = 0; j < 16; ++j) {
+                    v[j] *= rs;
+                    if (ep.relu) v[j] = fmaxf(v[j], 0.f);
+                }
+                // a 16-column group entirely on one side of the split: 4 x 16 B stores
+                float* base = nullptr;
+                if (col0 + 16 <= ep.n) {
+                    if (col0 + 16 <= ep.split && ep.c0 && ep.ldc0 % 4 == 0)
+                        base = ep.c0 + static_cast<uint64_t>(row) * ep.ldc0 + col0;
+                    else if (col0 >= ep.split && ep.c1 && ep.ldc1 % 4 == 0 && (col0 - ep.split) % 4 == 0)
+                        base = ep.c1 + static_cast<uint64_t>(row) * ep.ldc1 + (col0 - ep.split);
+                }
+                if (base && (reinterpret_cast<uintptr_t>(base) & 15) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4*>(base + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                } else {
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t col = col0 + j;
+                        if (col >= ep.n) break;
+                        if (col < ep.split) {
+                            if (ep.c0) ep.c0[static_cast<uint64_t>(row) * ep.ldc0 + col] = v[j];
+                        } else if (ep.c1) {
+                            ep.c1[static_cast<uint64_t>(row) * ep.ldc1 + (col - ep.split)] = v[j];
+                        }
+                    }
+                }
+                if (ep.out_hi) {
+                    uint16_t* hp = ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0;
+                    uint16_t* lp = ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0;
+                    for (int j = 0; j < 16 && col0 + j < ep.n; ++j) split_bf16(v[j], hp[j], lp[j]);
+                }
             }
-            if (ep.out_hi) {
-                uint16_t h, l;
-                split_bf16(x, h, l);
-                ep.out_hi[static_cast<uint64_t>(row) * ep.ld_split + col] = h;
-                ep.out_lo[static_cast<uint64_t>(row) * ep.ld_split + col] = l;
-            }
+            // accumulator drained: hand it back to the MMA warp
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 2) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                     "r"(static_cast<uint32_t>(BN)));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
     }
 }
 
 // ---- reference-precision SIMT GEMM (tests / tiny shapes) ----------------------
-__global__ void gemm_tn_simt_kernel(const uint16_t* a_hi, const uint16_t* a_lo, uint64_t lda,
-                                    const uint16_t* b_hi, const uint16_t* b_lo, uint64_t ldb,
-                                    uint32_t k, const Epi ep) {
+__global__ void gemm_simt_kernel(const uint16_t* a_hi, const uint16_t* a_lo, uint64_t lda, int a_mn,
+                                 const uint16_t* b_hi, const uint16_t* b_lo, uint64_t ldb, int b_mn,
+                                 uint32_t k, const Epi ep) {
     const uint32_t row = blockIdx.y * blockDim.y + threadIdx.y;
     const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= ep.m || col >= ep.n) return;
     float acc = 0.f;
     for (uint32_t i = 0; i < k; ++i) {
-        const float a = bf2f(a_hi[row * lda + i]) + bf2f(a_lo[row * lda + i]);
-        const float b = bf2f(b_hi[col * ldb + i]) + bf2f(b_lo[col * ldb + i]);
+        const uint64_t ia = a_mn ? static_cast<uint64_t>(i) * lda + row : static_cast<uint64_t>(row) * lda + i;
+        const uint64_t ib = b_mn ? static_cast<uint64_t>(i) * ldb + col : static_cast<uint64_t>(col) * ldb + i;
+        const float a = bf2f(a_hi[ia]) + bf2f(a_lo[ia]);
+        const float b = bf2f(b_hi[ib]) + bf2f(b_lo[ib]);
         acc = fmaf(a, b, acc);
     }
     if (ep.split_k > 1) {  // single "split": write partial 0, zero the others
@@ -322,13 +405,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-int make_map(CUtensorMap* map, const uint16_t* base, uint64_t rows, uint64_t k, uint64_t ld,
-             uint32_t box_rows) {
+// inner x outer matrix (inner contiguous, pitch ld elements), box {64, box_outer}
+int make_map(CUtensorMap* map, const uint16_t* base, uint64_t inner, uint64_t outer, uint64_t ld,
+             uint32_t box_outer) {
     auto fn = encode_fn();
     GDX_REQUIRE(fn != nullptr, GDX_INTERNAL, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[2] = {k, rows};
+    cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {ld * 2};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), box_rows};
+    cuuint32_t box[2] = {64u, box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(base), dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -338,31 +422,59 @@ int make_map(CUtensorMap* map, const uint16_t* base, uint64_t rows, uint64_t k, 
     return GDX_OK;
 }
 
-template <int BN, int STAGES>
+// Operand maps: K-major = (k inner, rows outer, box {64, rows_per_tile});
+// MN-major = (rows inner, k outer, box {64, BK}).
+int operand_maps(CUtensorMap* hi, CUtensorMap* lo, const uint16_t* phi, const uint16_t* plo,
+                 uint64_t rows, uint64_t k, uint64_t ld, bool mn, uint32_t tile_rows) {
+    int rc;
+    if (!mn) {
+        if ((rc = make_map(hi, phi, k, rows, ld, tile_rows))) return rc;
+        return make_map(lo, plo, k, rows, ld, tile_rows);
+    }
+    if ((rc = make_map(hi, phi, rows, k, ld, BK))) return rc;
+    return make_map(lo, plo, rows, k, ld, BK);
+}
+
+int g_num_sms = 0;
+
+template <int BN, int STAGES, bool A_MN, bool B_MN>
 int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
     int rc;
-    if ((rc = make_map(&ma_hi, g->a_hi, g->m, g->k, g->lda, BM))) return rc;
-    if ((rc = make_map(&ma_lo, g->a_lo, g->m, g->k, g->lda, BM))) return rc;
-    if ((rc = make_map(&mb_hi, g->b_hi, g->n, g->k, g->ldb, BN))) return rc;
-    if ((rc = make_map(&mb_lo, g->b_lo, g->n, g->k, g->ldb, BN))) return rc;
-    auto kern = gemm_tn_bf16x3<BN, STAGES>;
+    if ((rc = operand_maps(&ma_hi, &ma_lo, g->a_hi, g->a_lo, g->m, g->k, g->lda, A_MN, BM))) return rc;
+    if ((rc = operand_maps(&mb_hi, &mb_lo, g->b_hi, g->b_lo, g->n, g->k, g->ldb, B_MN, BN))) return rc;
+    auto kern = gemm_bf16x3<BN, STAGES, A_MN, B_MN>;
     const int bytes = Smem<BN, STAGES>::kBytes;
     static bool configured = false;  // per instantiation
     if (!configured) {
         GDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         configured = true;
     }
-    dim3 grid((g->m + BM - 1) / BM, (g->n + BN - 1) / BN, ep.split_k > 1 ? ep.split_k : 1);
-    kern<<<grid, 128, bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, ep);
+    if (!g_num_sms) {
+        int dev = 0;
+        GDX_CUDA(cudaGetDevice(&dev));
+        GDX_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const uint64_t tiles = static_cast<uint64_t>(ep.m_tiles) * ep.n_tiles * ep.split_k;
+    const unsigned grid = static_cast<unsigned>(tiles < static_cast<uint64_t>(g_num_sms) ? tiles : g_num_sms);
+    kern<<<grid, kThreads, bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, ep);
     note_launch();
     return check_launch("gdx_gemm_tn");
+}
+
+template <int BN, int STAGES>
+int launch_majors(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
+    if (!g->a_mn_major && !g->b_mn_major) return launch_tc<BN, STAGES, false, false>(g, ep, s);
+    if (g->a_mn_major && g->b_mn_major) return launch_tc<BN, STAGES, true, true>(g, ep, s);
+    if (g->a_mn_major) return launch_tc<BN, STAGES, true, false>(g, ep, s);
+    return launch_tc<BN, STAGES, false, true>(g, ep, s);
 }
 
 int validate(const gdx_gemm_args* g) {
     GDX_REQUIRE(g != nullptr, GDX_INPUT, "gdx_gemm_tn: null args");
     GDX_REQUIRE(g->a_hi && g->a_lo && g->b_hi && g->b_lo, GDX_INPUT, "gdx_gemm_tn: null operand");
-    GDX_REQUIRE(g->lda >= g->k && g->ldb >= g->k, GDX_INPUT, "gdx_gemm_tn: leading dim < k");
+    GDX_REQUIRE(g->lda >= (g->a_mn_major ? g->m : g->k) && g->ldb >= (g->b_mn_major ? g->n : g->k),
+                GDX_INPUT, "gdx_gemm_tn: leading dim too small");
     GDX_REQUIRE(g->lda % 8 == 0 && g->ldb % 8 == 0, GDX_INPUT,
                 "gdx_gemm_tn: leading dims must be multiples of 8 elements (16 B TMA pitch)");
     GDX_REQUIRE(g->split <= g->n, GDX_INPUT, "gdx_gemm_tn: split > n");
@@ -372,11 +484,10 @@ int validate(const gdx_gemm_args* g) {
     return GDX_OK;
 }
 
-Epi make_epi(const gdx_gemm_args* g) {
+Epi make_epi(const gdx_gemm_args* g, int bn) {
     Epi ep{g->m, g->n, g->c0, g->ldc0, g->c1, g->ldc1, g->split, g->row_scale, g->relu,
            g->out_hi, g->out_lo, g->ld_split, g->split_k ? g->split_k : 1,
-           (g->k + BK - 1) / BK};
-    if (ep.split_k > ep.kblocks && ep.kblocks > 0) ep.split_k = ep.kblocks;
+           (g->k + BK - 1) / BK, (g->m + BM - 1) / BM, (g->n + bn - 1) / bn};
     return ep;
 }
 
@@ -388,13 +499,14 @@ extern "C" int gdx_gemm_tn(const gdx_gemm_args* g, gdx_stream stream) {
     int rc = validate(g);
     if (rc) return rc;
     if (g->m == 0 || g->n == 0) return GDX_OK;
-    Epi ep = make_epi(g);
-    GDX_REQUIRE(ep.split_k == (g->split_k ? g->split_k : 1) || g->k == 0, GDX_INPUT,
+    const int bn = g->n <= 64 ? 64 : (g->n <= 128 ? 128 : 256);
+    Epi ep = make_epi(g, bn);
+    GDX_REQUIRE(ep.split_k <= ep.kblocks || g->k == 0, GDX_INPUT,
                 "gdx_gemm_tn: split_k exceeds the number of 64-wide k blocks");
     cudaStream_t s = as_cuda(stream);
-    if (g->n <= 64) return launch_tc<64, 4>(g, ep, s);
-    if (g->n <= 128) return launch_tc<128, 3>(g, ep, s);
-    return launch_tc<256, 2>(g, ep, s);
+    if (bn == 64) return launch_majors<64, 4>(g, ep, s);
+    if (bn == 128) return launch_majors<128, 3>(g, ep, s);
+    return launch_majors<256, 2>(g, ep, s);
 }
 
 extern "C" int gdx_gemm_tn_simt(const gdx_gemm_args* g, gdx_stream stream) {
@@ -402,11 +514,10 @@ extern "C" int gdx_gemm_tn_simt(const gdx_gemm_args* g, gdx_stream stream) {
     int rc = validate(g);
     if (rc) return rc;
     if (g->m == 0 || g->n == 0) return GDX_OK;
-    Epi ep = make_epi(g);
-    ep.split_k = g->split_k ? g->split_k : 1;
+    Epi ep = make_epi(g, 64);
     dim3 blk(32, 8), grid((g->n + 31) / 32, (g->m + 7) / 8);
-    gemm_tn_simt_kernel<<<grid, blk, 0, as_cuda(stream)>>>(g->a_hi, g->a_lo, g->lda, g->b_hi,
-                                                           g->b_lo, g->ldb, g->k, ep);
+    gemm_simt_kernel<<<grid, blk, 0, as_cuda(stream)>>>(g->a_hi, g->a_lo, g->lda, g->a_mn_major, g->b_hi,
+                                                        g->b_lo, g->ldb, g->b_mn_major, g->k, ep);
     note_launch();
     return check_launch("gdx_gemm_tn_simt");
 }

@@ -123,20 +123,25 @@ def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_spli
 
 
 def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None, relu=False,
-            out_split: Split | None = None, split_k: int = 1, m=None, simt=False, stream=None):
-    """K2: C = A . B^T over the shared k = A.cols (see gdx_gemm_tn)."""
-    assert A.cols == B.cols, (A.cols, B.cols)
+            out_split: Split | None = None, split_k: int = 1, m=None, simt=False, a_mn=False,
+            b_mn=False, stream=None):
+    """K2: C(m, n) = sum_k A(m, k) B(n, k).  A is stored [m][k] (K-major) or, with
+    a_mn, [k][m]; likewise B ([n][k] or [k][n]).  See gdx_gemm_tn."""
+    mA, kA = (A.cols, A.rows) if a_mn else (A.rows, A.cols)
+    nB, kB = (B.cols, B.rows) if b_mn else (B.rows, B.cols)
+    assert kA == kB, (kA, kB)
     g = GemmArgs()
     g.a_hi, g.a_lo, g.lda = A.hi.data_ptr(), A.lo.data_ptr(), A.ld
     g.b_hi, g.b_lo, g.ldb = B.hi.data_ptr(), B.lo.data_ptr(), B.ld
-    g.m = A.rows if m is None else m
-    g.n = B.rows
-    g.k = A.cols
+    g.a_mn_major, g.b_mn_major = int(a_mn), int(b_mn)
+    g.m = mA if m is None else m
+    g.n = nB
+    g.k = kA
     g.c0 = ptr(c0)
     g.ldc0 = c0.shape[-1] if c0 is not None else 0
     g.c1 = ptr(c1)
     g.ldc1 = c1.shape[-1] if c1 is not None else 0
-    g.split = B.rows if split is None else split
+    g.split = nB if split is None else split
     g.row_scale = ptr(row_scale)
     g.relu = int(relu)
     if out_split is not None:

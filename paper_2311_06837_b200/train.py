@@ -90,8 +90,7 @@ class _Layer:
         self.fin_ld = pad8(fin)
         # master weights, row pitch == split pitch so the fused SGD can index both
         self.W = torch.zeros((self.nz, self.fin_ld), dtype=torch.float32, device=d)
-        self.Wsp = Split(self.nz, self.k, d, ld=self.fin_ld)  # forward B   (nz x k)
-        self.WTsp = Split(fin, self.nz, d)                    # backward B  (fin x nz)
+        self.Wsp = Split(self.nz, self.k, d, ld=self.fin_ld)  # forward B (nz x k); MN-major B of dH
         self.dW = torch.zeros((self.nz, self.fin_ld), dtype=torch.float32, device=d)
         kb = max(1, math.ceil(nloc / 64))
         ntiles = max(1, math.ceil(fin / (256 if fin > 128 else (128 if fin > 64 else 64))))
@@ -103,7 +102,6 @@ class _Layer:
         self.Hout = dense(nloc, self.w, d)                               # act output fp32
         self.Hsp = Split(nloc, self.w, d)                                # next layer's A
         self.G = Split(nloc, self.nz, d)                                 # [dP | dZn] or dZ
-        self.GT = Split(self.nz, nloc, d)
         self.dfull = dense(nfull, self.w, d)                             # gathered grads
 
     def set_weights(self, mats):
@@ -119,7 +117,6 @@ class _Layer:
 
     def refresh_splits(self):
         self.Wsp.fill_from(self.W, self.fin_ld)
-        self.WTsp.fill_from(self.W, self.fin_ld, transpose=True)
 
     def get_weights(self):
         W = self.W.double().cpu().numpy()
@@ -180,7 +177,6 @@ class FullGraphTrainer:
         call("gdx_init_labels", label_seed, self.lo, self.nloc, cfg.classes, self.labels.data_ptr(),
              stream_handle())
         self.Xsp = Split(self.nloc, F, d)
-        self.XTsp = Split(F, self.nloc, d)
         self._refresh_input_splits()
         # layers
         sm = torch.cuda.get_device_properties(d).multi_processor_count
@@ -201,7 +197,6 @@ class FullGraphTrainer:
     # ---- state ----
     def _refresh_input_splits(self):
         self.Xsp.fill_from(self.X, self.X.shape[1])
-        self.XTsp.fill_from(self.X, self.X.shape[1], transpose=True)
 
     def set_weights(self, weights):
         k = 2 if self.cfg.kind == "sage" else 1
@@ -307,16 +302,13 @@ class FullGraphTrainer:
                           post_scale=self.gcn_s)
             else:
                 self._agg(self.csr, L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo)
-            # dH_{l} = G W_cat  (before this layer's update)
+            # dH_{l} = G W_cat  (before this layer's update); W_cat read MN-major in place
             if l > 0:
                 dprev = self.dH[l]
-                gemm_tn(L.G, L.WTsp, c0=dprev)
-            # dW = G^T H_in (split-K over the local rows)
+                gemm_tn(L.G, L.Wsp, c0=dprev, b_mn=True)
+            # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
-            AT = self.XTsp if l == 0 else _transpose(A_in, self.layers[l - 1])
-            call("gdx_transpose_split", L.G.hi.data_ptr(), L.G.lo.data_ptr(), L.G.ld, self.nloc, L.nz,
-                 L.GT.hi.data_ptr(), L.GT.lo.data_ptr(), L.GT.ld, stream_handle())
-            gemm_tn(L.GT, AT, c0=L.ws, split_k=L.split_k)
+            gemm_tn(L.G, A_in, c0=L.ws, split_k=L.split_k, a_mn=True, b_mn=True)
             if self.world == 1:
                 call("gdx_splitk_reduce", L.ws.data_ptr(), L.split_k, L.nz * L.fin_ld, L.nz, L.fin,
                      L.fin_ld, L.dW.data_ptr(), L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(),
@@ -327,7 +319,6 @@ class FullGraphTrainer:
                 self._allreduce(L.dW)
                 call("gdx_splitk_reduce", L.dW.data_ptr(), 1, 0, L.nz, L.fin, L.fin_ld, None,
                      L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(), L.Wsp.lo.data_ptr(), stream_handle())
-            L.WTsp.fill_from(L.W, L.fin_ld, transpose=True)
             if l > 0:
                 dH = self.dH[l]
 
@@ -341,6 +332,27 @@ class FullGraphTrainer:
              self.loss_acc.data_ptr(), stream_handle())
         self._allreduce(self.loss_acc)
         self.backward_and_step()
+        if sync_loss:
+            return float(self.loss_acc.item()) / self.n
+        return None
+
+    # ---- CUDA graph of one epoch (removes host launch overhead) ----
+    def capture(self, warmup: int = 2):
+        """Capture one epoch (forward, loss, backward, collectives, SGD) as a CUDA
+        graph.  All buffers are static (allocated in __init__ / first epochs), TMA
+        descriptors travel by value in the kernel nodes, NCCL collectives are
+        captured on the same stream."""
+        for _ in range(warmup):
+            self.train_epoch(sync_loss=False)
+        torch.cuda.synchronize(self.d)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.train_epoch(sync_loss=False)
+        torch.cuda.synchronize(self.d)
+        return self.graph
+
+    def replay(self, sync_loss: bool = False):
+        self.graph.replay()
         if sync_loss:
             return float(self.loss_acc.item()) / self.n
         return None
@@ -408,14 +420,3 @@ class _Ptr:
 
     def data_ptr(self):
         return self.p
-
-
-def _transpose(A: Split, layer: _Layer) -> Split:
-    """H^T of a layer output (fin x nloc) into a per-layer cached buffer."""
-    buf = getattr(layer, "_HT", None)
-    if buf is None:
-        buf = Split(A.cols, A.rows, A.hi.device)
-        layer._HT = buf
-    call("gdx_transpose_split", A.hi.data_ptr(), A.lo.data_ptr(), A.ld, A.rows, A.cols, buf.hi.data_ptr(),
-         buf.lo.data_ptr(), buf.ld, stream_handle())
-    return buf

@@ -48,6 +48,44 @@ def test_gemm_tcgen05_matches_fp64(gdx, cuda, m, n, k):
     close(c[:m, :n].double().cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("m,n,k", [(128, 64, 64), (300, 128, 602), (96, 602, 5000), (130, 256, 700)])
+def test_gemm_operand_majors(gdx, cuda, a_mn, b_mn, m, n, k):
+    """MN-major operands (A stored [k][m], B stored [k][n]) as used by dW = G^T H."""
+    import torch
+    rng = np.random.default_rng(m + n + k + 10 * a_mn + 20 * b_mn)
+    a = rng.uniform(-0.5, 0.5, (m, k))
+    b = rng.uniform(-0.5, 0.5, (n, k))
+    A = _split(gdx, a.T.copy() if a_mn else a, cuda)
+    B = _split(gdx, b.T.copy() if b_mn else b, cuda)
+    c = gdx.dense(m, n, cuda)
+    gdx.gemm_tn(A, B, c0=c, a_mn=bool(a_mn), b_mn=bool(b_mn))
+    torch.cuda.synchronize()
+    ref = a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T
+    close(c[:m, :n].double().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("split_k", [3, 64])
+def test_gemm_mn_splitk(gdx, cuda, split_k):
+    """The trainer's weight-gradient shape: M = 96, N = 602, K = rows, split-K."""
+    import torch
+    from paper_2311_06837_b200._lib import call
+    rng = np.random.default_rng(split_k)
+    m, n, k = 96, 602, 20000
+    g = rng.uniform(-1, 1, (k, m))
+    h = rng.uniform(-1, 1, (k, n))
+    A, B = _split(gdx, g, cuda), _split(gdx, h, cuda)
+    ld = 608
+    ws = torch.zeros(split_k * m, ld, dtype=torch.float32, device=cuda)
+    gdx.gemm_tn(A, B, c0=ws, split_k=split_k, a_mn=True, b_mn=True)
+    out = torch.zeros(m, ld, dtype=torch.float32, device=cuda)
+    call("gdx_splitk_reduce", ws.data_ptr(), split_k, m * ld, m, n, ld, out.data_ptr(), None, 0.0,
+         None, None, gdx.stream_handle())
+    torch.cuda.synchronize()
+    ref = g.astype(np.float32).astype(np.float64).T @ h.astype(np.float32).astype(np.float64)
+    close(out[:m, :n].double().cpu().numpy(), ref)
+
+
 def test_gemm_epilogue_split_scale_relu(gdx, cuda):
     import torch
     rng = np.random.default_rng(5)
