@@ -49,6 +49,9 @@ int gdx_host_gen_random_graph_fill(uint32_t n, double avg_degree, uint64_t seed,
                                    const uint64_t* row_offsets, uint32_t* cols);
 /* partition_random (partition.cpp:51-61). */
 int gdx_host_partition_random(uint32_t n, uint32_t parts, uint64_t seed, uint32_t* assignment);
+/* partition_mincut (partition.cpp:63-170) over a host CSR (bit-identical assignment). */
+int gdx_host_partition_mincut(uint32_t n, const uint64_t* row_offsets, const uint32_t* cols,
+                              uint32_t parts, uint64_t seed, double epsilon, uint32_t* assignment);
 
 /* ------------------------------------------------------------------------
  * K7 initialisation: make_features / make_layer_weights (reference_gnn.cpp:11-32)

@@ -13,7 +13,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <numeric>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -159,5 +161,105 @@ extern "C" int gdx_host_partition_random(uint32_t n, uint32_t parts, uint64_t se
     Stream r(seed, 0x7061727469ULL, 0);
     for (uint64_t i = n; i > 1; --i) std::swap(perm[i - 1], perm[r.below(i)]);
     for (uint32_t i = 0; i < n; ++i) assignment[perm[i]] = i % parts;
+    return GDX_OK;
+}
+
+// partition_mincut (partition.cpp:63-170): greedy region growing from high-degree
+// seeds (frontier vertex with the most edges into the region next, ties to the
+// lowest id), then <= 10 boundary-refinement passes under the size cap
+// floor(ceil(n/parts) * (1 + eps)).  Host preprocessing: deterministic and
+// sequential by construction; bit-identical assignment to the reference.
+extern "C" int gdx_host_partition_mincut(uint32_t n, const uint64_t* ro, const uint32_t* ci,
+                                         uint32_t parts, uint64_t seed, double eps,
+                                         uint32_t* assignment) {
+    (void)seed;  // growth and refinement are fully deterministic (partition.cpp:67)
+    if (parts == 0) return fail(GDX_INPUT, "partition: parts must be >= 1");
+    if (parts > n)
+        return fail(GDX_INPUT, "partition: parts (" + std::to_string(parts) +
+                                   ") exceeds vertex count (" + std::to_string(n) + ")");
+    if (eps < 0.0) return fail(GDX_INPUT, "partition: epsilon must be >= 0");
+    const uint32_t unassigned = parts;
+    std::vector<uint32_t> a(n, unassigned);
+    const uint32_t base = n / parts, rem = n % parts;
+    auto deg = [&](uint32_t v) { return static_cast<uint32_t>(ro[v + 1] - ro[v]); };
+    std::vector<uint32_t> by_degree(n);
+    std::iota(by_degree.begin(), by_degree.end(), 0u);
+    std::stable_sort(by_degree.begin(), by_degree.end(),
+                     [&](uint32_t x, uint32_t y) { return deg(x) > deg(y); });
+    size_t seed_scan = 0;
+    std::vector<uint32_t> gain(n, 0), touched;
+    constexpr uint32_t kMax = std::numeric_limits<uint32_t>::max();
+    for (uint32_t part = 0; part < parts; ++part) {
+        const uint32_t target = base + (part < rem ? 1 : 0);
+        uint32_t taken = 0;
+        std::priority_queue<std::pair<uint32_t, uint32_t>> frontier;  // (gain, MAX - v)
+        while (taken < target) {
+            uint32_t v = n;
+            while (!frontier.empty()) {
+                auto [g_at, key] = frontier.top();
+                frontier.pop();
+                const uint32_t cand = kMax - key;
+                if (a[cand] != unassigned || gain[cand] != g_at) continue;
+                v = cand;
+                break;
+            }
+            if (v == n) {
+                while (a[by_degree[seed_scan]] != unassigned) ++seed_scan;
+                v = by_degree[seed_scan];
+            }
+            a[v] = part;
+            ++taken;
+            for (uint64_t e = ro[v]; e < ro[v + 1]; ++e) {
+                const uint32_t u = ci[e];
+                if (a[u] != unassigned) continue;
+                if (gain[u] == 0) touched.push_back(u);
+                ++gain[u];
+                frontier.push({gain[u], kMax - u});
+            }
+        }
+        for (uint32_t u : touched) gain[u] = 0;
+        touched.clear();
+    }
+    std::vector<uint32_t> size(parts, 0);
+    for (uint32_t v = 0; v < n; ++v) ++size[a[v]];
+    uint32_t cap = static_cast<uint32_t>(
+        std::floor(static_cast<double>((n + parts - 1) / parts) * (1.0 + eps)));
+    cap = std::max<uint32_t>(cap, (n + parts - 1) / parts);
+    std::vector<uint64_t> conn(parts, 0);
+    std::vector<uint32_t> tparts;
+    for (int pass = 0; pass < 10; ++pass) {
+        bool moved = false;
+        for (uint32_t v = 0; v < n; ++v) {
+            const uint32_t own = a[v];
+            if (size[own] <= 1) continue;
+            tparts.clear();
+            for (uint64_t e = ro[v]; e < ro[v + 1]; ++e) {
+                const uint32_t q = a[ci[e]];
+                if (conn[q] == 0) tparts.push_back(q);
+                ++conn[q];
+            }
+            uint32_t best = own;
+            const uint64_t own_conn = conn[own];
+            uint64_t best_gain = 0;
+            for (uint32_t q : tparts) {
+                if (q == own || size[q] + 1 > cap) continue;
+                if (conn[q] > own_conn && conn[q] - own_conn > best_gain) {
+                    best_gain = conn[q] - own_conn;
+                    best = q;
+                } else if (conn[q] > own_conn && conn[q] - own_conn == best_gain && q < best) {
+                    best = q;
+                }
+            }
+            for (uint32_t q : tparts) conn[q] = 0;
+            if (best != own) {
+                a[v] = best;
+                --size[own];
+                ++size[best];
+                moved = true;
+            }
+        }
+        if (!moved) break;
+    }
+    std::copy(a.begin(), a.end(), assignment);
     return GDX_OK;
 }

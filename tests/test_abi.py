@@ -91,3 +91,35 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "nope.so"))
     with pytest.raises(InternalError):
         _lib.lib()
+
+
+@pytest.mark.parametrize("n,d,seed,parts", [(120, 6.0, 2200, 2), (10000, 10.0, 7, 2), (3000, 20.0, 1, 8),
+                                            (500, 3.0, 4, 7)])
+def test_host_partition_mincut_and_hierarchical_bit_exact(n, d, seed, parts):
+    import oracle as O
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.partition_host import hierarchical_partition, partition_mincut
+    if not O.ref_available():
+        pytest.skip("needs oracle/_ref")
+    R = O.ref()
+    g = G.gen_random_graph(n, d, seed)
+    h = R.grr_graph_from_csr(n, g.row_offsets(), g.col_indices())
+    ref = np.zeros(n, np.uint32)
+    assert R.grr_partition_mincut(h, parts, 1, 0.05, ref) == 0
+    assert np.array_equal(partition_mincut(g, parts, 1).assignment, ref)
+    sp, gp = np.zeros(n, np.uint32), np.zeros(n, np.uint32)
+    R.grr_hierarchical_partition(h, 2, 3, 1, 5, sp, gp)
+    R.grr_graph_free(h)
+    hp = hierarchical_partition(g, 2, 3, "mincut", 5)
+    assert np.array_equal(hp.server.assignment, sp) and np.array_equal(hp.gpu.assignment, gp)
+
+
+def test_golden_mincut_partition():
+    import os
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.partition_host import partition_mincut
+    gold = os.path.join(ROOT, "tests", "golden")
+    z = np.load(os.path.join(gold, "graph_er_10k_d10_s7.npz"))
+    f = np.load(os.path.join(gold, "forward_full_config1.npz"))
+    g = G.Graph(int(z["n"]), z["row_offsets"], z["cols"])
+    assert np.array_equal(partition_mincut(g, 2, 1).assignment, f["mincut2"])

@@ -147,6 +147,21 @@ def test_engine_golden(cuda):
         assert np.array_equal(v, cz[f"s{s}_r1_b0_vertices"])
         assert G.peel_mfg(g, v, t, 2) == [int(a) for a in cz[f"s{s}_r1_b0_mfg"]]
 
+    # plan_cobatch_fixed_r with the reference's min-cut target split (r = 1 and 3)
+    for s in range(2):
+        hop = cz[f"hop_s{s}"]
+        sub = G.DependencySubgraph(s, np.nonzero(hop == 0)[0].astype(np.uint32),
+                                   np.nonzero((hop != 0) & (hop != O.UNSEEN))[0].astype(np.uint32),
+                                   hop[(hop != 0) & (hop != O.UNSEEN)], 0, 1, True)
+        for r in (1, 3):
+            plan = G.plan_cobatch_fixed_r(sub, g, 2, G.SamplingConfig(1, 3, 5), r, G.ModelSpec(2, 8, 8))
+            assert plan.batch_count() == int(cz[f"s{s}_r{r}_batches"][0])
+            for b, bt in enumerate(plan.batches):
+                assert np.array_equal(bt.target_vertices, cz[f"s{s}_r{r}_b{b}_targets"])
+                assert np.array_equal(bt.vertices, cz[f"s{s}_r{r}_b{b}_vertices"])
+                assert bt.mfg_vertices_per_layer == [int(a) for a in cz[f"s{s}_r{r}_b{b}_mfg"]]
+                assert bt.est_memory_bytes == int(cz[f"s{s}_r{r}_b{b}_bytes"][0])
+
     def owner_dev(v, sp_a, gp_a, s):
         shares = G.split_batch(v, sp, gp, s, 3)
         out = np.zeros(len(v), np.uint32)
