@@ -72,13 +72,19 @@ int gdx_init_labels(uint64_t seed, uint64_t base, uint32_t rows, uint32_t classe
 /* ------------------------------------------------------------------------
  * K1/K3 aggregation: the forward_full inner loop (reference_gnn.cpp:76-83),
  * forward_server_local's masked loop (:123-134) and the transposed backward.
- *   out[v] = act( post_scale[v] * (self_coef * src[self_base+v]
- *                                  + sum_{e in [row_ptr[v], row_end[v])} src[col[e]])
+ *   out[v] = act( post_scale[v] * (self_coef * src[self_base+v] + partial[v]
+ *                                  + sum_{e in [row_ptr[v], row_end[v]) \ skip} src[col[e]])
  *                 + add[v] )
+ * The skip range / partial pair splits a row into the locally owned column block
+ * (aggregated while the all-gather of remote rows is in flight) and the rest.
  * ---------------------------------------------------------------------- */
 typedef struct gdx_aggregate_args {
     const uint64_t* row_ptr;  /* [rows+1] */
-    const uint64_t* row_end;  /* nullable: per-row end (hop masking), else row_ptr[v+1] */
+    const uint64_t* row_end;  /* nullable: per-row end, else row_ptr[v+1] */
+    const uint64_t* skip_lo;  /* nullable pair: per-row sub-range [skip_lo, skip_hi) excluded */
+    const uint64_t* skip_hi;
+    const float* partial;     /* nullable: partial sums [rows x ld_partial] added before scaling */
+    uint64_t ld_partial;
     const uint32_t* col;
     uint32_t rows;
     uint32_t width;           /* feature width F (any; fast paths for F % 4 == 0) */
@@ -97,6 +103,9 @@ typedef struct gdx_aggregate_args {
     uint64_t ld_split;
 } gdx_aggregate_args;
 int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream);
+/* seg_lo[v], seg_hi[v] = sub-range of row v's (sorted) column ids inside [lo, hi). */
+int gdx_row_split(const uint64_t* row_ptr, const uint32_t* col, uint32_t rows, uint32_t lo,
+                  uint32_t hi, uint64_t* seg_lo, uint64_t* seg_hi, gdx_stream stream);
 /* Tuning hook (benchmarks only): forces a kernel variant (unroll depth 4 or 8). */
 int gdx_aggregate_variant(const gdx_aggregate_args* a, int variant, gdx_stream stream);
 

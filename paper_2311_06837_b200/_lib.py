@@ -22,7 +22,8 @@ u32 = C.c_uint32
 
 class AggregateArgs(C.Structure):
     _fields_ = [
-        ("row_ptr", vp), ("row_end", vp), ("col", vp), ("rows", u32), ("width", u32),
+        ("row_ptr", vp), ("row_end", vp), ("skip_lo", vp), ("skip_hi", vp), ("partial", vp),
+        ("ld_partial", u64), ("col", vp), ("rows", u32), ("width", u32),
         ("src", vp), ("ld_src", u64), ("self_coef", C.c_float), ("self_base", u64),
         ("post_scale", vp), ("add", vp), ("ld_add", u64), ("relu", C.c_int),
         ("out", vp), ("ld_out", u64), ("out_hi", vp), ("out_lo", vp), ("ld_split", u64),
@@ -52,6 +53,7 @@ _SIGS = {
     "gdx_init_labels": (C.c_int, [u64, u64, u32, u32, vp, vp]),
     "gdx_aggregate": (C.c_int, [C.POINTER(AggregateArgs), vp]),
     "gdx_aggregate_variant": (C.c_int, [C.POINTER(AggregateArgs), C.c_int, vp]),
+    "gdx_row_split": (C.c_int, [vp, vp, u32, u32, u32, vp, vp, vp]),
     "gdx_gemm_tn": (C.c_int, [C.POINTER(GemmArgs), vp]),
     "gdx_gemm_tn_simt": (C.c_int, [C.POINTER(GemmArgs), vp]),
     "gdx_splitk_reduce": (C.c_int, [vp, u32, u64, u32, u32, u64, vp, vp, C.c_float, vp, vp, vp]),

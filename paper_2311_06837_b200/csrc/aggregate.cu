@@ -65,6 +65,10 @@ __device__ __forceinline__ void add4(float4& a, const float4& b) {
 struct AggParams {
     const uint64_t* row_ptr;
     const uint64_t* row_end;
+    const uint64_t* skip_lo;  // optional excluded sub-range [skip_lo, skip_hi) per row
+    const uint64_t* skip_hi;
+    const float* partial;     // optional partial sums added before the epilogue
+    uint64_t ld_partial;
     const uint32_t* col;
     uint32_t rows;
     uint32_t c4;        // width / 4
@@ -114,13 +118,21 @@ __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
 
+        // with a skip range the row is processed as [beg, skip_lo) then [skip_hi, end)
+        const int nseg = p.skip_lo ? 2 : 1;
+        for (int seg = 0; seg < nseg; ++seg) {
+        uint64_t sbeg = beg, send = end;
+        if (p.skip_lo) {
+            if (seg == 0) send = p.skip_lo[row];
+            else sbeg = p.skip_hi[row];
+        }
         // index chunks of 32 are software-pipelined: chunk k+1's column ids are in
         // flight while chunk k's rows are gathered.
-        uint32_t my = (beg + lane < end) ? ld_stream_u32(p.col + beg + lane, pol_stream) : 0u;
-        for (uint64_t e0 = beg; e0 < end; e0 += 32) {
-            const uint32_t cnt = static_cast<uint32_t>((end - e0) < 32 ? (end - e0) : 32);
+        uint32_t my = (sbeg + lane < send) ? ld_stream_u32(p.col + sbeg + lane, pol_stream) : 0u;
+        for (uint64_t e0 = sbeg; e0 < send; e0 += 32) {
+            const uint32_t cnt = static_cast<uint32_t>((send - e0) < 32 ? (send - e0) : 32);
             const uint64_t e1 = e0 + 32;
-            const uint32_t nxt = (e1 + lane < end) ? ld_stream_u32(p.col + e1 + lane, pol_stream) : 0u;
+            const uint32_t nxt = (e1 + lane < send) ? ld_stream_u32(p.col + e1 + lane, pol_stream) : 0u;
             uint32_t j = 0;
             // full steps: no per-edge predicates, UNROLL gathers in flight per lane
             for (; j + STEP <= cnt; j += STEP) {
@@ -150,6 +162,7 @@ __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
             }
             my = nxt;
         }
+        }
         // combine the EPW lane groups into group 0
 #pragma unroll
         for (int k = EPW / 2; k >= 1; k >>= 1) {
@@ -168,6 +181,13 @@ __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
             const uint32_t ch = lin + c * LPE;
             if (!chan_on[c]) continue;
             float4 r = acc[c];
+            if (p.partial) {
+                const float4 q = ld_plain4(p.partial + row * p.ld_partial + 4 * ch);
+                r.x += q.x;
+                r.y += q.y;
+                r.z += q.z;
+                r.w += q.w;
+            }
             if (p.self_coef != 0.f) {
                 const float4 s = ld_plain4(p.src + (p.self_base + row) * p.ld_src + 4 * ch);
                 r.x += p.self_coef * s.x;
@@ -214,18 +234,38 @@ __global__ void __launch_bounds__(256) aggregate_scalar(const AggParams p, uint3
          row += warps_total) {
         const uint64_t beg = p.row_ptr[row];
         const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
+        const uint64_t s0 = p.skip_lo ? p.skip_lo[row] : end, s1 = p.skip_hi ? p.skip_hi[row] : end;
         const float scale = p.post_scale ? p.post_scale[row] : 1.f;
         for (uint32_t c = lane; c < width; c += 32) {
             float acc = p.self_coef != 0.f ? p.self_coef * p.src[(p.self_base + row) * p.ld_src + c]
                                            : 0.f;
-            for (uint64_t e = beg; e < end; ++e)
-                acc += p.src[static_cast<uint64_t>(p.col[e]) * p.ld_src + c];
+            for (uint64_t e = beg; e < s0; ++e) acc += p.src[static_cast<uint64_t>(p.col[e]) * p.ld_src + c];
+            for (uint64_t e = s1; e < end; ++e) acc += p.src[static_cast<uint64_t>(p.col[e]) * p.ld_src + c];
+            if (p.partial) acc += p.partial[row * p.ld_partial + c];
             acc *= scale;
             if (p.add) acc += p.add[row * p.ld_add + c];
             if (p.relu) acc = fmaxf(acc, 0.f);
             if (p.out) p.out[row * p.ld_out + c] = acc;
             if (p.out_hi) split_bf16(acc, p.out_hi[row * p.ld_split + c], p.out_lo[row * p.ld_split + c]);
         }
+    }
+}
+
+// Per-row sub-range of column ids in [lo, hi): rows are sorted, so it is contiguous.
+__global__ void row_split_kernel(const uint64_t* row_ptr, const uint32_t* col, uint32_t rows,
+                                 uint32_t lo, uint32_t hi, uint64_t* seg_lo, uint64_t* seg_hi) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < rows; v += gridDim.x * blockDim.x) {
+        auto lower = [&](uint32_t key) {
+            uint64_t a = row_ptr[v], b = row_ptr[v + 1];
+            while (a < b) {
+                const uint64_t m = a + (b - a) / 2;
+                if (col[m] < key) a = m + 1;
+                else b = m;
+            }
+            return a;
+        };
+        seg_lo[v] = lower(lo);
+        seg_hi[v] = lower(hi);
     }
 }
 
@@ -296,12 +336,16 @@ int aggregate_impl(const gdx_aggregate_args* a, int variant, gdx_stream stream) 
     GDX_REQUIRE(!a->out || a->ld_out >= a->width, GDX_INPUT, "gdx_aggregate: ld_out < width");
     GDX_REQUIRE(!a->out_hi == !a->out_lo, GDX_INPUT, "gdx_aggregate: out_hi/out_lo must pair");
     if (a->rows == 0) return GDX_OK;
-    AggParams p{a->row_ptr, a->row_end, a->col, a->rows, a->width / 4, a->src, a->ld_src,
+    GDX_REQUIRE(!a->skip_lo == !a->skip_hi, GDX_INPUT, "gdx_aggregate: skip_lo/skip_hi must pair");
+    GDX_REQUIRE(!a->partial || a->ld_partial >= a->width, GDX_INPUT, "gdx_aggregate: ld_partial < width");
+    AggParams p{a->row_ptr, a->row_end, a->skip_lo, a->skip_hi, a->partial, a->ld_partial, a->col,
+                a->rows, a->width / 4, a->src, a->ld_src,
                 static_cast<uint32_t>(a->ld_src * 4), a->self_coef, a->self_base, a->post_scale,
                 a->add, a->ld_add, a->relu, a->out, a->ld_out, a->out_hi, a->out_lo, a->ld_split};
     const bool vec = a->width % 4 == 0 && a->ld_src % 4 == 0 && aligned16(a->src) && a->width <= 4096 &&
                      a->ld_src * 4 < (1ull << 32) &&
                      (!a->add || (a->ld_add % 4 == 0 && aligned16(a->add))) &&
+                     (!a->partial || (a->ld_partial % 4 == 0 && aligned16(a->partial))) &&
                      (!a->out || (a->ld_out % 4 == 0 && aligned16(a->out))) &&
                      (!a->out_hi || (a->ld_split % 4 == 0 && (reinterpret_cast<uintptr_t>(a->out_hi) & 7) == 0 &&
                                      (reinterpret_cast<uintptr_t>(a->out_lo) & 7) == 0));
@@ -326,4 +370,16 @@ extern "C" int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream) {
 
 extern "C" int gdx_aggregate_variant(const gdx_aggregate_args* a, int variant, gdx_stream stream) {
     return gdx::aggregate_impl(a, variant, stream);
+}
+
+extern "C" int gdx_row_split(const uint64_t* row_ptr, const uint32_t* col, uint32_t rows, uint32_t lo,
+                             uint32_t hi, uint64_t* seg_lo, uint64_t* seg_hi, gdx_stream stream) {
+    GDX_REQUIRE(row_ptr && seg_lo && seg_hi && (col || rows == 0), GDX_INPUT, "gdx_row_split: null pointer");
+    GDX_REQUIRE(lo <= hi, GDX_INPUT, "gdx_row_split: lo > hi");
+    if (!rows) return GDX_OK;
+    unsigned blocks = (rows + 255) / 256;
+    if (blocks > 148u * 32u) blocks = 148u * 32u;
+    gdx::row_split_kernel<<<blocks, 256, 0, gdx::as_cuda(stream)>>>(row_ptr, col, rows, lo, hi, seg_lo, seg_hi);
+    gdx::note_launch();
+    return gdx::check_launch("gdx_row_split");
 }

@@ -96,24 +96,31 @@ def dense(rows: int, cols: int, device, zero: bool = True) -> torch.Tensor:
 
 def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_split: Split | None = None,
               self_coef: float = 0.0, self_base: int = 0, post_scale=None, add=None, relu=False,
-              row_end=None, stream=None, variant: int = 0):
-    """K1/K3 (see include/gdx.h gdx_aggregate)."""
+              row_end=None, row_begin=None, skip=None, partial=None, stream=None, variant: int = 0):
+    """K1/K3 (see include/gdx.h gdx_aggregate).  row_begin/row_end override the CSR
+    row bounds; skip = (seg_lo, seg_hi) excludes a per-row sub-range; partial adds
+    precomputed partial sums before the epilogue."""
     a = AggregateArgs()
-    a.row_ptr = g.row_ptr.data_ptr()
-    a.row_end = ptr(row_end)
+    a.row_ptr = g.row_ptr.data_ptr() if row_begin is None else row_begin.data_ptr()
+    a.row_end = ptr(row_end) if row_begin is None else (row_end.data_ptr() if row_end is not None
+                                                         else g.row_ptr[1:].data_ptr())
+    if skip is not None:
+        a.skip_lo, a.skip_hi = skip[0].data_ptr(), skip[1].data_ptr()
+    if partial is not None:
+        a.partial, a.ld_partial = partial.data_ptr(), partial.stride(0)
     a.col = g.col.data_ptr()
     a.rows = g.rows
     a.width = width
     a.src = src.data_ptr()
-    a.ld_src = src.shape[-1] if src.dim() == 2 else width
+    a.ld_src = src.stride(0) if src.dim() == 2 else width
     a.self_coef = self_coef
     a.self_base = self_base
     a.post_scale = ptr(post_scale)
     a.add = ptr(add)
-    a.ld_add = add.shape[-1] if add is not None else 0
+    a.ld_add = add.stride(0) if add is not None else 0
     a.relu = int(relu)
     a.out = ptr(out)
-    a.ld_out = out.shape[-1] if out is not None else 0
+    a.ld_out = out.stride(0) if out is not None else 0
     if out_split is not None:
         a.out_hi, a.out_lo, a.ld_split = out_split.hi.data_ptr(), out_split.lo.data_ptr(), out_split.ld
     if variant:

@@ -162,6 +162,14 @@ class FullGraphTrainer:
         lci = g.col_indices()[base:int(ro[self.hi])]
         self.csr = DeviceCSR.upload(lro, lci, d)
         self.nnz_local = len(lci)
+        # per-row sub-range of locally owned sources: aggregated while the all-gather runs
+        self.overlap = world > 1
+        if self.overlap:
+            self.seg_lo = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
+            self.seg_hi = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
+            call("gdx_row_split", self.csr.row_ptr.data_ptr(), self.csr.col.data_ptr(), self.nloc,
+                 self.lo, self.hi, self.seg_lo.data_ptr(), self.seg_hi.data_ptr(), stream_handle())
+            self.nnz_local_src = int((self.seg_hi - self.seg_lo)[:self.nloc].sum().item())
         deg = np.diff(lro).astype(np.float64)
         self.inv_deg = torch.from_numpy(np.where(deg > 0, 1.0 / np.maximum(deg, 1), 0.0)
                                         .astype(np.float32)).to(d)
@@ -188,6 +196,7 @@ class FullGraphTrainer:
             weights = init_weights(cfg, weight_seed)
         self.set_weights(weights)
         self.dlogits = dense(self.nloc, self.layers[-1].w, d)
+        self.partial = dense(self.nloc, max(L.w for L in self.layers), d) if self.overlap else None
         self.dH = [dense(self.nloc, pad8(cfg.dims[l]), d) for l in range(cfg.layers)]
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=d)
         self.keep_activations = False
@@ -228,7 +237,13 @@ class FullGraphTrainer:
         a.record()
         aggregate(csr, src, width, **kw)
         b.record()
-        nnz, rows = self.nnz_local, csr.rows
+        rows = csr.rows
+        if "row_begin" in kw:               # local-source pass of a split aggregation
+            nnz = self.nnz_local_src
+        elif "skip" in kw:                  # remote-source pass (+ partial read)
+            nnz = self.nnz_local - self.nnz_local_src
+        else:
+            nnz = self.nnz_local
         ev.append((a, b, 4 * nnz + 8 * (rows + 1) + 4 * width * nnz + 4 * width * rows))
 
     def kernel_event_summary(self):
@@ -236,6 +251,20 @@ class FullGraphTrainer:
         torch.cuda.synchronize()
         ev = getattr(self, "_events", None) or []
         return (sum(a.elapsed_time(b) for a, b, _ in ev), len(ev), sum(x for _, _, x in ev))
+
+    def _exchange_aggregate(self, full: torch.Tensor, width: int, **epi):
+        """All-gather `full` and aggregate the owned rows from it.  With N > 1 the
+        locally owned source block is aggregated while NCCL moves the remote blocks,
+        then the remote sources finish the rows with the fused epilogue."""
+        work = self.exchange.allgather_rows_async(full) if self.overlap else None
+        if work is None:
+            if self.overlap:
+                pass  # already gathered synchronously (unequal blocks)
+            return self._agg(self.csr, full, width, **epi)
+        P = self.partial[:, :pad4(width)] if self.partial.shape[1] != pad4(width) else self.partial
+        self._agg(self.csr, full, width, out=P, row_begin=self.seg_lo, row_end=self.seg_hi)
+        work.wait()
+        return self._agg(self.csr, full, width, skip=(self.seg_lo, self.seg_hi), partial=P, **epi)
 
     # ---- collectives ----
     def _allgather_rows(self, full: torch.Tensor):
@@ -258,16 +287,15 @@ class FullGraphTrainer:
                 gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s)
             else:
                 gemm_tn(A, L.Wsp, c0=own)
-            self._allgather_rows(L.Zfull)
             if cfg.kind == "sage":
-                self._agg(self.csr, L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=0.0,
-                          self_base=self.lo, post_scale=self.inv_deg, add=L.S, relu=relu)
+                self._exchange_aggregate(L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=0.0,
+                                         self_base=self.lo, post_scale=self.inv_deg, add=L.S, relu=relu)
             elif cfg.kind == "gcn":
-                self._agg(self.csr, L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=1.0,
-                          self_base=self.lo, post_scale=self.gcn_s, relu=relu)
+                self._exchange_aggregate(L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=1.0,
+                                         self_base=self.lo, post_scale=self.gcn_s, relu=relu)
             else:
-                self._agg(self.csr, L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=1.0,
-                          self_base=self.lo, relu=relu)
+                self._exchange_aggregate(L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=1.0,
+                                         self_base=self.lo, relu=relu)
             A = L.Hsp
             if self.keep_activations:
                 acts.append(L.Hout[:self.nloc, :L.fout].clone())
@@ -292,16 +320,15 @@ class FullGraphTrainer:
                 call("gdx_grad_prepare", dH.data_ptr(), dH.shape[1], _lib.ptr(mask), L.Hout.shape[1],
                      self.nloc, L.w, _lib.ptr(scale), None, 0, own.data_ptr(), own.shape[1],
                      None, None, 0, stream_handle())
-            self._allgather_rows(L.dfull)
             # dZ = agg^T(gs): SAGE -> G[:, w:2w]; GCN/SUM -> G (all columns)
             if cfg.kind == "sage":
                 Gn = _SplitView(L.G, L.w)
-                self._agg(self.csr, L.dfull, L.w, out_split=Gn, self_coef=0.0, self_base=self.lo)
+                self._exchange_aggregate(L.dfull, L.w, out_split=Gn, self_coef=0.0, self_base=self.lo)
             elif cfg.kind == "gcn":
-                self._agg(self.csr, L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo,
-                          post_scale=self.gcn_s)
+                self._exchange_aggregate(L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo,
+                                         post_scale=self.gcn_s)
             else:
-                self._agg(self.csr, L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo)
+                self._exchange_aggregate(L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo)
             # dH_{l} = G W_cat  (before this layer's update); W_cat read MN-major in place
             if l > 0:
                 dprev = self.dH[l]
@@ -374,6 +401,17 @@ class RowExchange:
         self.rank, self.world, self.pg = rank, world, pg
         sizes = np.diff(self.offsets)
         self.equal_blocks = bool(np.all(sizes == sizes[0]))
+
+    def allgather_rows_async(self, full: torch.Tensor):
+        """Start the all-gather on NCCL's stream (equal blocks); returns a handle whose
+        wait() orders the current stream after it, or None when nothing to do."""
+        if self.world == 1 or not self.equal_blocks:
+            self.allgather_rows(full)
+            return None
+        import torch.distributed as dist
+        n = int(self.offsets[-1])
+        lo, hi = int(self.offsets[self.rank]), int(self.offsets[self.rank + 1])
+        return dist.all_gather_into_tensor(full[:n], full[lo:hi], group=self.pg, async_op=True)
 
     def allgather_rows(self, full: torch.Tensor):
         if self.world == 1:
