@@ -225,7 +225,9 @@ def main():
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = True  # collectives get SMs ahead of the aggregation
+        dist.init_process_group("nccl", device_id=dev, pg_options=opts)
         pg = dist.group.WORLD
 
     import paper_2311_06837_b200 as G

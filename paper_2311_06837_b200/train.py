@@ -91,7 +91,7 @@ class _Layer:
         # master weights, row pitch == split pitch so the fused SGD can index both
         self.W = torch.zeros((self.nz, self.fin_ld), dtype=torch.float32, device=d)
         self.Wsp = Split(self.nz, self.k, d, ld=self.fin_ld)  # forward B (nz x k); MN-major B of dH
-        self.dW = torch.zeros((self.nz, self.fin_ld), dtype=torch.float32, device=d)
+        self.dW = None  # view into the trainer's flat gradient buffer (set by the trainer)
         kb = max(1, math.ceil(nloc / 64))
         ntiles = max(1, math.ceil(fin / (256 if fin > 128 else (128 if fin > 64 else 64))))
         self.split_k = max(1, min(kb, splitk_target // ntiles))
@@ -163,7 +163,8 @@ class FullGraphTrainer:
         self.csr = DeviceCSR.upload(lro, lci, d)
         self.nnz_local = len(lci)
         # per-row sub-range of locally owned sources: aggregated while the all-gather runs
-        self.overlap = world > 1
+        import os
+        self.overlap = world > 1 and os.environ.get("GDX_OVERLAP", "1") != "0"
         if self.overlap:
             self.seg_lo = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
             self.seg_hi = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
@@ -192,6 +193,13 @@ class FullGraphTrainer:
         for l in range(cfg.layers):
             self.layers.append(_Layer(cfg.kind, cfg.dims[l], cfg.dims[l + 1], self.nloc,
                                       self.nrows_gather, d, 2 * sm, l == 0))
+        # all weight gradients (+ the loss) in one flat buffer: one all-reduce per epoch
+        sizes = [L.nz * L.fin_ld for L in self.layers]
+        self.grad_flat = torch.zeros(sum(sizes) + 1, dtype=torch.float32, device=d)
+        off = 0
+        for L, sz in zip(self.layers, sizes):
+            L.dW = self.grad_flat[off:off + sz].view(L.nz, L.fin_ld)
+            off += sz
         if weights is None:
             weights = init_weights(cfg, weight_seed)
         self.set_weights(weights)
@@ -256,10 +264,11 @@ class FullGraphTrainer:
         """All-gather `full` and aggregate the owned rows from it.  With N > 1 the
         locally owned source block is aggregated while NCCL moves the remote blocks,
         then the remote sources finish the rows with the fused epilogue."""
-        work = self.exchange.allgather_rows_async(full) if self.overlap else None
-        if work is None:
-            if self.overlap:
-                pass  # already gathered synchronously (unequal blocks)
+        if not self.overlap:
+            self.exchange.allgather_rows(full)
+            return self._agg(self.csr, full, width, **epi)
+        work = self.exchange.allgather_rows_async(full)
+        if work is None:  # gathered synchronously (unequal blocks)
             return self._agg(self.csr, full, width, **epi)
         P = self.partial[:, :pad4(width)] if self.partial.shape[1] != pad4(width) else self.partial
         self._agg(self.csr, full, width, out=P, row_begin=self.seg_lo, row_end=self.seg_hi)
@@ -336,18 +345,23 @@ class FullGraphTrainer:
             # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
             gemm_tn(L.G, A_in, c0=L.ws, split_k=L.split_k, a_mn=True, b_mn=True)
-            if self.world == 1:
+            if self.world == 1:  # reduce split-K partials and apply SGD in one pass
                 call("gdx_splitk_reduce", L.ws.data_ptr(), L.split_k, L.nz * L.fin_ld, L.nz, L.fin,
                      L.fin_ld, L.dW.data_ptr(), L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(),
                      L.Wsp.lo.data_ptr(), stream_handle())
-            else:
+            else:                # reduce partials; SGD after the epoch's single all-reduce
                 call("gdx_splitk_reduce", L.ws.data_ptr(), L.split_k, L.nz * L.fin_ld, L.nz, L.fin,
                      L.fin_ld, L.dW.data_ptr(), None, 0.0, None, None, stream_handle())
-                self._allreduce(L.dW)
-                call("gdx_splitk_reduce", L.dW.data_ptr(), 1, 0, L.nz, L.fin, L.fin_ld, None,
-                     L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(), L.Wsp.lo.data_ptr(), stream_handle())
             if l > 0:
                 dH = self.dH[l]
+        if self.world > 1:
+            # one all-reduce for every layer's dW and the loss, then SGD (+ split refresh)
+            self.grad_flat[-1:].copy_(self.loss_acc)
+            self._allreduce(self.grad_flat)
+            self.loss_acc.copy_(self.grad_flat[-1:])
+            for L in self.layers:
+                call("gdx_splitk_reduce", L.dW.data_ptr(), 1, 0, L.nz, L.fin, L.fin_ld, None,
+                     L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(), L.Wsp.lo.data_ptr(), stream_handle())
 
     def train_epoch(self, sync_loss: bool = True):
         """Forward, loss, backward, SGD.  Returns the loss (host float) if sync_loss."""
@@ -357,8 +371,7 @@ class FullGraphTrainer:
         call("gdx_softmax_xent", logits.data_ptr(), logits.shape[1], self.nloc, self.cfg.classes,
              self.labels.data_ptr(), 1.0 / self.n, self.dlogits.data_ptr(), self.dlogits.shape[1],
              self.loss_acc.data_ptr(), stream_handle())
-        self._allreduce(self.loss_acc)
-        self.backward_and_step()
+        self.backward_and_step()  # (multi-GPU: the loss rides on the gradient all-reduce)
         if sync_loss:
             return float(self.loss_acc.item()) / self.n
         return None

@@ -24,7 +24,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    opts = dist.ProcessGroupNCCL.Options()
+    opts.is_high_priority_stream = True  # collectives get SMs ahead of the aggregation
+    dist.init_process_group("nccl", device_id=dev, pg_options=opts)
     import paper_2311_06837_b200 as G
     from paper_2311_06837_b200.train import FullGraphTrainer, ModelConfig, init_weights
 
