@@ -104,6 +104,10 @@ def port() -> C.CDLL:
         L.gro_train_epoch.argtypes = [C.c_uint32, _u64p, _u32p, _f64p, _i32p, C.c_uint32,
                                       C.POINTER(_ModelC), _f64p, C.c_double, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_uint32, C.c_int]
+        L.gro_train_epoch_masked.restype = C.c_double
+        L.gro_train_epoch_masked.argtypes = [C.c_uint32, _u64p, _u32p, _f64p, _i32p, C.c_uint32,
+                                             C.POINTER(_ModelC), _f64p, C.c_double, C.c_void_p,
+                                             C.c_uint32, C.c_double, C.c_int]
         _port = L
     return _port
 
@@ -373,6 +377,18 @@ def train_epoch(g: CSR, x: np.ndarray, labels: np.ndarray, model: Model, w: np.n
     if not want_state:
         return loss
     return loss, grads, _split_acts(acts, g.n, model.dims[1:]), _split_acts(dacts, g.n, model.dims[1:])
+
+
+def train_epoch_masked(g: CSR, x: np.ndarray, labels: np.ndarray, model: Model, w: np.ndarray,
+                       lr: float, loss_rows: int, loss_count: float, nthreads: int = 1):
+    """Epoch with the loss over rows < loss_rows / loss_count.  lr == 0 returns the
+    gradients without updating (for summing several subgraphs).  Returns (loss, grads)."""
+    grads = np.zeros(model.weight_count(), np.float64)
+    loss = port().gro_train_epoch_masked(g.n, g.row_offsets, g.cols, np.ascontiguousarray(x, np.float64),
+                                         np.ascontiguousarray(labels, np.int32), int(model.dims[-1]),
+                                         C.byref(model._c), w, lr, _ptr(grads), loss_rows, loss_count,
+                                         nthreads)
+    return loss, grads
 
 
 def make_labels(n: int, classes: int, seed: int) -> np.ndarray:

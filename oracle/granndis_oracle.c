@@ -739,20 +739,21 @@ void gro_model_forward(uint32_t n, const uint64_t* ro, const uint32_t* ci, const
     free_state(m, &st);
 }
 
-double gro_train_epoch(uint32_t n, const uint64_t* ro, const uint32_t* ci, const double* x,
-                       const int32_t* labels, uint32_t C, const gro_model* m, double* w,
-                       double lr, double* grads, double* acts, double* dacts, uint32_t row_limit,
-                       int nthreads) {
+static double train_impl(uint32_t n, const uint64_t* ro, const uint32_t* ci, const double* x,
+                         const int32_t* labels, uint32_t C, const gro_model* m, double* w,
+                         double lr, double* grads, double* acts, double* dacts, uint32_t row_limit,
+                         uint32_t loss_rows, double loss_count, int nthreads) {
     uint32_t L = m->layers;
     uint32_t rows = row_limit < n ? row_limit : n;
+    if (loss_rows > rows) loss_rows = rows;
     fwd_state st;
     forward_impl(n, rows, ro, ci, x, m, w, &st, nthreads);
 
-    /* softmax cross-entropy, mean over `rows` rows */
+    /* softmax cross-entropy over rows < loss_rows, normalised by loss_count */
     double* dH = (double*)calloc((size_t)n * C, sizeof(double));
     double loss = 0.0;
     const double* logits = st.H[L];
-    for (uint32_t v = 0; v < rows; ++v) {
+    for (uint32_t v = 0; v < loss_rows; ++v) {
         const double* z = logits + (size_t)v * C;
         double mx = z[0];
         for (uint32_t c = 1; c < C; ++c) mx = z[c] > mx ? z[c] : mx;
@@ -761,9 +762,9 @@ double gro_train_epoch(uint32_t n, const uint64_t* ro, const uint32_t* ci, const
         double lse = mx + log(sum);
         loss += lse - z[labels[v]];
         for (uint32_t c = 0; c < C; ++c)
-            dH[(size_t)v * C + c] = (exp(z[c] - lse) - (c == (uint32_t)labels[v] ? 1.0 : 0.0)) / rows;
+            dH[(size_t)v * C + c] = (exp(z[c] - lse) - (c == (uint32_t)labels[v] ? 1.0 : 0.0)) / loss_count;
     }
-    loss /= rows;
+    loss /= loss_count;
 
     uint64_t wc = gro_weight_count(m);
     double* dW = (double*)calloc(wc, sizeof(double));
@@ -817,7 +818,8 @@ double gro_train_epoch(uint32_t n, const uint64_t* ro, const uint32_t* ci, const
     }
     (void)dacts_off_total;
     if (grads) memcpy(grads, dW, sizeof(double) * wc);
-    for (uint64_t k = 0; k < wc; ++k) w[k] -= lr * dW[k];
+    if (lr != 0.0)
+        for (uint64_t k = 0; k < wc; ++k) w[k] -= lr * dW[k];
     if (acts) {
         size_t off = 0;
         for (uint32_t l = 1; l <= L; ++l) {
@@ -830,4 +832,21 @@ double gro_train_epoch(uint32_t n, const uint64_t* ro, const uint32_t* ci, const
     free(dH);
     free_state(m, &st);
     return loss;
+}
+
+double gro_train_epoch(uint32_t n, const uint64_t* ro, const uint32_t* ci, const double* x,
+                       const int32_t* labels, uint32_t C, const gro_model* m, double* w,
+                       double lr, double* grads, double* acts, double* dacts, uint32_t row_limit,
+                       int nthreads) {
+    uint32_t rows = row_limit < n ? row_limit : n;
+    return train_impl(n, ro, ci, x, labels, C, m, w, lr, grads, acts, dacts, row_limit, rows,
+                      (double)rows, nthreads);
+}
+
+double gro_train_epoch_masked(uint32_t n, const uint64_t* ro, const uint32_t* ci, const double* x,
+                              const int32_t* labels, uint32_t C, const gro_model* m, double* w,
+                              double lr, double* grads, uint32_t loss_rows, double loss_count,
+                              int nthreads) {
+    return train_impl(n, ro, ci, x, labels, C, m, w, lr, grads, NULL, NULL, n, loss_rows, loss_count,
+                      nthreads);
 }

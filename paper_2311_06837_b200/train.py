@@ -135,7 +135,12 @@ class FullGraphTrainer:
 
     def __init__(self, g: Graph, cfg: ModelConfig, *, rank: int = 0, world: int = 1,
                  feature_seed: int = 1, label_seed: int = 2, weights=None, weight_seed: int = 3,
-                 pg=None, device=None):
+                 pg=None, device=None, subgraph=None):
+        """subgraph: optional DependencySubgraph of this rank (EAS / shared-preload
+        mode): the rank trains on its own preloaded inner + halo
+        vertices, the loss covers its inner vertices, and only the weight gradients
+        are exchanged (all-reduce over pg).  Without it, ranks own contiguous row
+        blocks of the whole graph and all-gather each layer's rows."""
         require_cuda()
         if cfg.kind not in ("sage", "gcn", "sum"):
             raise InputError(f"unknown model kind {cfg.kind!r}")
@@ -145,46 +150,74 @@ class FullGraphTrainer:
         self.d = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         d = self.d
         n = g.num_vertices()
-        # ceil-sized contiguous row blocks: rank r owns [r*B, min((r+1)*B, n)); the
-        # gathered buffers hold world*B rows so every all-gather block is B rows.
-        B = -(-n // world)
-        self.block = B
-        self.offsets = np.minimum(np.arange(world + 1, dtype=np.int64) * B, n)
-        self.lo, self.hi = int(self.offsets[rank]), int(self.offsets[rank + 1])
-        self.nloc = self.hi - self.lo
         self.n = n
-        self.nrows_gather = world * B
-        self.exchange = RowExchange(np.arange(world + 1, dtype=np.int64) * B, rank, world, pg)
-        # local CSR rows [lo, hi) with global column ids
-        ro = g.row_offsets()
-        base = int(ro[self.lo])
-        lro = (ro[self.lo:self.hi + 1] - np.uint64(base)).astype(np.uint64)
-        lci = g.col_indices()[base:int(ro[self.hi])]
-        self.csr = DeviceCSR.upload(lro, lci, d)
-        self.nnz_local = len(lci)
+        F = cfg.dims[0]
+        self.F = F
+        self.subgraph_mode = subgraph is not None
+        if not self.subgraph_mode:
+            # ceil-sized contiguous row blocks: rank r owns [r*B, min((r+1)*B, n)); the
+            # gathered buffers hold world*B rows so every all-gather block is B rows.
+            B = -(-n // world)
+            self.block = B
+            self.offsets = np.minimum(np.arange(world + 1, dtype=np.int64) * B, n)
+            self.lo, self.hi = int(self.offsets[rank]), int(self.offsets[rank + 1])
+            self.nloc = self.hi - self.lo
+            self.nrows_gather = world * B
+            self.exchange = RowExchange(np.arange(world + 1, dtype=np.int64) * B, rank, world, pg)
+            ro = g.row_offsets()
+            base = int(ro[self.lo])
+            lro = (ro[self.lo:self.hi + 1] - np.uint64(base)).astype(np.uint64)
+            lci = g.col_indices()[base:int(ro[self.hi])]
+            self.csr = DeviceCSR.upload(lro, lci, d)
+            self.nnz_local = len(lci)
+            deg = torch.from_numpy(np.diff(lro).astype(np.float64)).to(d)
+            self.loss_rows, self.loss_count = self.nloc, float(n)
+            # inputs: rows of the keyed streams (feature row v starts at draw v*F)
+            self.X = dense(self.nloc, F, d)
+            call("gdx_init_uniform", feature_seed, FEAT_TAG, 0, self.lo * F, self.nloc, F, -0.5, 0.5,
+                 self.X.data_ptr(), self.X.shape[1], stream_handle())
+            self.labels = torch.empty(max(self.nloc, 1), dtype=torch.int32, device=d)
+            call("gdx_init_labels", label_seed, self.lo, self.nloc, cfg.classes,
+                 self.labels.data_ptr(), stream_handle())
+        else:
+            from .gnn import LocalSubgraph
+            loc = LocalSubgraph(subgraph, g, d)
+            self.local = loc
+            self.lo, self.nloc = 0, loc.n
+            self.hi = loc.n
+            self.nrows_gather = loc.n
+            self.exchange = RowExchange(np.array([0, loc.n], np.int64), 0, 1, None)
+            self.csr = loc.csr
+            self.nnz_local = int(loc.lptr[-1].item())
+            deg = (loc.lptr[1:] - loc.lptr[:-1]).double()
+            self.loss_rows = loc.upto(0)  # inner vertices come first (hop 0)
+            cnt = torch.tensor([float(self.loss_rows)], dtype=torch.float64, device=d)
+            if world > 1:
+                import torch.distributed as dist
+                dist.all_reduce(cnt, group=pg)
+            self.loss_count = float(cnt.item())
+            # preloaded inputs: the global stream rows of every local vertex
+            Xall = dense(n, F, d)
+            call("gdx_init_uniform", feature_seed, FEAT_TAG, 0, 0, n, F, -0.5, 0.5, Xall.data_ptr(),
+                 Xall.shape[1], stream_handle())
+            self.X = dense(self.nloc, F, d)
+            call("gdx_gather_rows", Xall.data_ptr(), Xall.shape[1], loc.l2g.data_ptr(), self.nloc, F,
+                 self.X.data_ptr(), self.X.shape[1], stream_handle())
+            del Xall
+            lab = torch.empty(max(n, 1), dtype=torch.int32, device=d)
+            call("gdx_init_labels", label_seed, 0, n, cfg.classes, lab.data_ptr(), stream_handle())
+            self.labels = lab[loc.l2g[:max(self.nloc, 1)].long()].contiguous()
+        self.inv_deg = torch.where(deg > 0, 1.0 / deg.clamp(min=1), torch.zeros_like(deg)).float()
+        self.gcn_s = (1.0 / torch.sqrt(deg + 1.0)).float()
         # per-row sub-range of locally owned sources: aggregated while the all-gather runs
         import os
-        self.overlap = world > 1 and os.environ.get("GDX_OVERLAP", "1") != "0"
+        self.overlap = (not self.subgraph_mode) and world > 1 and os.environ.get("GDX_OVERLAP", "1") != "0"
         if self.overlap:
             self.seg_lo = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
             self.seg_hi = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
             call("gdx_row_split", self.csr.row_ptr.data_ptr(), self.csr.col.data_ptr(), self.nloc,
                  self.lo, self.hi, self.seg_lo.data_ptr(), self.seg_hi.data_ptr(), stream_handle())
             self.nnz_local_src = int((self.seg_hi - self.seg_lo)[:self.nloc].sum().item())
-        deg = np.diff(lro).astype(np.float64)
-        self.inv_deg = torch.from_numpy(np.where(deg > 0, 1.0 / np.maximum(deg, 1), 0.0)
-                                        .astype(np.float32)).to(d)
-        self.gcn_s = torch.from_numpy((1.0 / np.sqrt(deg + 1.0)).astype(np.float32)).to(d)
-        # inputs: features of owned rows (stream (feature_seed, "feat") row-major over all
-        # vertices, so row v starts at draw v*F), labels of owned rows
-        F = cfg.dims[0]
-        self.F = F
-        self.X = dense(self.nloc, F, d)
-        call("gdx_init_uniform", feature_seed, FEAT_TAG, 0, self.lo * F, self.nloc, F, -0.5, 0.5,
-             self.X.data_ptr(), self.X.shape[1], stream_handle())
-        self.labels = torch.empty(max(self.nloc, 1), dtype=torch.int32, device=d)
-        call("gdx_init_labels", label_seed, self.lo, self.nloc, cfg.classes, self.labels.data_ptr(),
-             stream_handle())
         self.Xsp = Split(self.nloc, F, d)
         self._refresh_input_splits()
         # layers
@@ -280,7 +313,10 @@ class FullGraphTrainer:
         self.exchange.allgather_rows(full)
 
     def _allreduce(self, t: torch.Tensor):
-        self.exchange.allreduce(t)
+        """Gradient all-reduce over every rank (both modes)."""
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t, group=self.pg)
 
     # ---- one epoch ----
     def forward(self):
@@ -368,12 +404,12 @@ class FullGraphTrainer:
         self.loss_acc.zero_()
         logits = self.forward()
         Lz = self.layers[-1]
-        call("gdx_softmax_xent", logits.data_ptr(), logits.shape[1], self.nloc, self.cfg.classes,
-             self.labels.data_ptr(), 1.0 / self.n, self.dlogits.data_ptr(), self.dlogits.shape[1],
-             self.loss_acc.data_ptr(), stream_handle())
+        call("gdx_softmax_xent", logits.data_ptr(), logits.shape[1], self.loss_rows, self.cfg.classes,
+             self.labels.data_ptr(), 1.0 / self.loss_count, self.dlogits.data_ptr(),
+             self.dlogits.shape[1], self.loss_acc.data_ptr(), stream_handle())
         self.backward_and_step()  # (multi-GPU: the loss rides on the gradient all-reduce)
         if sync_loss:
-            return float(self.loss_acc.item()) / self.n
+            return float(self.loss_acc.item()) / self.loss_count
         return None
 
     # ---- CUDA graph of one epoch (removes host launch overhead) ----
@@ -394,7 +430,7 @@ class FullGraphTrainer:
     def replay(self, sync_loss: bool = False):
         self.graph.replay()
         if sync_loss:
-            return float(self.loss_acc.item()) / self.n
+            return float(self.loss_acc.item()) / self.loss_count
         return None
 
     def aggregation_edges_per_epoch(self) -> int:

@@ -69,3 +69,43 @@ def test_reddit_width_layer_parity(cuda):
     """602-wide inputs (Reddit feature width), 41 classes, one epoch."""
     lg, lr = run_pair("sage", 2000, 40.0, [602, 64, 41], 2, 0.1)
     assert np.all(np.abs(lg - lr) <= 1e-3)
+
+
+@pytest.mark.parametrize("kind,m,k", [("gcn", 1, 15), ("sage", 2, 4), ("gcn", 3, O.UNLIMITED)])
+def test_subgraph_training_matches_oracle(cuda, kind, m, k):
+    """EAS / preload mode: train on one server's preloaded inner + halo subgraph,
+    loss on its inner vertices; the oracle runs the same epoch on the induced
+    local graph (hop-ordered local ids, inner first)."""
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.train import FullGraphTrainer, ModelConfig, init_weights
+
+    n, dims = 3000, [48, 32, 32, 8]
+    g = G.gen_random_graph(n, 12.0, 9)
+    p = G.partition_random(g, 4, 2)
+    sub = G.extract_sampled(g, p, 1, G.SamplingConfig(m, k, 5))
+    cfg = ModelConfig(kind, dims, lr=0.5)
+    w0 = init_weights(cfg, 3)
+    tr = FullGraphTrainer(g, cfg, weights=w0, subgraph=sub)
+    # the oracle's local graph: same numbering as the engine (hop, id) and induced rows
+    hop = sub.hop_array(n)
+    order = np.lexsort((np.arange(n), hop))[: len(sub.inner_vertices) + len(sub.halo_vertices)]
+    local = np.full(n, -1, np.int64)
+    local[order] = np.arange(len(order))
+    ro, ci = g.row_offsets(), g.col_indices()
+    rows, cols = [], []
+    for i, v in enumerate(order):
+        nb = local[ci[ro[v]:ro[v + 1]]]
+        nb = nb[nb >= 0]
+        rows.append(len(nb))
+        cols.append(nb)
+    lro = np.concatenate([[0], np.cumsum(rows)]).astype(np.uint64)
+    lc = O.CSR(len(order), lro, np.concatenate(cols).astype(np.uint32))
+    x = O.make_features(n, dims[0], 1).astype(np.float32).astype(np.float64)[order]
+    lab = O.make_labels(n, dims[-1], 2)[order]
+    model = O.Model({"sage": O.SAGE, "gcn": O.GCN}[kind], dims)
+    w = np.concatenate([a.astype(np.float32).astype(np.float64).ravel() for a in w0])
+    n_inner = len(sub.inner_vertices)
+    for e in range(6):
+        lg = tr.train_epoch()
+        loss, grads = O.train_epoch_masked(lc, x, lab, model, w, 0.5, n_inner, float(n_inner), nthreads=4)
+        assert abs(lg - loss) <= 1e-3, (e, lg, loss)
