@@ -33,6 +33,23 @@ sys.path.insert(0, HERE)
 REDDIT = dict(n=232965, degree=491.99, seed=11, dims=[602, 64, 64, 41])
 METRIC = "GCN epoch ms & aggregation edges/s, synthetic Reddit-shape graph, 1/2/4/8 B200"
 MODEL = "sage"
+# BASELINE.json configs beyond the headline (configs[1]); selected with --config
+CONFIGS = {
+    "reddit-sage": dict(n=232965, degree=491.99, seed=11, kind="sage", dims=[602, 64, 64, 41],
+                        mode="full", lr=0.1,
+                        workload="reddit-shape full-graph 3-layer GraphSAGE-mean training epoch "
+                                 "(BASELINE configs[1])"),
+    "reddit-gcn56-eas": dict(n=232965, degree=491.99, seed=11, kind="gcn", dims=[602] + [64] * 55 + [41],
+                             mode="eas", eas=(1, 15, 3), lr=0.01,
+                             workload="reddit-shape 56-layer normalised GCN, expansion-aware sampling "
+                                      "EAS(m=1,k=15,seed=3), one emulated server per GPU (random "
+                                      "partition), loss on inner vertices (BASELINE configs[2])"),
+    "products-gcn": dict(n=2449029, degree=25.26, seed=13, kind="gcn", dims=[100, 64, 64, 47],
+                         mode="full", lr=0.1,
+                         workload="ogbn-products-shape full-graph 3-layer normalised GCN, features "
+                                  "resident on every GPU (shared preload with one server) "
+                                  "(BASELINE configs[3])"),
+}
 
 
 def parse():
@@ -45,8 +62,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
-    ap.add_argument("--n", type=int, default=REDDIT["n"])
-    ap.add_argument("--degree", type=float, default=REDDIT["degree"])
+    ap.add_argument("--config", default="reddit-sage", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=0, help="override the vertex count (0: config's)")
+    ap.add_argument("--degree", type=float, default=0.0)
     return ap.parse_args()
 
 
@@ -213,6 +231,9 @@ def run_reference(args, world, rank):
 
 def main():
     args = parse()
+    C = CONFIGS[args.config]
+    args.n = args.n or C["n"]
+    args.degree = args.degree or C["degree"]
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank)
@@ -235,10 +256,15 @@ def main():
     from paper_2311_06837_b200.train import FullGraphTrainer, ModelConfig
 
     t0 = time.perf_counter()
-    g = G.gen_random_graph(args.n, args.degree, REDDIT["seed"])
+    g = G.gen_random_graph(args.n, args.degree, C["seed"])
     t_gen = time.perf_counter() - t0
-    cfg = ModelConfig(MODEL, list(REDDIT["dims"]), lr=0.1)
-    tr = FullGraphTrainer(g, cfg, rank=rank, world=world, pg=pg)
+    cfg = ModelConfig(C["kind"], list(C["dims"]), lr=C["lr"])
+    sub = None
+    if C["mode"] == "eas":
+        m, k, sseed = C["eas"]
+        part = G.partition_random(g, world, 1)
+        sub = G.extract_sampled(g, part, rank, G.SamplingConfig(m, k, sseed))
+    tr = FullGraphTrainer(g, cfg, rank=rank, world=world, pg=pg, subgraph=sub)
 
     def barrier():
         if world > 1:
@@ -313,14 +339,18 @@ def main():
 
     l2_peak = probe_l2_peak(torch, dev)
     edges_total = g.num_edges()
-    agg_edges_epoch = 2 * cfg.layers * edges_total
+    # edges aggregated per epoch over all ranks (forward + backward passes)
+    ed = torch.tensor([float(tr.nnz_local)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ed)
+    agg_edges_epoch = 2 * cfg.layers * float(ed[0])
     peak, peak_kind = load_peaks()
     agg_avg_ms = (agg_ms_total / agg_launches) if agg_launches else None
     achieved = (agg_bytes / agg_launches) / (agg_avg_ms * 1e-3) / 1e9 if agg_launches else None
 
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and args.config == "reddit-sage":
             cpu = cpu_baseline_record(args)
         clocks = clk.summary()
         out = {
@@ -337,9 +367,9 @@ def main():
             "dtype": "f32 (tcgen05 GEMMs: bf16x3 split, fp32 accumulate)",
             "data": "synthetic: gen_random_graph(232965, 491.99, 11) Reddit-shape G(n,p), "
                     "features/weights/labels from the reference keyed RNG streams",
-            "config": {"workload": "reddit-shape full-graph 3-layer GraphSAGE-mean training epoch "
-                                   "(BASELINE configs[1])",
-                       "model": "graphsage-mean 602-64-64-41, no bias, SGD lr 0.1",
+            "config": {"workload": C["workload"], "name": args.config,
+                       "model": f"{cfg.kind} {'-'.join(map(str, cfg.dims[:3]))}...{cfg.dims[-1]} "
+                                f"({cfg.layers} layers), no bias, SGD lr {cfg.lr}",
                        "vertices": args.n, "directed_edges": edges_total, "global_batch": args.n,
                        "parallelism": f"row-partition x{world} (all-gather per layer, NCCL)",
                        "l2": "no flush: each epoch streams >1 GB (CSR cols 458 MB + features 567 MB) "
