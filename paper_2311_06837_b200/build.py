@@ -67,5 +67,55 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return OUT
 
 
+API_OUT = os.path.join(HERE, "libgranndis_b200.so")
+REF_TESTS = "/root/reference/proj/tests"
+SUITE_OUT = os.path.join(ROOT, "build", "ref_suite_b200")
+
+
+def build_cxx_api(verbose: bool = False, force: bool = False) -> str:
+    """libgranndis_b200.so: the reference's C++ API (include/granndis_b200/granndis.hpp)
+    over the engine, self-contained (libgdx objects linked in)."""
+    build(verbose, force)
+    src = os.path.join(CSRC, "granndis_api.cpp")
+    obj = os.path.join(OBJ, "granndis_api.o")
+    hdr = [os.path.join(ROOT, "include", "granndis_b200", "granndis.hpp"),
+           os.path.join(ROOT, "include", "gdx.h")]
+    if force or _stale(obj, [src] + hdr):
+        cmd = ["g++", "-O2", "-std=c++20", "-fPIC", "-I" + os.path.join(ROOT, "include"),
+               "-I/usr/local/cuda/include", "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    objs = [obj] + [os.path.join(OBJ, f + ".o") for f in SOURCES_CU + SOURCES_CXX]
+    if force or _stale(API_OUT, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", API_OUT] + objs + ["-Xcompiler", "-fopenmp", "-lgomp"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return API_OUT
+
+
+def build_ref_suite(verbose: bool = False, force: bool = False):
+    """Compile the reference's own doctest suites for the hot path (read in place from
+    /root/reference, never copied) against libgranndis_b200.so -> build/ref_suite_b200.
+    Skipped where /root/reference is absent (the GPU box uses the prebuilt binary)."""
+    if not os.path.isdir(REF_TESTS):
+        return None
+    build_cxx_api(verbose, force)
+    srcs = [os.path.join(REF_TESTS, "test_reference_gnn.cpp"), os.path.join(REF_TESTS, "test_extract.cpp"),
+            os.path.join(ROOT, "tests", "cxx", "doctest_main.cpp")]
+    if force or _stale(SUITE_OUT, srcs + [API_OUT]):
+        cmd = ["g++", "-O2", "-std=c++20", "-I" + os.path.join(ROOT, "tests", "cxx"),
+               "-I" + os.path.join(ROOT, "include", "granndis_compat"), "-I" + os.path.join(ROOT, "include"),
+               *srcs, "-L" + HERE, "-lgranndis_b200", "-Wl,-rpath,$ORIGIN/../paper_2311_06837_b200",
+               "-o", SUITE_OUT]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return SUITE_OUT
+
+
 if __name__ == "__main__":
     build(verbose=True, force="--force" in sys.argv)
+    build_cxx_api(verbose=True)
+    build_ref_suite(verbose=True)

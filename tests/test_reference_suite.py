@@ -1,0 +1,35 @@
+"""The reference's OWN doctest suites for the hot path (proj/tests/test_reference_gnn.cpp
+and test_extract.cpp), compiled unchanged against the drop-in C++ API
+(include/granndis_b200/granndis.hpp -> libgranndis_b200.so, i.e. the GPU engine)
+by paper_2311_06837_b200/build.py -> build/ref_suite_b200.
+
+Every case must pass except the ones listed in FP64_ONLY: assertions written for
+the reference's fp64 arithmetic at a tighter tolerance than the engine's fp32
+contract (|a-b| <= 1e-4 scaled, BASELINE.json north_star)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SUITE = os.path.join(ROOT, "build", "ref_suite_b200")
+
+# test_reference_gnn.cpp:179-208 compares two summation orders at doctest::Approx
+# epsilon 1e-9; fp32 results differ at ~1e-7 relative.
+FP64_ONLY = {"permutation safety up to summation order"}
+
+
+def test_reference_doctest_suites_on_the_gpu_engine(cuda):
+    if not os.path.exists(SUITE):
+        pytest.skip("build/ref_suite_b200 not built (needs /root/reference at build time)")
+    r = subprocess.run([SUITE], capture_output=True, text=True, timeout=900)
+    lines = r.stdout.splitlines()
+    passed = [l[6:] for l in lines if l.startswith("PASS  ")]
+    failed = [l[6:] for l in lines if l.startswith("FAIL  ")]
+    summary = [l for l in lines if l.startswith("[ref-suite]")]
+    assert summary, r.stdout[-3000:] + r.stderr[-2000:]
+    unexpected = [f for f in failed if f not in FP64_ONLY]
+    assert not unexpected, "\n".join(lines[-60:])
+    assert len(passed) >= 25, summary
