@@ -42,8 +42,8 @@ struct Dev {
         cuda(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
         if (zero) cuda(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)), "cudaMemset");
     }
-    Dev(const T* host, size_t count) : Dev(count, false) {
-        if (count) cuda(cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+    Dev(const T* host, size_t count) : Dev(count, host == nullptr) {
+        if (count && host) cuda(cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice), "H2D");
     }
     Dev(const Dev&) = delete;
     Dev& operator=(const Dev&) = delete;
@@ -79,7 +79,8 @@ struct DevCSR {
 DevCSR upload(const Graph& g) {
     DevCSR d;
     d.rp = Dev<uint64_t>(g.row_offsets().data(), g.row_offsets().size());
-    d.col = Dev<uint32_t>(g.col_indices().data(), std::max<size_t>(g.col_indices().size(), 1));
+    d.col = g.col_indices().empty() ? Dev<uint32_t>(1)
+                                    : Dev<uint32_t>(g.col_indices().data(), g.col_indices().size());
     d.rows = g.num_vertices();
     return d;
 }
@@ -553,6 +554,13 @@ DenseFeatures forward_server_local(const DependencySubgraph& sub, const Graph& g
         throw ContractError("forward_server_local: subgraph too shallow or sampled for exact " +
                             std::to_string(layers) + "-layer computation");
     const uint32_t n = g.num_vertices();
+    if (layers == 0) {  // no layer runs: the inner rows verbatim (reference_gnn.cpp:140-146)
+        DenseFeatures out(static_cast<uint32_t>(sub.inner_vertices.size()), x.cols);
+        for (VertexId r = 0; r < sub.inner_vertices.size(); ++r)
+            std::copy(x.row(sub.inner_vertices[r]).begin(), x.row(sub.inner_vertices[r]).end(),
+                      out.row(r).begin());
+        return out;
+    }
     std::vector<uint32_t> hop(n, GDX_UNSEEN);
     for (VertexId v : sub.inner_vertices) hop[v] = 0;
     uint32_t max_hop = 0;

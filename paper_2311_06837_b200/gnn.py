@@ -174,6 +174,8 @@ def forward_server_local(sub: DependencySubgraph, g: Graph, x: Matrix, w, layers
     if require_exact and (sub.sampled or sub.hop_limit < layers):
         raise ContractError(f"forward_server_local: subgraph too shallow or sampled for exact "
                             f"{layers}-layer computation")
+    if layers == 0:  # no layer runs: the inner rows verbatim (reference_gnn.cpp:140-146)
+        return x[np.asarray(sub.inner_vertices, np.int64)].copy()
     d = _dev()
     loc = LocalSubgraph(sub, g, d)
     F = x.shape[1]
