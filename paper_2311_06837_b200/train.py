@@ -438,6 +438,48 @@ class FullGraphTrainer:
         return 2 * self.cfg.layers * self.nnz_local
 
 
+class FeatureStream:
+    """Double-buffered host->device feature loading for the end-to-end path: the
+    next step's feature block is copied (own stream, pinned source) while the
+    current epoch computes; consume() orders the compute stream after the copy,
+    converts it to the split-bf16 GEMM operand and frees the staging buffer."""
+
+    def __init__(self, tr: "FullGraphTrainer"):
+        self.tr = tr
+        d = tr.d
+        self.stage = [dense(tr.nloc, tr.F, d) for _ in range(2)]
+        self.labels = [torch.empty_like(tr.labels) for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(device=d)
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.free = [torch.cuda.Event() for _ in range(2)]
+        self.issued = 0
+        self.consumed = 0
+
+    def prefetch(self, x_host: torch.Tensor, labels_host: torch.Tensor | None = None):
+        i = self.issued % 2
+        cs = self.copy_stream
+        if self.issued >= 2:
+            cs.wait_event(self.free[i])
+        cs.wait_stream(torch.cuda.current_stream()) if self.issued == 0 else None
+        with torch.cuda.stream(cs):
+            self.stage[i][:self.tr.nloc, :self.tr.F].copy_(x_host, non_blocking=True)
+            if labels_host is not None:
+                self.labels[i][:self.tr.nloc].copy_(labels_host, non_blocking=True)
+            self.ready[i].record(cs)
+        self.issued += 1
+
+    def consume(self, with_labels: bool = True):
+        i = self.consumed % 2
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self.ready[i])
+        tr = self.tr
+        tr.Xsp.fill_from(self.stage[i], self.stage[i].shape[1])
+        if with_labels:
+            tr.labels.copy_(self.labels[i])
+        self.free[i].record(cur)
+        self.consumed += 1
+
+
 class RowExchange:
     """The per-layer exchange of a row-partitioned full graph:
     every rank owns the contiguous row block offsets[r]:offsets[r+1] of a
