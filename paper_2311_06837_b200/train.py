@@ -79,15 +79,30 @@ def init_weights(cfg: ModelConfig, seed: int) -> list:
     return ws
 
 
+L2_RESIDENT_BYTES = 96 << 20  # gathered matrices up to this size stay in the 126 MB L2
+
+
+def agg_width(fout: int, rows: int) -> int:
+    """Row width of a gathered matrix.  L2-resident matrices pad to 32-byte sectors
+    (what the L2 gather pays for); HBM-resident ones pad to whole 128-byte lines,
+    since a misaligned row costs an extra DRAM line per gather (measured: 48-wide
+    rows are slower than 64-wide ones when gathered from HBM)."""
+    w8 = pad8(fout)
+    if rows * w8 * 4 <= L2_RESIDENT_BYTES:
+        return w8
+    return 32 if fout <= 32 else (w8 + 31) // 32 * 32
+
+
 class _Layer:
     """Device state of one layer: W_cat (fp32 master + split copies), buffers."""
 
-    def __init__(self, kind, fin, fout, nloc, nfull, d, splitk_target, first):
+    def __init__(self, kind, fin, fout, nloc, nfull, d, splitk_target, first, fin_w=None):
         self.kind, self.fin, self.fout = kind, fin, fout
-        self.k = fin if first else pad8(fin)      # GEMM K: the input operand's logical width
-        self.w = pad8(fout)                       # aggregation width (32 B sectors)
+        # GEMM K: the input operand's logical width (the previous layer's row width)
+        self.k = fin if first else (fin_w if fin_w is not None else pad8(fin))
+        self.w = agg_width(fout, nfull)           # aggregation / row width of this layer
         self.nz = 2 * self.w if kind == "sage" else self.w   # GEMM N (W_cat rows)
-        self.fin_ld = pad8(fin)
+        self.fin_ld = pad8(self.k)
         # master weights, row pitch == split pitch so the fused SGD can index both
         self.W = torch.zeros((self.nz, self.fin_ld), dtype=torch.float32, device=d)
         self.Wsp = Split(self.nz, self.k, d, ld=self.fin_ld)  # forward B (nz x k); MN-major B of dH
@@ -225,7 +240,8 @@ class FullGraphTrainer:
         self.layers = []
         for l in range(cfg.layers):
             self.layers.append(_Layer(cfg.kind, cfg.dims[l], cfg.dims[l + 1], self.nloc,
-                                      self.nrows_gather, d, 2 * sm, l == 0))
+                                      self.nrows_gather, d, 2 * sm, l == 0,
+                                      self.layers[-1].w if l else None))
         # all weight gradients (+ the loss) in one flat buffer: one all-reduce per epoch
         sizes = [L.nz * L.fin_ld for L in self.layers]
         self.grad_flat = torch.zeros(sum(sizes) + 1, dtype=torch.float32, device=d)
@@ -238,7 +254,8 @@ class FullGraphTrainer:
         self.set_weights(weights)
         self.dlogits = dense(self.nloc, self.layers[-1].w, d)
         self.partial = dense(self.nloc, max(L.w for L in self.layers), d) if self.overlap else None
-        self.dH = [dense(self.nloc, pad8(cfg.dims[l]), d) for l in range(cfg.layers)]
+        self.dH = [dense(self.nloc, self.layers[l - 1].w if l else pad8(cfg.dims[0]), d)
+                   for l in range(cfg.layers)]
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=d)
         self.keep_activations = False
         self.activations = []
