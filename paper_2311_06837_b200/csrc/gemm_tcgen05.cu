@@ -15,10 +15,11 @@
 // bf16 tensor rate -- the GEMMs here are skinny (N <= 256) and HBM-bound anyway.
 //
 // Persistent structure: one CTA per SM loops over output tiles (128 x BN, and
-// K ranges for split-K); 192 threads:
+// K ranges for split-K); 320 threads:
 //   warp 0 / lane 0 : TMA producer   (cp.async.bulk.tensor, 128B swizzle, mbarrier tx)
 //   warp 1 / lane 0 : MMA issuer     (tcgen05.mma, tcgen05.commit releases stages / accumulators)
-//   warps 2-5       : epilogue       (tcgen05.ld 32x32b -> scale/ReLU -> vector stores)
+//   warps 2-9       : epilogue       (tcgen05.ld 32x32b.x32 -> scale/ReLU -> vector stores);
+//                     two warps per 32-lane TMEM quarter, each taking half the columns
 // The accumulator is double-buffered in TMEM (2 x BN fp32 columns) so the
 // epilogue of tile i overlaps the TMA + MMA of tile i+1.
 #include <cudaTypedefs.h>
@@ -32,7 +33,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // 2 role warps + 8 epilogue warps
+constexpr int kEpiWarps = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -119,6 +121,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t addr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(addr));
+}
+
 struct Epi {
     uint32_t m, n;
     float* c0;
@@ -185,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+            mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -277,8 +290,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        // ---------------- epilogue warps 2..5 ----------------
-        const uint32_t lane_base = 32 * (warp & 3);  // TMEM lanes this warp may access
+        // ---------------- epilogue warps 2..9 ----------------
+        const uint32_t lane_base = 32 * (warp & 3);       // TMEM lanes this warp may access
+        constexpr int kCols = BN / 2;                     // columns per epilogue warp
+        const uint32_t col_base = (warp - 2) / 4 * kCols;  // which half of the tile
         uint32_t tl = 0;
         for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
             uint32_t mt, nt, z;
@@ -291,60 +306,69 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool row_ok = row < ep.m;
             const float rs = (row_ok && ep.row_scale && ep.split_k <= 1) ? ep.row_scale[row] : 1.f;
 #pragma unroll 1
-            for (int cb = 0; cb < BN; cb += 16) {
-                float v[16];
-                if (has_k) {
-                    tmem_ld16(tmem + (lane_base << 16) + acc * BN + cb, v);
-                } else {
+            for (int cb = 0; cb < kCols; cb += 32) {
+                uint32_t raw[32];
+                tmem_ld32_nowait(tmem + (lane_base << 16) + acc * BN + col_base + cb, raw);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                float v[32];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = 0.f;
-                }
-                const uint32_t col0 = nt * BN + cb;
-                if (!row_ok || col0 >= ep.n) continue;
-                if (ep.split_k > 1) {
-                    float* dst = ep.c0 + static_cast<uint64_t>(z) * ep.m * ep.ldc0 +
-                                 static_cast<uint64_t>(row) * ep.ldc0 + col0;
-                    if (col0 + 16 <= ep.n && (ep.ldc0 % 4) == 0) {
+                for (int j = 0; j < 32; ++j) v[j] = has_k ? __uint_as_float(raw[j]) : 0.f;
+                if (!row_ok) continue;
+#pragma unroll
+                for (int h = 0; h < 32; h += 16) {
+                    const uint32_t col0 = nt * BN + col_base + cb + h;
+                    if (col0 >= ep.n) continue;
+                    float* vv = v + h;
+                    if (ep.split_k > 1) {
+                        float* dst = ep.c0 + static_cast<uint64_t>(z) * ep.m * ep.ldc0 +
+                                     static_cast<uint64_t>(row) * ep.ldc0 + col0;
+                        if (col0 + 16 <= ep.n && (ep.ldc0 % 4) == 0) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4)
+                                *reinterpret_cast<float4*>(dst + j) = make_float4(vv[j], vv[j + 1], vv[j + 2], vv[j + 3]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (col0 + j < ep.n) dst[j] = vv[j];
+                        }
+                        continue;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        vv[j] *= rs;
+                        if (ep.relu) vv[j] = fmaxf(vv[j], 0.f);
+                    }
+                    // a 16-column group entirely on one side of the split: 4 x 16 B stores
+                    float* base = nullptr;
+                    if (col0 + 16 <= ep.n) {
+                        if (col0 + 16 <= ep.split && ep.c0 && ep.ldc0 % 4 == 0)
+                            base = ep.c0 + static_cast<uint64_t>(row) * ep.ldc0 + col0;
+                        else if (col0 >= ep.split && ep.c1 && ep.ldc1 % 4 == 0 && (col0 - ep.split) % 4 == 0)
+                            base = ep.c1 + static_cast<uint64_t>(row) * ep.ldc1 + (col0 - ep.split);
+                    }
+                    if (base && (reinterpret_cast<uintptr_t>(base) & 15) == 0) {
 #pragma unroll
                         for (int j = 0; j < 16; j += 4)
-                            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                            *reinterpret_cast<float4*>(base + j) = make_float4(vv[j], vv[j + 1], vv[j + 2], vv[j + 3]);
                     } else {
-                        for (int j = 0; j < 16 && col0 + j < ep.n; ++j) dst[j] = v[j];
-                    }
-                    continue;
-                }
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    v[j] *= rs;
-                    if (ep.relu) v[j] = fmaxf(v[j], 0.f);
-                }
-                // a 16-column group entirely on one side of the split: 4 x 16 B stores
-                float* base = nullptr;
-                if (col0 + 16 <= ep.n) {
-                    if (col0 + 16 <= ep.split && ep.c0 && ep.ldc0 % 4 == 0)
-                        base = ep.c0 + static_cast<uint64_t>(row) * ep.ldc0 + col0;
-                    else if (col0 >= ep.split && ep.c1 && ep.ldc1 % 4 == 0 && (col0 - ep.split) % 4 == 0)
-                        base = ep.c1 + static_cast<uint64_t>(row) * ep.ldc1 + (col0 - ep.split);
-                }
-                if (base && (reinterpret_cast<uintptr_t>(base) & 15) == 0) {
-#pragma unroll
-                    for (int j = 0; j < 16; j += 4)
-                        *reinterpret_cast<float4*>(base + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                } else {
-                    for (int j = 0; j < 16; ++j) {
-                        const uint32_t col = col0 + j;
-                        if (col >= ep.n) break;
-                        if (col < ep.split) {
-                            if (ep.c0) ep.c0[static_cast<uint64_t>(row) * ep.ldc0 + col] = v[j];
-                        } else if (ep.c1) {
-                            ep.c1[static_cast<uint64_t>(row) * ep.ldc1 + (col - ep.split)] = v[j];
+                        for (int j = 0; j < 16; ++j) {
+                            const uint32_t col = col0 + j;
+                            if (col >= ep.n) continue;
+                            if (col < ep.split) {
+                                if (ep.c0) ep.c0[static_cast<uint64_t>(row) * ep.ldc0 + col] = vv[j];
+                            } else if (ep.c1) {
+                                ep.c1[static_cast<uint64_t>(row) * ep.ldc1 + (col - ep.split)] = vv[j];
+                            }
                         }
                     }
-                }
-                if (ep.out_hi) {
-                    uint16_t* hp = ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0;
-                    uint16_t* lp = ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0;
-                    for (int j = 0; j < 16 && col0 + j < ep.n; ++j) split_bf16(v[j], hp[j], lp[j]);
+                    if (ep.out_hi) {
+                        uint16_t* hp = ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0;
+                        uint16_t* lp = ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (col0 + j < ep.n) split_bf16(vv[j], hp[j], lp[j]);
+                    }
                 }
             }
             // accumulator drained: hand it back to the MMA warp

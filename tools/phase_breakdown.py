@@ -67,8 +67,12 @@ def main():
     ex_ar = T.RowExchange.allreduce
     T.RowExchange.allreduce = lambda self, t: wrap("allreduce", ex_ar)(self, t)
 
-    g = G.gen_random_graph(232965, 491.99, 11)
-    tr = T.FullGraphTrainer(g, T.ModelConfig("sage", [602, 64, 64, 41]), rank=rank, world=world, pg=pg)
+    cfgname = os.environ.get("GDX_CONFIG", "reddit-sage")
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import CONFIGS
+    C = CONFIGS[cfgname]
+    g = G.gen_random_graph(C["n"], C["degree"], C["seed"])
+    tr = T.FullGraphTrainer(g, T.ModelConfig(C["kind"], C["dims"], lr=C["lr"]), rank=rank, world=world, pg=pg)
     for _ in range(3):
         tr.train_epoch(sync_loss=False)
     torch.cuda.synchronize()
