@@ -114,8 +114,10 @@ int gdx_aggregate_variant(const gdx_aggregate_args* a, int variant, gdx_stream s
  *   C[m][n] = sum_k (A_hi+A_lo)(m,k) * (B_hi+B_lo)(n,k)   (3 bf16 MMAs, fp32 TMEM acc)
  * with each operand K-major or MN-major (so G^T H needs no transposes).
  * Persistent: one CTA per SM, double-buffered TMEM accumulator.
- * Epilogue: C *= row_scale[m]; relu; columns [0,split) -> c0, [split,n) -> c1;
- * optional split-bf16 copy.  split_k > 1 writes raw partials to
+ * Epilogue: C = mask ? (mask > 0 ? C : 0) : C; [split copy if split_unscaled];
+ * C *= row_scale[m]; relu; columns [0,split) -> c0, [split,n) -> c1; optional split-bf16
+ * copy (after scaling unless split_unscaled).  The mask form fuses the ReLU backward
+ * and degree scaling of the next aggregation into the dH GEMM.  split_k > 1 writes raw partials to
  * c0 + z*m*ldc0 (z < split_k) for gdx_splitk_reduce.
  * Constraints: lda, ldb multiples of 8 elements; device pointers 16 B aligned.
  * Note: inputs are read by TMA through tensor maps built per call on the host.
@@ -133,6 +135,9 @@ typedef struct gdx_gemm_args {
     int relu;
     uint16_t* out_hi; uint16_t* out_lo; uint64_t ld_split;   /* nullable */
     uint32_t split_k;         /* 0/1: none */
+    const float* mask;        /* nullable [m x ld_mask]: C = 0 where mask <= 0 (ReLU backward) */
+    uint64_t ld_mask;
+    int split_unscaled;       /* 1: the split-bf16 copy is taken before row_scale */
 } gdx_gemm_args;
 int gdx_gemm_tn(const gdx_gemm_args* g, gdx_stream stream);
 /* Reference-precision SIMT fallback of the same contract, for tests only. */
@@ -165,6 +170,13 @@ int gdx_grad_prepare(const float* dH, uint64_t ld_dh, const float* H, uint64_t l
 int gdx_softmax_xent(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
                      const int32_t* labels, float inv_count, float* dlogits, uint64_t ld_d,
                      double* loss_sum, gdx_stream stream);
+/* Same, fused with the backward prep of the last layer: g = dlogits is written as a
+ * split-bf16 copy (g_hi/g_lo, nullable) and as gs = g * row_scale[v] (gs, nullable;
+ * row_scale nullable = 1); dlogits itself is optional. */
+int gdx_softmax_xent_fused(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
+                           const int32_t* labels, float inv_count, float* dlogits, uint64_t ld_d,
+                           const float* row_scale, float* gs, uint64_t ld_gs, uint16_t* g_hi,
+                           uint16_t* g_lo, uint64_t ld_g, double* loss_sum, gdx_stream stream);
 /* Bandwidth probe for roofline denominators: reads `bytes` of buf `reps` times,
  * mode 0 = coalesced stream, mode 1 = random 256 B row gathers (bytes moved =
  * reps * bytes in both modes).  Time it with events on `stream`. */

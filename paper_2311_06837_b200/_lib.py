@@ -36,7 +36,8 @@ class GemmArgs(C.Structure):
         ("a_mn_major", C.c_int), ("b_mn_major", C.c_int),
         ("m", u32), ("n", u32), ("k", u32), ("c0", vp), ("ldc0", u64), ("c1", vp), ("ldc1", u64),
         ("split", u32), ("row_scale", vp), ("relu", C.c_int), ("out_hi", vp), ("out_lo", vp),
-        ("ld_split", u64), ("split_k", u32),
+        ("ld_split", u64), ("split_k", u32), ("mask", vp), ("ld_mask", u64),
+        ("split_unscaled", C.c_int),
     ]
 
 
@@ -61,6 +62,8 @@ _SIGS = {
     "gdx_transpose_split": (C.c_int, [vp, vp, u64, u32, u32, vp, vp, u64, vp]),
     "gdx_grad_prepare": (C.c_int, [vp, u64, vp, u64, u32, u32, vp, vp, u64, vp, u64, vp, vp, u64, vp]),
     "gdx_softmax_xent": (C.c_int, [vp, u64, u32, u32, vp, C.c_float, vp, u64, vp, vp]),
+    "gdx_softmax_xent_fused": (C.c_int, [vp, u64, u32, u32, vp, C.c_float, vp, u64, vp, vp, u64, vp, vp,
+                                         u64, vp, vp]),
     "gdx_degree_scale": (C.c_int, [vp, u32, C.c_int, vp, vp]),
     "gdx_probe_bandwidth": (C.c_int, [vp, u64, u32, C.c_int, vp, vp]),
     "gdx_sampled_growth": (C.c_int, [vp, vp, u32, vp, vp, u32, u32, u64, vp, vp, vp]),

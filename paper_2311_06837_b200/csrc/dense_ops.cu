@@ -103,10 +103,13 @@ __global__ void grad_prepare_kernel(const float* dH, uint64_t ld_dh, const float
     }
 }
 
-// One warp per row; classes <= 32*8.
+// One warp per row.  Optional fused outputs of the last layer's backward prep:
+// split-bf16 copy of g = dlogits and gs = g * row_scale.
 __global__ void softmax_xent_kernel(const float* logits, uint64_t ld, uint32_t rows,
                                     uint32_t classes, const int32_t* labels, float inv_count,
-                                    float* dlogits, uint64_t ld_d, double* loss_sum) {
+                                    float* dlogits, uint64_t ld_d, const float* row_scale, float* gs,
+                                    uint64_t ld_gs, uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g,
+                                    double* loss_sum) {
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -121,9 +124,13 @@ __global__ void softmax_xent_kernel(const float* logits, uint64_t ld, uint32_t r
         for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         const float lse = mx + logf(sum);
         const int32_t y = labels[r];
+        const float rs = row_scale ? row_scale[r] : 1.f;
         for (uint32_t c = lane; c < classes; c += 32) {
             const float p = expf(z[c] - lse);
-            dlogits[static_cast<uint64_t>(r) * ld_d + c] = (p - (static_cast<int32_t>(c) == y ? 1.f : 0.f)) * inv_count;
+            const float g = (p - (static_cast<int32_t>(c) == y ? 1.f : 0.f)) * inv_count;
+            if (dlogits) dlogits[static_cast<uint64_t>(r) * ld_d + c] = g;
+            if (gs) gs[static_cast<uint64_t>(r) * ld_gs + c] = g * rs;
+            if (g_hi) split_bf16(g, g_hi[static_cast<uint64_t>(r) * ld_g + c], g_lo[static_cast<uint64_t>(r) * ld_g + c]);
         }
         if (lane == 0) local += static_cast<double>(lse - z[y]);
     }
@@ -294,9 +301,27 @@ extern "C" int gdx_softmax_xent(const float* logits, uint64_t ld, uint32_t rows,
     if (!rows) return GDX_OK;
     const uint64_t threads = static_cast<uint64_t>(rows) * 32;
     softmax_xent_kernel<<<grid_for(threads), 256, 0, as_cuda(stream)>>>(
-        logits, ld, rows, classes, labels, inv_count, dlogits, ld_d, loss_sum);
+        logits, ld, rows, classes, labels, inv_count, dlogits, ld_d, nullptr, nullptr, 0, nullptr,
+        nullptr, 0, loss_sum);
     note_launch();
     return check_launch("gdx_softmax_xent");
+}
+
+extern "C" int gdx_softmax_xent_fused(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
+                                      const int32_t* labels, float inv_count, float* dlogits,
+                                      uint64_t ld_d, const float* row_scale, float* gs, uint64_t ld_gs,
+                                      uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g, double* loss_sum,
+                                      gdx_stream stream) {
+    GDX_REQUIRE(logits && labels && loss_sum, GDX_INPUT, "gdx_softmax_xent_fused: null pointer");
+    GDX_REQUIRE(!g_hi == !g_lo, GDX_INPUT, "gdx_softmax_xent_fused: g_hi/g_lo must pair");
+    GDX_REQUIRE(classes >= 1, GDX_INPUT, "gdx_softmax_xent_fused: classes must be >= 1");
+    if (!rows) return GDX_OK;
+    const uint64_t threads = static_cast<uint64_t>(rows) * 32;
+    softmax_xent_kernel<<<grid_for(threads), 256, 0, as_cuda(stream)>>>(
+        logits, ld, rows, classes, labels, inv_count, dlogits, ld_d, row_scale, gs, ld_gs, g_hi, g_lo,
+        ld_g, loss_sum);
+    note_launch();
+    return check_launch("gdx_softmax_xent_fused");
 }
 
 extern "C" int gdx_degree_scale(const uint64_t* row_ptr, uint32_t rows, int kind, float* out,

@@ -147,6 +147,9 @@ struct Epi {
     uint32_t split_k;
     uint32_t kblocks;   // total k blocks
     uint32_t m_tiles, n_tiles;
+    const float* mask;
+    uint64_t ld_mask;
+    int split_unscaled;
 };
 
 template <int BN, int STAGES>
@@ -333,6 +336,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         continue;
                     }
+                    if (ep.mask) {  // ReLU backward: zero where the forward activation was not positive
+                        const float* mp = ep.mask + static_cast<uint64_t>(row) * ep.ld_mask + col0;
+                        if (col0 + 16 <= ep.n && (ep.ld_mask % 4) == 0 &&
+                            (reinterpret_cast<uintptr_t>(mp) & 15) == 0) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4) {
+                                const float4 q = __ldg(reinterpret_cast<const float4*>(mp + j));
+                                if (!(q.x > 0.f)) vv[j] = 0.f;
+                                if (!(q.y > 0.f)) vv[j + 1] = 0.f;
+                                if (!(q.z > 0.f)) vv[j + 2] = 0.f;
+                                if (!(q.w > 0.f)) vv[j + 3] = 0.f;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (col0 + j < ep.n && !(mp[j] > 0.f)) vv[j] = 0.f;
+                        }
+                    }
+                    if (ep.out_hi && ep.split_unscaled) {
+                        uint16_t* hp = ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0;
+                        uint16_t* lp = ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (col0 + j < ep.n) split_bf16(vv[j], hp[j], lp[j]);
+                    }
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         vv[j] *= rs;
@@ -362,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
-                    if (ep.out_hi) {
+                    if (ep.out_hi && !ep.split_unscaled) {
                         uint16_t* hp = ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0;
                         uint16_t* lp = ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0;
 #pragma unroll
@@ -404,6 +432,9 @@ __global__ void gemm_simt_kernel(const uint16_t* a_hi, const uint16_t* a_lo, uin
             ep.c0[static_cast<uint64_t>(z) * ep.m * ep.ldc0 + row * ep.ldc0 + col] = z == 0 ? acc : 0.f;
         return;
     }
+    if (ep.mask && !(ep.mask[row * ep.ld_mask + col] > 0.f)) acc = 0.f;
+    if (ep.out_hi && ep.split_unscaled)
+        split_bf16(acc, ep.out_hi[row * ep.ld_split + col], ep.out_lo[row * ep.ld_split + col]);
     float x = acc * (ep.row_scale ? ep.row_scale[row] : 1.f);
     if (ep.relu) x = fmaxf(x, 0.f);
     if (col < ep.split) {
@@ -411,7 +442,8 @@ __global__ void gemm_simt_kernel(const uint16_t* a_hi, const uint16_t* a_lo, uin
     } else if (ep.c1) {
         ep.c1[row * ep.ldc1 + col - ep.split] = x;
     }
-    if (ep.out_hi) split_bf16(x, ep.out_hi[row * ep.ld_split + col], ep.out_lo[row * ep.ld_split + col]);
+    if (ep.out_hi && !ep.split_unscaled)
+        split_bf16(x, ep.out_hi[row * ep.ld_split + col], ep.out_lo[row * ep.ld_split + col]);
 }
 
 // ---- host side --------------------------------------------------------------
@@ -505,13 +537,15 @@ int validate(const gdx_gemm_args* g) {
     GDX_REQUIRE(g->c0 || g->c1 || g->out_hi, GDX_INPUT, "gdx_gemm_tn: no output");
     GDX_REQUIRE(!g->out_hi == !g->out_lo, GDX_INPUT, "gdx_gemm_tn: out_hi/out_lo must pair");
     GDX_REQUIRE(g->split_k <= 1 || g->c0, GDX_INPUT, "gdx_gemm_tn: split_k needs c0 workspace");
+    GDX_REQUIRE(!g->mask || g->ld_mask >= g->n, GDX_INPUT, "gdx_gemm_tn: ld_mask < n");
     return GDX_OK;
 }
 
 Epi make_epi(const gdx_gemm_args* g, int bn) {
     Epi ep{g->m, g->n, g->c0, g->ldc0, g->c1, g->ldc1, g->split, g->row_scale, g->relu,
            g->out_hi, g->out_lo, g->ld_split, g->split_k ? g->split_k : 1,
-           (g->k + BK - 1) / BK, (g->m + BM - 1) / BM, (g->n + bn - 1) / bn};
+           (g->k + BK - 1) / BK, (g->m + BM - 1) / BM, (g->n + bn - 1) / bn,
+           g->mask, g->ld_mask, g->split_unscaled};
     return ep;
 }
 

@@ -252,10 +252,7 @@ class FullGraphTrainer:
         if weights is None:
             weights = init_weights(cfg, weight_seed)
         self.set_weights(weights)
-        self.dlogits = dense(self.nloc, self.layers[-1].w, d)
         self.partial = dense(self.nloc, max(L.w for L in self.layers), d) if self.overlap else None
-        self.dH = [dense(self.nloc, self.layers[l - 1].w if l else pad8(cfg.dims[0]), d)
-                   for l in range(cfg.layers)]
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=d)
         self.keep_activations = False
         self.activations = []
@@ -364,24 +361,24 @@ class FullGraphTrainer:
         self.activations = acts
         return self.layers[-1].Hout
 
+    def _grad_targets(self, l: int):
+        """Where the prepared gradient of layer l's output goes: gs = g * dst_scale into the
+        gathered buffer's own rows, and (SAGE) the unscaled split copy into G[:, :w]."""
+        L = self.layers[l]
+        own = L.dfull[self.lo:self.hi]
+        scale = {"sage": self.inv_deg, "gcn": self.gcn_s}.get(self.cfg.kind)
+        split = L.G if self.cfg.kind == "sage" else None
+        return own, scale, split
+
     def backward_and_step(self):
+        """Backward of every layer + SGD.  The last layer's g comes fused out of the
+        softmax kernel; each lower layer's g = dH * relu' (scaled for the next
+        aggregation, split for the weight gradient) comes fused out of the dH GEMM
+        epilogue, so there is no separate elementwise pass."""
         cfg = self.cfg
         nL = cfg.layers
-        dH = self.dlogits
         for l in range(nL - 1, -1, -1):
             L = self.layers[l]
-            relu = l + 1 < nL
-            own = L.dfull[self.lo:self.hi]
-            mask = L.Hout if relu else None
-            if cfg.kind == "sage":
-                call("gdx_grad_prepare", dH.data_ptr(), dH.shape[1], _lib.ptr(mask), L.Hout.shape[1],
-                     self.nloc, L.w, self.inv_deg.data_ptr(), None, 0, own.data_ptr(), own.shape[1],
-                     L.G.hi.data_ptr(), L.G.lo.data_ptr(), L.G.ld, stream_handle())
-            else:
-                scale = self.gcn_s if cfg.kind == "gcn" else None
-                call("gdx_grad_prepare", dH.data_ptr(), dH.shape[1], _lib.ptr(mask), L.Hout.shape[1],
-                     self.nloc, L.w, _lib.ptr(scale), None, 0, own.data_ptr(), own.shape[1],
-                     None, None, 0, stream_handle())
             # dZ = agg^T(gs): SAGE -> G[:, w:2w]; GCN/SUM -> G (all columns)
             if cfg.kind == "sage":
                 Gn = _SplitView(L.G, L.w)
@@ -391,10 +388,12 @@ class FullGraphTrainer:
                                          post_scale=self.gcn_s)
             else:
                 self._exchange_aggregate(L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo)
-            # dH_{l} = G W_cat  (before this layer's update); W_cat read MN-major in place
+            # dH_{l} = G W_cat (before this layer's update; W_cat read MN-major in place),
+            # epilogue: ReLU backward with H_{l} as mask, scale, split -> layer l-1's inputs
             if l > 0:
-                dprev = self.dH[l]
-                gemm_tn(L.G, L.Wsp, c0=dprev, b_mn=True)
+                own, scale, split = self._grad_targets(l - 1)
+                gemm_tn(L.G, L.Wsp, c0=own, b_mn=True, mask=self.layers[l - 1].Hout,
+                        row_scale=scale, out_split=split, split_unscaled=True)
             # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
             gemm_tn(L.G, A_in, c0=L.ws, split_k=L.split_k, a_mn=True, b_mn=True)
@@ -405,8 +404,6 @@ class FullGraphTrainer:
             else:                # reduce partials; SGD after the epoch's single all-reduce
                 call("gdx_splitk_reduce", L.ws.data_ptr(), L.split_k, L.nz * L.fin_ld, L.nz, L.fin,
                      L.fin_ld, L.dW.data_ptr(), None, 0.0, None, None, stream_handle())
-            if l > 0:
-                dH = self.dH[l]
         if self.world > 1:
             # one all-reduce for every layer's dW and the loss, then SGD (+ split refresh)
             self.grad_flat[-1:].copy_(self.loss_acc)
@@ -420,10 +417,13 @@ class FullGraphTrainer:
         """Forward, loss, backward, SGD.  Returns the loss (host float) if sync_loss."""
         self.loss_acc.zero_()
         logits = self.forward()
-        Lz = self.layers[-1]
-        call("gdx_softmax_xent", logits.data_ptr(), logits.shape[1], self.loss_rows, self.cfg.classes,
-             self.labels.data_ptr(), 1.0 / self.loss_count, self.dlogits.data_ptr(),
-             self.dlogits.shape[1], self.loss_acc.data_ptr(), stream_handle())
+        own, scale, split = self._grad_targets(self.cfg.layers - 1)
+        call("gdx_softmax_xent_fused", logits.data_ptr(), logits.shape[1], self.loss_rows,
+             self.cfg.classes, self.labels.data_ptr(), 1.0 / self.loss_count, None, 0,
+             _lib.ptr(scale), own.data_ptr(), own.stride(0),
+             _lib.ptr(split.hi) if split is not None else None,
+             _lib.ptr(split.lo) if split is not None else None, split.ld if split is not None else 0,
+             self.loss_acc.data_ptr(), stream_handle())
         self.backward_and_step()  # (multi-GPU: the loss rides on the gradient all-reduce)
         if sync_loss:
             return float(self.loss_acc.item()) / self.loss_count

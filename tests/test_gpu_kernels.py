@@ -195,3 +195,24 @@ def test_labels_bit_exact(cuda):
     out = torch.empty(5000, dtype=torch.int32, device=cuda)
     call("gdx_init_labels", 11, 0, 5000, 41, out.data_ptr(), stream_handle())
     assert np.array_equal(out.cpu().numpy(), O.make_labels(5000, 41, 11))
+
+
+def test_gemm_mask_epilogue_fused_backward(gdx, cuda):
+    """dH GEMM epilogue of the trainer: ReLU-backward mask, unscaled split copy, row scale."""
+    import torch
+    rng = np.random.default_rng(11)
+    m, n, k = 517, 64, 96
+    g = rng.uniform(-1, 1, (m, k))
+    w = rng.uniform(-1, 1, (k, n))          # stored [k][n]: MN-major B
+    mask = rng.uniform(-1, 1, (m, n)).astype(np.float32)
+    scale = rng.uniform(0.1, 2.0, m).astype(np.float32)
+    A, B = _split(gdx, g, cuda), _split(gdx, w, cuda)
+    out = gdx.dense(m, n, cuda)
+    sp = gdx.Split(m, n, cuda)
+    gdx.gemm_tn(A, B, c0=out, b_mn=True, mask=torch.from_numpy(mask).to(cuda),
+                row_scale=torch.from_numpy(scale).to(cuda), out_split=sp, split_unscaled=True)
+    torch.cuda.synchronize()
+    dh = g.astype(np.float32).astype(np.float64) @ w.astype(np.float32).astype(np.float64)
+    gref = np.where(mask > 0, dh, 0.0)
+    close(sp.to_float().double().cpu().numpy(), gref)
+    close(out[:m, :n].double().cpu().numpy(), gref * scale[:, None])
