@@ -132,6 +132,27 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t addr, uint32_t (&r)[32
         : "r"(addr));
 }
 
+// split-bf16 copy of 16 values at hp/lp: 8-byte vector stores when aligned
+__device__ __forceinline__ void store_split16(const float* vv, uint16_t* hp, uint16_t* lp, uint32_t col0,
+                                              uint32_t n) {
+    if (col0 + 16 <= n && (reinterpret_cast<uintptr_t>(hp) & 7) == 0 && (reinterpret_cast<uintptr_t>(lp) & 7) == 0) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+            ushort4 h, l;
+            split_bf16(vv[j], h.x, l.x);
+            split_bf16(vv[j + 1], h.y, l.y);
+            split_bf16(vv[j + 2], h.z, l.z);
+            split_bf16(vv[j + 3], h.w, l.w);
+            *reinterpret_cast<ushort4*>(hp + j) = h;
+            *reinterpret_cast<ushort4*>(lp + j) = l;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (col0 + j < n) split_bf16(vv[j], hp[j], lp[j]);
+    }
+}
+
 struct Epi {
     uint32_t m, n;
     float* c0;
@@ -354,13 +375,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 if (col0 + j < ep.n && !(mp[j] > 0.f)) vv[j] = 0.f;
                         }
                     }
-                    if (ep.out_hi && ep.split_unscaled) {
-                        uint16_t* hp = ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0;
-                        uint16_t* lp = ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (col0 + j < ep.n) split_bf16(vv[j], hp[j], lp[j]);
-                    }
+                    if (ep.out_hi && ep.split_unscaled)
+                        store_split16(vv, ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0,
+                                      ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0, col0, ep.n);
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         vv[j] *= rs;
@@ -390,13 +407,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
-                    if (ep.out_hi && !ep.split_unscaled) {
-                        uint16_t* hp = ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0;
-                        uint16_t* lp = ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (col0 + j < ep.n) split_bf16(vv[j], hp[j], lp[j]);
-                    }
+                    if (ep.out_hi && !ep.split_unscaled)
+                        store_split16(vv, ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0,
+                                      ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0, col0, ep.n);
                 }
             }
             // accumulator drained: hand it back to the MMA warp

@@ -23,6 +23,7 @@ SHAPES = [
     ("products L2 fwd", 2449029, 64, 64, 0, 0, 1),
     ("products dH", 2449029, 64, 64, 0, 1, 1),
     ("products dW L2", 64, 64, 2449029, 1, 1, 296),
+    ("reddit dH L2 fused(mask,scale,split)", 232965, 64, 128, 0, 1, -1),
 ]
 
 
@@ -37,9 +38,14 @@ def main():
         B = D.Split(k, n, d) if b_mn else D.Split(n, k, d)
         for t in (A.hi, A.lo, B.hi, B.lo):
             t.copy_(torch.randint(-16000, 16000, t.shape, dtype=torch.int16, device=d))
+        fused = sk < 0
+        sk = max(sk, 1)
         rows = sk * m if sk > 1 else m
         C = torch.zeros((rows, D.pad4(n)), dtype=torch.float32, device=d)
         kw = dict(c0=C, split_k=sk, a_mn=bool(a_mn), b_mn=bool(b_mn))
+        if fused:
+            kw.update(mask=torch.randn(m, D.pad4(n), device=d), row_scale=torch.rand(m, device=d),
+                      out_split=D.Split(m, n, d), split_unscaled=True)
         for _ in range(3):
             D.gemm_tn(A, B, **kw)
         torch.cuda.synchronize()
