@@ -107,7 +107,7 @@ def port() -> C.CDLL:
         L.gro_train_epoch_masked.restype = C.c_double
         L.gro_train_epoch_masked.argtypes = [C.c_uint32, _u64p, _u32p, _f64p, _i32p, C.c_uint32,
                                              C.POINTER(_ModelC), _f64p, C.c_double, C.c_void_p,
-                                             C.c_uint32, C.c_double, C.c_int]
+                                             C.c_uint32, C.c_double, C.c_void_p, C.c_int]
         _port = L
     return _port
 
@@ -380,14 +380,16 @@ def train_epoch(g: CSR, x: np.ndarray, labels: np.ndarray, model: Model, w: np.n
 
 
 def train_epoch_masked(g: CSR, x: np.ndarray, labels: np.ndarray, model: Model, w: np.ndarray,
-                       lr: float, loss_rows: int, loss_count: float, nthreads: int = 1):
+                       lr: float, loss_rows: int, loss_count: float, nthreads: int = 1,
+                       layer_rows=None):
     """Epoch with the loss over rows < loss_rows / loss_count.  lr == 0 returns the
     gradients without updating (for summing several subgraphs).  Returns (loss, grads)."""
     grads = np.zeros(model.weight_count(), np.float64)
+    lr_arr = None if layer_rows is None else np.ascontiguousarray(layer_rows, np.uint32)
     loss = port().gro_train_epoch_masked(g.n, g.row_offsets, g.cols, np.ascontiguousarray(x, np.float64),
                                          np.ascontiguousarray(labels, np.int32), int(model.dims[-1]),
                                          C.byref(model._c), w, lr, _ptr(grads), loss_rows, loss_count,
-                                         nthreads)
+                                         _ptr(lr_arr), nthreads)
     return loss, grads
 
 

@@ -688,7 +688,7 @@ typedef struct {
 
 static void forward_impl(uint32_t n, uint32_t rows, const uint64_t* ro, const uint32_t* ci,
                          const double* x, const gro_model* m, const double* w, fwd_state* st,
-                         int nt) {
+                         int nt, const uint32_t* layer_rows) {
     uint32_t L = m->layers;
     st->H = (double**)calloc(L + 1, sizeof(double*));
     st->A = (double**)calloc(L, sizeof(double*));
@@ -699,6 +699,9 @@ static void forward_impl(uint32_t n, uint32_t rows, const uint64_t* ro, const ui
         uint32_t di = m->dims[l], dout = m->dims[l + 1];
         st->A[l] = (double*)calloc((size_t)n * di, sizeof(double));
         st->H[l + 1] = (double*)calloc((size_t)n * dout, sizeof(double));
+        /* hop masking (reference_gnn.cpp:119-137): layer l produces rows < layer_rows[l];
+         * rows never produced stay zero and contribute nothing when gathered */
+        if (layer_rows) rows = layer_rows[l];
         aggregate(m->kind, rows, ro, ci, st->H[l], di, st->s, st->A[l], nt);
         if (m->kind == GRO_SAGE) {
             rows_times_wt(rows, st->H[l], di, wl, dout, st->H[l + 1], 0, nt);
@@ -729,7 +732,7 @@ static void free_state(const gro_model* m, fwd_state* st) {
 void gro_model_forward(uint32_t n, const uint64_t* ro, const uint32_t* ci, const double* x,
                        const gro_model* m, const double* w, double* acts, int nthreads) {
     fwd_state st;
-    forward_impl(n, n, ro, ci, x, m, w, &st, nthreads);
+    forward_impl(n, n, ro, ci, x, m, w, &st, nthreads, NULL);
     size_t off = 0;
     for (uint32_t l = 1; l <= m->layers; ++l) {
         size_t sz = (size_t)n * m->dims[l];
@@ -742,12 +745,13 @@ void gro_model_forward(uint32_t n, const uint64_t* ro, const uint32_t* ci, const
 static double train_impl(uint32_t n, const uint64_t* ro, const uint32_t* ci, const double* x,
                          const int32_t* labels, uint32_t C, const gro_model* m, double* w,
                          double lr, double* grads, double* acts, double* dacts, uint32_t row_limit,
-                         uint32_t loss_rows, double loss_count, int nthreads) {
+                         uint32_t loss_rows, double loss_count, int nthreads,
+                         const uint32_t* layer_rows) {
     uint32_t L = m->layers;
     uint32_t rows = row_limit < n ? row_limit : n;
     if (loss_rows > rows) loss_rows = rows;
     fwd_state st;
-    forward_impl(n, rows, ro, ci, x, m, w, &st, nthreads);
+    forward_impl(n, rows, ro, ci, x, m, w, &st, nthreads, layer_rows);
 
     /* softmax cross-entropy over rows < loss_rows, normalised by loss_count */
     double* dH = (double*)calloc((size_t)n * C, sizeof(double));
@@ -840,13 +844,13 @@ double gro_train_epoch(uint32_t n, const uint64_t* ro, const uint32_t* ci, const
                        int nthreads) {
     uint32_t rows = row_limit < n ? row_limit : n;
     return train_impl(n, ro, ci, x, labels, C, m, w, lr, grads, acts, dacts, row_limit, rows,
-                      (double)rows, nthreads);
+                      (double)rows, nthreads, NULL);
 }
 
 double gro_train_epoch_masked(uint32_t n, const uint64_t* ro, const uint32_t* ci, const double* x,
                               const int32_t* labels, uint32_t C, const gro_model* m, double* w,
                               double lr, double* grads, uint32_t loss_rows, double loss_count,
-                              int nthreads) {
+                              const uint32_t* layer_rows, int nthreads) {
     return train_impl(n, ro, ci, x, labels, C, m, w, lr, grads, NULL, NULL, n, loss_rows, loss_count,
-                      nthreads);
+                      nthreads, layer_rows);
 }

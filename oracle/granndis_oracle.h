@@ -120,11 +120,13 @@ double gro_train_epoch(uint32_t n, const uint64_t* ro, const uint32_t* ci, const
 /* Same epoch with the loss restricted to rows < loss_rows and normalised by
  * loss_count (>= loss_rows: the global count when several subgraphs train
  * together); SGD is skipped when lr == 0 (gradients only, for summing across
- * subgraphs).  Returns the (partial) loss sum / loss_count. */
+ * subgraphs).  layer_rows (nullable, [layers]): layer l produces only rows <
+ * layer_rows[l] -- the hop masking of forward_server_local (reference_gnn.cpp:119-137)
+ * when local ids are ordered by hop.  Returns the (partial) loss sum / loss_count. */
 double gro_train_epoch_masked(uint32_t n, const uint64_t* ro, const uint32_t* ci, const double* x,
                               const int32_t* labels, uint32_t num_classes, const gro_model* m,
                               double* w, double lr, double* grads, uint32_t loss_rows,
-                              double loss_count, int nthreads);
+                              double loss_count, const uint32_t* layer_rows, int nthreads);
 
 #ifdef __cplusplus
 }

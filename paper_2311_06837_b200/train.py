@@ -222,6 +222,19 @@ class FullGraphTrainer:
             lab = torch.empty(max(n, 1), dtype=torch.int32, device=d)
             call("gdx_init_labels", label_seed, 0, n, cfg.classes, lab.data_ptr(), stream_handle())
             self.labels = lab[loc.l2g[:max(self.nloc, 1)].long()].contiguous()
+        # rows produced by each layer: everything in full-graph mode; in subgraph mode the
+        # hop masking of forward_server_local (reference_gnn.cpp:119-137): layer l (0-based)
+        # reads rows with hop <= L-l and produces rows with hop <= L-l-1, a prefix of the
+        # (hop, id)-ordered local ids; rows never produced stay zero.
+        Lc = cfg.layers
+        if self.subgraph_mode:
+            self.rows_in = [self.local.upto(Lc - l) for l in range(Lc)]
+            self.rows_out = [self.local.upto(Lc - l - 1) for l in range(Lc)]
+            if self.rows_in[0] < self.nloc:  # inputs beyond L hops are unavailable
+                self.X[self.rows_in[0]:].zero_()
+        else:
+            self.rows_in = [self.nloc] * Lc
+            self.rows_out = [self.nloc] * Lc
         self.inv_deg = torch.where(deg > 0, 1.0 / deg.clamp(min=1), torch.zeros_like(deg)).float()
         self.gcn_s = (1.0 / torch.sqrt(deg + 1.0)).float()
         # per-row sub-range of locally owned sources: aggregated while the all-gather runs
@@ -307,13 +320,15 @@ class FullGraphTrainer:
         ev = getattr(self, "_events", None) or []
         return (sum(a.elapsed_time(b) for a, b, _ in ev), len(ev), sum(x for _, _, x in ev))
 
-    def _exchange_aggregate(self, full: torch.Tensor, width: int, **epi):
+    def _exchange_aggregate(self, full: torch.Tensor, width: int, rows: int | None = None, **epi):
         """All-gather `full` and aggregate the owned rows from it.  With N > 1 the
         locally owned source block is aggregated while NCCL moves the remote blocks,
-        then the remote sources finish the rows with the fused epilogue."""
+        then the remote sources finish the rows with the fused epilogue.  rows:
+        aggregate only the first `rows` rows (hop masking in subgraph mode)."""
         if not self.overlap:
             self.exchange.allgather_rows(full)
-            return self._agg(self.csr, full, width, **epi)
+            csr = self.csr if rows is None or rows == self.csr.rows else self.csr.slice_rows(0, rows)
+            return self._agg(csr, full, width, **epi)
         work = self.exchange.allgather_rows_async(full)
         if work is None:  # gathered synchronously (unequal blocks)
             return self._agg(self.csr, full, width, **epi)
@@ -340,21 +355,23 @@ class FullGraphTrainer:
         for l, L in enumerate(self.layers):
             relu = l + 1 < cfg.layers
             own = L.Zfull[self.lo:self.hi]
+            m_in, r_out = self.rows_in[l], self.rows_out[l]
             if cfg.kind == "sage":
-                gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w)
+                gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w, m=m_in)
             elif cfg.kind == "gcn":
-                gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s)
+                gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s, m=m_in)
             else:
-                gemm_tn(A, L.Wsp, c0=own)
+                gemm_tn(A, L.Wsp, c0=own, m=m_in)
             if cfg.kind == "sage":
-                self._exchange_aggregate(L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=0.0,
-                                         self_base=self.lo, post_scale=self.inv_deg, add=L.S, relu=relu)
+                self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=L.Hout, out_split=L.Hsp,
+                                         self_coef=0.0, self_base=self.lo, post_scale=self.inv_deg,
+                                         add=L.S, relu=relu)
             elif cfg.kind == "gcn":
-                self._exchange_aggregate(L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=1.0,
-                                         self_base=self.lo, post_scale=self.gcn_s, relu=relu)
+                self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=L.Hout, out_split=L.Hsp,
+                                         self_coef=1.0, self_base=self.lo, post_scale=self.gcn_s, relu=relu)
             else:
-                self._exchange_aggregate(L.Zfull, L.w, out=L.Hout, out_split=L.Hsp, self_coef=1.0,
-                                         self_base=self.lo, relu=relu)
+                self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=L.Hout, out_split=L.Hsp,
+                                         self_coef=1.0, self_base=self.lo, relu=relu)
             A = L.Hsp
             if self.keep_activations:
                 acts.append(L.Hout[:self.nloc, :L.fout].clone())
@@ -380,20 +397,23 @@ class FullGraphTrainer:
         for l in range(nL - 1, -1, -1):
             L = self.layers[l]
             # dZ = agg^T(gs): SAGE -> G[:, w:2w]; GCN/SUM -> G (all columns)
+            r_in = self.rows_in[l]   # dZ is needed for the rows that fed layer l
             if cfg.kind == "sage":
                 Gn = _SplitView(L.G, L.w)
-                self._exchange_aggregate(L.dfull, L.w, out_split=Gn, self_coef=0.0, self_base=self.lo)
+                self._exchange_aggregate(L.dfull, L.w, rows=r_in, out_split=Gn, self_coef=0.0,
+                                         self_base=self.lo)
             elif cfg.kind == "gcn":
-                self._exchange_aggregate(L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo,
-                                         post_scale=self.gcn_s)
+                self._exchange_aggregate(L.dfull, L.w, rows=r_in, out_split=L.G, self_coef=1.0,
+                                         self_base=self.lo, post_scale=self.gcn_s)
             else:
-                self._exchange_aggregate(L.dfull, L.w, out_split=L.G, self_coef=1.0, self_base=self.lo)
+                self._exchange_aggregate(L.dfull, L.w, rows=r_in, out_split=L.G, self_coef=1.0,
+                                         self_base=self.lo)
             # dH_{l} = G W_cat (before this layer's update; W_cat read MN-major in place),
             # epilogue: ReLU backward with H_{l} as mask, scale, split -> layer l-1's inputs
             if l > 0:
                 own, scale, split = self._grad_targets(l - 1)
                 gemm_tn(L.G, L.Wsp, c0=own, b_mn=True, mask=self.layers[l - 1].Hout,
-                        row_scale=scale, out_split=split, split_unscaled=True)
+                        row_scale=scale, out_split=split, split_unscaled=True, m=self.rows_out[l - 1])
             # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
             gemm_tn(L.G, A_in, c0=L.ws, split_k=L.split_k, a_mn=True, b_mn=True)

@@ -71,7 +71,8 @@ def test_reddit_width_layer_parity(cuda):
     assert np.all(np.abs(lg - lr) <= 1e-3)
 
 
-@pytest.mark.parametrize("kind,m,k", [("gcn", 1, 15), ("sage", 2, 4), ("gcn", 3, O.UNLIMITED)])
+@pytest.mark.parametrize("kind,m,k", [("gcn", 1, 15), ("sage", 2, 4), ("gcn", 3, O.UNLIMITED),
+                                      ("sage", 5, 3), ("sum", 2, 6)])
 def test_subgraph_training_matches_oracle(cuda, kind, m, k):
     """EAS / preload mode: train on one server's preloaded inner + halo subgraph,
     loss on its inner vertices; the oracle runs the same epoch on the induced
@@ -105,7 +106,11 @@ def test_subgraph_training_matches_oracle(cuda, kind, m, k):
     model = O.Model({"sage": O.SAGE, "gcn": O.GCN}[kind], dims)
     w = np.concatenate([a.astype(np.float32).astype(np.float64).ravel() for a in w0])
     n_inner = len(sub.inner_vertices)
+    L = len(dims) - 1
+    hop_sorted = hop[order]
+    layer_rows = [int(np.sum(hop_sorted <= L - l - 1)) for l in range(L)]  # hop masking
     for e in range(6):
         lg = tr.train_epoch()
-        loss, grads = O.train_epoch_masked(lc, x, lab, model, w, 0.5, n_inner, float(n_inner), nthreads=4)
+        loss, grads = O.train_epoch_masked(lc, x, lab, model, w, 0.5, n_inner, float(n_inner),
+                                           nthreads=4, layer_rows=layer_rows)
         assert abs(lg - loss) <= 1e-3, (e, lg, loss)
