@@ -138,6 +138,12 @@ typedef struct gdx_gemm_args {
     const float* mask;        /* nullable [m x ld_mask]: C = 0 where mask <= 0 (ReLU backward) */
     uint64_t ld_mask;
     int split_unscaled;       /* 1: the split-bf16 copy is taken before row_scale */
+    /* Fused exchange: every value stored to output `peer_target` (0: c0, 1: c1) is also
+     * stored at the same offset in npeers peer buffers (address + peer_delta[r] bytes;
+     * CUDA IPC mappings over NVLink), see gdx_peer_signal/gdx_peer_wait. */
+    uint32_t npeers;
+    int peer_target;
+    int64_t peer_delta[7];
 } gdx_gemm_args;
 int gdx_gemm_tn(const gdx_gemm_args* g, gdx_stream stream);
 /* Reference-precision SIMT fallback of the same contract, for tests only. */
@@ -147,6 +153,25 @@ int gdx_gemm_tn_simt(const gdx_gemm_args* g, gdx_stream stream);
 int gdx_splitk_reduce(const float* ws, uint32_t split_k, uint64_t stride, uint32_t rows,
                       uint32_t cols, uint64_t ld, float* out, float* w, float lr,
                       uint16_t* w_hi, uint16_t* w_lo, gdx_stream stream);
+
+/* ------------------------------------------------------------------------
+ * Row exchange over NVLink peer memory (the a13 exchange of the trainer, fused
+ * into the producing GEMM / softmax epilogues instead of a separate all-gather).
+ * ---------------------------------------------------------------------- */
+int gdx_device_alloc(uint64_t bytes, void** out);      /* zeroed cudaMalloc (IPC-able base) */
+int gdx_device_free(void* p);
+int gdx_ipc_get_handle(const void* base, void* handle64);   /* 64-byte cudaIpcMemHandle */
+int gdx_ipc_open(const void* handle64, void** out);         /* lazy peer access enabled */
+int gdx_ipc_close(void* p);
+/* After the producing kernel: release its peer stores and increment this rank's slot
+ * in every peer's arrival array (peer_slots_dev: device array of npeers IPC-mapped
+ * u64 slot pointers). */
+int gdx_peer_signal(unsigned long long* const* peer_slots_dev, uint32_t npeers, gdx_stream stream);
+/* Before gathering remote rows: *expected += 1, spin (acquire, system scope) until
+ * slots[r] >= *expected for every r != self; traps after timeout_ns.  Device-side
+ * state only, so it can be captured in a CUDA graph and replayed. */
+int gdx_peer_wait(unsigned long long* slots, unsigned long long* expected, uint32_t world,
+                  uint32_t self, uint64_t timeout_ns, gdx_stream stream);
 
 /* ------------------------------------------------------------------------
  * Layout / elementwise helpers of the training extension (no reference code).
@@ -177,6 +202,12 @@ int gdx_softmax_xent_fused(const float* logits, uint64_t ld, uint32_t rows, uint
                            const int32_t* labels, float inv_count, float* dlogits, uint64_t ld_d,
                            const float* row_scale, float* gs, uint64_t ld_gs, uint16_t* g_hi,
                            uint16_t* g_lo, uint64_t ld_g, double* loss_sum, gdx_stream stream);
+/* Same, with gs also stored into npeers peer buffers (gs + gs_peer_delta[r] bytes). */
+int gdx_softmax_xent_fused_peers(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
+                                 const int32_t* labels, float inv_count, const float* row_scale,
+                                 float* gs, uint64_t ld_gs, uint16_t* g_hi, uint16_t* g_lo,
+                                 uint64_t ld_g, double* loss_sum, uint32_t npeers,
+                                 const int64_t* gs_peer_delta, gdx_stream stream);
 /* Bandwidth probe for roofline denominators: reads `bytes` of buf `reps` times,
  * mode 0 = coalesced stream, mode 1 = random 256 B row gathers (bytes moved =
  * reps * bytes in both modes).  Time it with events on `stream`. */

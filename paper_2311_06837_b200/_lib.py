@@ -37,7 +37,8 @@ class GemmArgs(C.Structure):
         ("m", u32), ("n", u32), ("k", u32), ("c0", vp), ("ldc0", u64), ("c1", vp), ("ldc1", u64),
         ("split", u32), ("row_scale", vp), ("relu", C.c_int), ("out_hi", vp), ("out_lo", vp),
         ("ld_split", u64), ("split_k", u32), ("mask", vp), ("ld_mask", u64),
-        ("split_unscaled", C.c_int),
+        ("split_unscaled", C.c_int), ("npeers", u32), ("peer_target", C.c_int),
+        ("peer_delta", C.c_int64 * 7),
     ]
 
 
@@ -62,6 +63,15 @@ _SIGS = {
     "gdx_transpose_split": (C.c_int, [vp, vp, u64, u32, u32, vp, vp, u64, vp]),
     "gdx_grad_prepare": (C.c_int, [vp, u64, vp, u64, u32, u32, vp, vp, u64, vp, u64, vp, vp, u64, vp]),
     "gdx_softmax_xent": (C.c_int, [vp, u64, u32, u32, vp, C.c_float, vp, u64, vp, vp]),
+    "gdx_softmax_xent_fused_peers": (C.c_int, [vp, u64, u32, u32, vp, C.c_float, vp, vp, u64, vp, vp,
+                                               u64, vp, u32, vp, vp]),
+    "gdx_device_alloc": (C.c_int, [u64, C.POINTER(vp)]),
+    "gdx_device_free": (C.c_int, [vp]),
+    "gdx_ipc_get_handle": (C.c_int, [vp, vp]),
+    "gdx_ipc_open": (C.c_int, [vp, C.POINTER(vp)]),
+    "gdx_ipc_close": (C.c_int, [vp]),
+    "gdx_peer_signal": (C.c_int, [vp, u32, vp]),
+    "gdx_peer_wait": (C.c_int, [vp, vp, u32, u32, u64, vp]),
     "gdx_softmax_xent_fused": (C.c_int, [vp, u64, u32, u32, vp, C.c_float, vp, u64, vp, vp, u64, vp, vp,
                                          u64, vp, vp]),
     "gdx_degree_scale": (C.c_int, [vp, u32, C.c_int, vp, vp]),

@@ -26,7 +26,7 @@ CU_FLAGS = ARCH + COMMON + ["-Xcompiler", "-fPIC,-ffp-contract=off", "--expt-rel
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
              "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include"]
 
-SOURCES_CU = ["aggregate.cu", "gemm_tcgen05.cu", "dense_ops.cu", "sampling.cu"]
+SOURCES_CU = ["aggregate.cu", "gemm_tcgen05.cu", "dense_ops.cu", "sampling.cu", "exchange.cu"]
 SOURCES_CXX = ["host.cpp"]
 
 

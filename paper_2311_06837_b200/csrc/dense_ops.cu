@@ -105,11 +105,16 @@ __global__ void grad_prepare_kernel(const float* dH, uint64_t ld_dh, const float
 
 // One warp per row.  Optional fused outputs of the last layer's backward prep:
 // split-bf16 copy of g = dlogits and gs = g * row_scale.
+struct PeerDeltas {
+    uint32_t n;
+    int64_t d[7];
+};
+
 __global__ void softmax_xent_kernel(const float* logits, uint64_t ld, uint32_t rows,
                                     uint32_t classes, const int32_t* labels, float inv_count,
                                     float* dlogits, uint64_t ld_d, const float* row_scale, float* gs,
                                     uint64_t ld_gs, uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g,
-                                    double* loss_sum) {
+                                    double* loss_sum, PeerDeltas peers) {
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -129,7 +134,12 @@ __global__ void softmax_xent_kernel(const float* logits, uint64_t ld, uint32_t r
             const float p = expf(z[c] - lse);
             const float g = (p - (static_cast<int32_t>(c) == y ? 1.f : 0.f)) * inv_count;
             if (dlogits) dlogits[static_cast<uint64_t>(r) * ld_d + c] = g;
-            if (gs) gs[static_cast<uint64_t>(r) * ld_gs + c] = g * rs;
+            if (gs) {
+                float* p = gs + static_cast<uint64_t>(r) * ld_gs + c;
+                *p = g * rs;
+                for (uint32_t q = 0; q < peers.n; ++q)
+                    *reinterpret_cast<float*>(reinterpret_cast<char*>(p) + peers.d[q]) = g * rs;
+            }
             if (g_hi) split_bf16(g, g_hi[static_cast<uint64_t>(r) * ld_g + c], g_lo[static_cast<uint64_t>(r) * ld_g + c]);
         }
         if (lane == 0) local += static_cast<double>(lse - z[y]);
@@ -302,7 +312,7 @@ extern "C" int gdx_softmax_xent(const float* logits, uint64_t ld, uint32_t rows,
     const uint64_t threads = static_cast<uint64_t>(rows) * 32;
     softmax_xent_kernel<<<grid_for(threads), 256, 0, as_cuda(stream)>>>(
         logits, ld, rows, classes, labels, inv_count, dlogits, ld_d, nullptr, nullptr, 0, nullptr,
-        nullptr, 0, loss_sum);
+        nullptr, 0, loss_sum, PeerDeltas{});
     note_launch();
     return check_launch("gdx_softmax_xent");
 }
@@ -319,9 +329,30 @@ extern "C" int gdx_softmax_xent_fused(const float* logits, uint64_t ld, uint32_t
     const uint64_t threads = static_cast<uint64_t>(rows) * 32;
     softmax_xent_kernel<<<grid_for(threads), 256, 0, as_cuda(stream)>>>(
         logits, ld, rows, classes, labels, inv_count, dlogits, ld_d, row_scale, gs, ld_gs, g_hi, g_lo,
-        ld_g, loss_sum);
+        ld_g, loss_sum, PeerDeltas{});
     note_launch();
     return check_launch("gdx_softmax_xent_fused");
+}
+
+extern "C" int gdx_softmax_xent_fused_peers(const float* logits, uint64_t ld, uint32_t rows,
+                                            uint32_t classes, const int32_t* labels, float inv_count,
+                                            const float* row_scale, float* gs, uint64_t ld_gs,
+                                            uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g,
+                                            double* loss_sum, uint32_t npeers,
+                                            const int64_t* gs_peer_delta, gdx_stream stream) {
+    GDX_REQUIRE(logits && labels && loss_sum && gs, GDX_INPUT, "gdx_softmax_xent_fused_peers: null pointer");
+    GDX_REQUIRE(npeers <= 7 && (npeers == 0 || gs_peer_delta), GDX_INPUT,
+                "gdx_softmax_xent_fused_peers: at most 7 peers");
+    GDX_REQUIRE(!g_hi == !g_lo, GDX_INPUT, "gdx_softmax_xent_fused_peers: g_hi/g_lo must pair");
+    if (!rows) return GDX_OK;
+    PeerDeltas pd{npeers, {}};
+    for (uint32_t r = 0; r < npeers; ++r) pd.d[r] = gs_peer_delta[r];
+    const uint64_t threads = static_cast<uint64_t>(rows) * 32;
+    softmax_xent_kernel<<<grid_for(threads), 256, 0, as_cuda(stream)>>>(
+        logits, ld, rows, classes, labels, inv_count, nullptr, 0, row_scale, gs, ld_gs, g_hi, g_lo, ld_g,
+        loss_sum, pd);
+    note_launch();
+    return check_launch("gdx_softmax_xent_fused_peers");
 }
 
 extern "C" int gdx_degree_scale(const uint64_t* row_ptr, uint32_t rows, int kind, float* out,

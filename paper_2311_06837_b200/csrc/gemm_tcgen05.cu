@@ -171,7 +171,23 @@ struct Epi {
     const float* mask;
     uint64_t ld_mask;
     int split_unscaled;
+    uint32_t npeers;        // fused exchange: peer copies of output `peer_target`
+    int peer_target;
+    int64_t peer_delta[7];
 };
+
+// store one float4 locally and, for the exchanged output, into every peer buffer
+__device__ __forceinline__ void store4x(float* p, const float4& v, const Epi& ep, bool xchg) {
+    *reinterpret_cast<float4*>(p) = v;
+    if (xchg)
+        for (uint32_t r = 0; r < ep.npeers; ++r)
+            *reinterpret_cast<float4*>(reinterpret_cast<char*>(p) + ep.peer_delta[r]) = v;
+}
+__device__ __forceinline__ void store1x(float* p, float v, const Epi& ep, bool xchg) {
+    *p = v;
+    if (xchg)
+        for (uint32_t r = 0; r < ep.npeers; ++r) *reinterpret_cast<float*>(reinterpret_cast<char*>(p) + ep.peer_delta[r]) = v;
+}
 
 template <int BN, int STAGES>
 struct Smem {
@@ -385,25 +401,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     // a 16-column group entirely on one side of the split: 4 x 16 B stores
                     float* base = nullptr;
+                    bool xchg = false;
                     if (col0 + 16 <= ep.n) {
-                        if (col0 + 16 <= ep.split && ep.c0 && ep.ldc0 % 4 == 0)
+                        if (col0 + 16 <= ep.split && ep.c0 && ep.ldc0 % 4 == 0) {
                             base = ep.c0 + static_cast<uint64_t>(row) * ep.ldc0 + col0;
-                        else if (col0 >= ep.split && ep.c1 && ep.ldc1 % 4 == 0 && (col0 - ep.split) % 4 == 0)
+                            xchg = ep.npeers && ep.peer_target == 0;
+                        } else if (col0 >= ep.split && ep.c1 && ep.ldc1 % 4 == 0 && (col0 - ep.split) % 4 == 0) {
                             base = ep.c1 + static_cast<uint64_t>(row) * ep.ldc1 + (col0 - ep.split);
+                            xchg = ep.npeers && ep.peer_target == 1;
+                        }
                     }
                     if (base && (reinterpret_cast<uintptr_t>(base) & 15) == 0) {
 #pragma unroll
                         for (int j = 0; j < 16; j += 4)
-                            *reinterpret_cast<float4*>(base + j) = make_float4(vv[j], vv[j + 1], vv[j + 2], vv[j + 3]);
+                            store4x(base + j, make_float4(vv[j], vv[j + 1], vv[j + 2], vv[j + 3]), ep, xchg);
                     } else {
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const uint32_t col = col0 + j;
                             if (col >= ep.n) continue;
                             if (col < ep.split) {
-                                if (ep.c0) ep.c0[static_cast<uint64_t>(row) * ep.ldc0 + col] = vv[j];
+                                if (ep.c0) store1x(ep.c0 + static_cast<uint64_t>(row) * ep.ldc0 + col, vv[j], ep,
+                                                   ep.npeers && ep.peer_target == 0);
                             } else if (ep.c1) {
-                                ep.c1[static_cast<uint64_t>(row) * ep.ldc1 + (col - ep.split)] = vv[j];
+                                store1x(ep.c1 + static_cast<uint64_t>(row) * ep.ldc1 + (col - ep.split), vv[j], ep,
+                                        ep.npeers && ep.peer_target == 1);
                             }
                         }
                     }
@@ -451,9 +473,9 @@ __global__ void gemm_simt_kernel(const uint16_t* a_hi, const uint16_t* a_lo, uin
     float x = acc * (ep.row_scale ? ep.row_scale[row] : 1.f);
     if (ep.relu) x = fmaxf(x, 0.f);
     if (col < ep.split) {
-        if (ep.c0) ep.c0[row * ep.ldc0 + col] = x;
+        if (ep.c0) store1x(ep.c0 + row * ep.ldc0 + col, x, ep, ep.npeers && ep.peer_target == 0);
     } else if (ep.c1) {
-        ep.c1[row * ep.ldc1 + col - ep.split] = x;
+        store1x(ep.c1 + row * ep.ldc1 + col - ep.split, x, ep, ep.npeers && ep.peer_target == 1);
     }
     if (ep.out_hi && !ep.split_unscaled)
         split_bf16(x, ep.out_hi[row * ep.ld_split + col], ep.out_lo[row * ep.ld_split + col]);
@@ -551,6 +573,8 @@ int validate(const gdx_gemm_args* g) {
     GDX_REQUIRE(!g->out_hi == !g->out_lo, GDX_INPUT, "gdx_gemm_tn: out_hi/out_lo must pair");
     GDX_REQUIRE(g->split_k <= 1 || g->c0, GDX_INPUT, "gdx_gemm_tn: split_k needs c0 workspace");
     GDX_REQUIRE(!g->mask || g->ld_mask >= g->n, GDX_INPUT, "gdx_gemm_tn: ld_mask < n");
+    GDX_REQUIRE(g->npeers <= 7, GDX_INPUT, "gdx_gemm_tn: at most 7 peers");
+    GDX_REQUIRE(g->npeers == 0 || g->split_k <= 1, GDX_INPUT, "gdx_gemm_tn: peers with split_k");
     return GDX_OK;
 }
 
@@ -558,7 +582,8 @@ Epi make_epi(const gdx_gemm_args* g, int bn) {
     Epi ep{g->m, g->n, g->c0, g->ldc0, g->c1, g->ldc1, g->split, g->row_scale, g->relu,
            g->out_hi, g->out_lo, g->ld_split, g->split_k ? g->split_k : 1,
            (g->k + BK - 1) / BK, (g->m + BM - 1) / BM, (g->n + bn - 1) / bn,
-           g->mask, g->ld_mask, g->split_unscaled};
+           g->mask, g->ld_mask, g->split_unscaled, g->npeers, g->peer_target, {}};
+    for (int r = 0; r < 7; ++r) ep.peer_delta[r] = g->peer_delta[r];
     return ep;
 }
 

@@ -131,7 +131,7 @@ def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_spli
 
 def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None, relu=False,
             out_split: Split | None = None, split_k: int = 1, m=None, simt=False, a_mn=False,
-            b_mn=False, mask=None, split_unscaled=False, stream=None):
+            b_mn=False, mask=None, split_unscaled=False, peers=None, stream=None):
     """K2: C(m, n) = sum_k A(m, k) B(n, k).  A is stored [m][k] (K-major) or, with
     a_mn, [k][m]; likewise B ([n][k] or [k][n]).  See gdx_gemm_tn."""
     mA, kA = (A.cols, A.rows) if a_mn else (A.rows, A.cols)
@@ -157,6 +157,11 @@ def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None,
     if mask is not None:
         g.mask, g.ld_mask = mask.data_ptr(), mask.stride(0)
     g.split_unscaled = int(split_unscaled)
+    if peers is not None:  # (target output, byte deltas): fused NVLink exchange
+        target, deltas = peers
+        g.npeers, g.peer_target = len(deltas), int(target)
+        for i, dl in enumerate(deltas):
+            g.peer_delta[i] = int(dl)
     call("gdx_gemm_tn_simt" if simt else "gdx_gemm_tn", _lib.C.byref(g), stream_handle(stream))
 
 

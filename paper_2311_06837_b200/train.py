@@ -25,6 +25,7 @@ fp64 oracle restatement (parity unpinned: no reference implementation exists).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -96,7 +97,7 @@ def agg_width(fout: int, rows: int) -> int:
 class _Layer:
     """Device state of one layer: W_cat (fp32 master + split copies), buffers."""
 
-    def __init__(self, kind, fin, fout, nloc, nfull, d, splitk_target, first, fin_w=None):
+    def __init__(self, kind, fin, fout, nloc, nfull, d, splitk_target, first, fin_w=None, p2p=None):
         self.kind, self.fin, self.fout = kind, fin, fout
         # GEMM K: the input operand's logical width (the previous layer's row width)
         self.k = fin if first else (fin_w if fin_w is not None else pad8(fin))
@@ -113,11 +114,16 @@ class _Layer:
         self.ws = torch.zeros((self.split_k * self.nz, self.fin_ld), dtype=torch.float32, device=d)
         # activations
         self.S = dense(nloc, self.w, d) if kind == "sage" else None     # SAGE self path
-        self.Zfull = dense(nfull, self.w, d)                             # gathered rows
+        if p2p is None:
+            self.Zfull = dense(nfull, self.w, d)                         # gathered rows
+            self.dfull = dense(nfull, self.w, d)                         # gathered grads
+            self.z_peers = self.d_peers = None
+        else:   # shared with the peers: producers store straight into every rank's copy
+            self.Zfull, self.z_peers = p2p.buffer(nfull, self.w)
+            self.dfull, self.d_peers = p2p.buffer(nfull, self.w)
         self.Hout = dense(nloc, self.w, d)                               # act output fp32
         self.Hsp = Split(nloc, self.w, d)                                # next layer's A
         self.G = Split(nloc, self.nz, d)                                 # [dP | dZn] or dZ
-        self.dfull = dense(nfull, self.w, d)                             # gathered grads
 
     def set_weights(self, mats):
         """mats: [W] or [W_self, W_neigh] (fout x fin each), fp64 numpy."""
@@ -238,8 +244,9 @@ class FullGraphTrainer:
         self.inv_deg = torch.where(deg > 0, 1.0 / deg.clamp(min=1), torch.zeros_like(deg)).float()
         self.gcn_s = (1.0 / torch.sqrt(deg + 1.0)).float()
         # per-row sub-range of locally owned sources: aggregated while the all-gather runs
-        import os
-        self.overlap = (not self.subgraph_mode) and world > 1 and os.environ.get("GDX_OVERLAP", "1") != "0"
+        use_p2p = (not self.subgraph_mode) and world > 1 and os.environ.get("GDX_EXCHANGE", "p2p") == "p2p"
+        self.overlap = (not self.subgraph_mode) and world > 1 and (
+            use_p2p or os.environ.get("GDX_OVERLAP", "1") != "0")
         if self.overlap:
             self.seg_lo = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
             self.seg_hi = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
@@ -248,13 +255,15 @@ class FullGraphTrainer:
             self.nnz_local_src = int((self.seg_hi - self.seg_lo)[:self.nloc].sum().item())
         self.Xsp = Split(self.nloc, F, d)
         self._refresh_input_splits()
+        # row exchange: fused NVLink peer stores (default) or NCCL all-gather
+        self.p2p = P2PExchange(rank, world, pg, d) if use_p2p else None
         # layers
         sm = torch.cuda.get_device_properties(d).multi_processor_count
         self.layers = []
         for l in range(cfg.layers):
             self.layers.append(_Layer(cfg.kind, cfg.dims[l], cfg.dims[l + 1], self.nloc,
                                       self.nrows_gather, d, 2 * sm, l == 0,
-                                      self.layers[-1].w if l else None))
+                                      self.layers[-1].w if l else None, p2p=self.p2p))
         # all weight gradients (+ the loss) in one flat buffer: one all-reduce per epoch
         sizes = [L.nz * L.fin_ld for L in self.layers]
         self.grad_flat = torch.zeros(sum(sizes) + 1, dtype=torch.float32, device=d)
@@ -325,6 +334,13 @@ class FullGraphTrainer:
         locally owned source block is aggregated while NCCL moves the remote blocks,
         then the remote sources finish the rows with the fused epilogue.  rows:
         aggregate only the first `rows` rows (hop masking in subgraph mode)."""
+        if self.p2p is not None:
+            # the producer already pushed our rows into every peer and signalled;
+            # aggregate the owned sources, wait for the peers' rows, finish the rest
+            P = self.partial[:, :pad4(width)] if self.partial.shape[1] != pad4(width) else self.partial
+            self._agg(self.csr, full, width, out=P, row_begin=self.seg_lo, row_end=self.seg_hi)
+            self.p2p.wait()
+            return self._agg(self.csr, full, width, skip=(self.seg_lo, self.seg_hi), partial=P, **epi)
         if not self.overlap:
             self.exchange.allgather_rows(full)
             csr = self.csr if rows is None or rows == self.csr.rows else self.csr.slice_rows(0, rows)
@@ -357,11 +373,13 @@ class FullGraphTrainer:
             own = L.Zfull[self.lo:self.hi]
             m_in, r_out = self.rows_in[l], self.rows_out[l]
             if cfg.kind == "sage":
-                gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w, m=m_in)
+                gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w, m=m_in, peers=self._peers(L.z_peers, 1))
             elif cfg.kind == "gcn":
-                gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s, m=m_in)
+                gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s, m=m_in, peers=self._peers(L.z_peers, 0))
             else:
-                gemm_tn(A, L.Wsp, c0=own, m=m_in)
+                gemm_tn(A, L.Wsp, c0=own, m=m_in, peers=self._peers(L.z_peers, 0))
+            if self.p2p is not None:
+                self.p2p.signal()
             if cfg.kind == "sage":
                 self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=L.Hout, out_split=L.Hsp,
                                          self_coef=0.0, self_base=self.lo, post_scale=self.inv_deg,
@@ -377,6 +395,9 @@ class FullGraphTrainer:
                 acts.append(L.Hout[:self.nloc, :L.fout].clone())
         self.activations = acts
         return self.layers[-1].Hout
+
+    def _peers(self, deltas, target: int):
+        return None if (self.p2p is None or deltas is None) else (target, deltas)
 
     def _grad_targets(self, l: int):
         """Where the prepared gradient of layer l's output goes: gs = g * dst_scale into the
@@ -413,7 +434,10 @@ class FullGraphTrainer:
             if l > 0:
                 own, scale, split = self._grad_targets(l - 1)
                 gemm_tn(L.G, L.Wsp, c0=own, b_mn=True, mask=self.layers[l - 1].Hout,
-                        row_scale=scale, out_split=split, split_unscaled=True, m=self.rows_out[l - 1])
+                        row_scale=scale, out_split=split, split_unscaled=True, m=self.rows_out[l - 1],
+                        peers=self._peers(self.layers[l - 1].d_peers, 0))
+                if self.p2p is not None:
+                    self.p2p.signal()
             # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
             gemm_tn(L.G, A_in, c0=L.ws, split_k=L.split_k, a_mn=True, b_mn=True)
@@ -438,12 +462,22 @@ class FullGraphTrainer:
         self.loss_acc.zero_()
         logits = self.forward()
         own, scale, split = self._grad_targets(self.cfg.layers - 1)
-        call("gdx_softmax_xent_fused", logits.data_ptr(), logits.shape[1], self.loss_rows,
-             self.cfg.classes, self.labels.data_ptr(), 1.0 / self.loss_count, None, 0,
-             _lib.ptr(scale), own.data_ptr(), own.stride(0),
-             _lib.ptr(split.hi) if split is not None else None,
-             _lib.ptr(split.lo) if split is not None else None, split.ld if split is not None else 0,
-             self.loss_acc.data_ptr(), stream_handle())
+        if self.p2p is not None:
+            Lz = self.layers[-1]
+            deltas = (_lib.C.c_int64 * 7)(*Lz.d_peers)
+            call("gdx_softmax_xent_fused_peers", logits.data_ptr(), logits.shape[1], self.loss_rows,
+                 self.cfg.classes, self.labels.data_ptr(), 1.0 / self.loss_count, _lib.ptr(scale),
+                 own.data_ptr(), own.stride(0), _lib.ptr(split.hi) if split is not None else None,
+                 _lib.ptr(split.lo) if split is not None else None, split.ld if split is not None else 0,
+                 self.loss_acc.data_ptr(), len(Lz.d_peers), deltas, stream_handle())
+            self.p2p.signal()
+        else:
+            call("gdx_softmax_xent_fused", logits.data_ptr(), logits.shape[1], self.loss_rows,
+                 self.cfg.classes, self.labels.data_ptr(), 1.0 / self.loss_count, None, 0,
+                 _lib.ptr(scale), own.data_ptr(), own.stride(0),
+                 _lib.ptr(split.hi) if split is not None else None,
+                 _lib.ptr(split.lo) if split is not None else None,
+                 split.ld if split is not None else 0, self.loss_acc.data_ptr(), stream_handle())
         self.backward_and_step()  # (multi-GPU: the loss rides on the gradient all-reduce)
         if sync_loss:
             return float(self.loss_acc.item()) / self.loss_count
@@ -515,6 +549,88 @@ class FeatureStream:
             tr.labels.copy_(self.labels[i])
         self.free[i].record(cur)
         self.consumed += 1
+
+
+class _RawCUDA:
+    """CUDA Array Interface wrapper so torch can view memory libgdx allocated."""
+
+    def __init__(self, ptr: int, shape, typestr: str = "<f4"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class P2PExchange:
+    """Row exchange fused into the producers over NVLink peer memory.
+
+    Each gathered buffer is a separate cudaMalloc allocation whose CUDA IPC handle is
+    shared with every rank; the producing GEMM / softmax epilogue stores each owned
+    row into the local buffer AND at the same offset in every peer's buffer
+    (peer_delta), then `signal()` bumps this rank's slot in every peer's arrival
+    array; `wait()` (before the remote-source aggregation) spins until every peer's
+    slot reached the round.  No all-gather kernel, no staging copy."""
+
+    TIMEOUT_NS = 20_000_000_000  # a wedged peer traps after 20 s instead of hanging
+
+    def __init__(self, rank: int, world: int, pg, device):
+        import torch.distributed as dist
+        self.rank, self.world, self.pg, self.d = rank, world, pg, device
+        self._owned, self._opened = [], []
+        self.slots = self._alloc(8 * world)            # arrival slot per source rank
+        self.expected = self._alloc(8)                 # rounds this rank has waited for
+        handles = self._gather_handle(self.slots)
+        peer_slot_ptrs = []
+        for r in range(world):
+            if r == rank:
+                continue
+            base = self._open(handles[r])
+            peer_slot_ptrs.append(base + 8 * rank)      # our slot in peer r's array
+        self.peer_slots_dev = torch.tensor(peer_slot_ptrs, dtype=torch.int64, device=device)
+        dist.barrier(group=pg)
+
+    def _alloc(self, nbytes: int) -> int:
+        p = _lib.C.c_void_p()
+        call("gdx_device_alloc", nbytes, _lib.C.byref(p))
+        self._owned.append(p.value)
+        return p.value
+
+    def _open(self, handle: bytes) -> int:
+        buf = _lib.C.create_string_buffer(handle, 64)
+        p = _lib.C.c_void_p()
+        call("gdx_ipc_open", buf, _lib.C.byref(p))
+        self._opened.append(p.value)
+        return p.value
+
+    def _gather_handle(self, ptr: int) -> list:
+        import torch.distributed as dist
+        h = _lib.C.create_string_buffer(64)
+        call("gdx_ipc_get_handle", ptr, h)
+        out = [None] * self.world
+        dist.all_gather_object(out, h.raw, group=self.pg)
+        return out
+
+    def buffer(self, rows: int, cols: int):
+        """Zeroed [rows, cols] fp32 buffer shared with every peer; returns
+        (tensor, byte deltas to the same address in each peer's buffer)."""
+        ptr = self._alloc(rows * cols * 4)
+        t = torch.as_tensor(_RawCUDA(ptr, (rows, cols)), device=self.d)
+        handles = self._gather_handle(ptr)
+        deltas = [self._open(handles[r]) - ptr for r in range(self.world) if r != self.rank]
+        return t, deltas
+
+    def signal(self):
+        call("gdx_peer_signal", self.peer_slots_dev.data_ptr(), self.world - 1, stream_handle())
+
+    def wait(self):
+        call("gdx_peer_wait", self.slots, self.expected, self.world, self.rank, self.TIMEOUT_NS,
+             stream_handle())
+
+    def close(self):
+        for p in self._opened:
+            _lib.lib().gdx_ipc_close(p)
+        self._opened = []
+        for p in self._owned:
+            _lib.lib().gdx_device_free(p)
+        self._owned = []
 
 
 class RowExchange:
