@@ -163,6 +163,8 @@ int gdx_device_free(void* p);
 int gdx_ipc_get_handle(const void* base, void* handle64);   /* 64-byte cudaIpcMemHandle */
 int gdx_ipc_open(const void* handle64, void** out);         /* lazy peer access enabled */
 int gdx_ipc_close(void* p);
+/* One copy-engine push (cudaMemcpyAsync D2D; dst may be an IPC-mapped peer address). */
+int gdx_memcpy_async(void* dst, const void* src, uint64_t bytes, gdx_stream stream);
 /* After the producing kernel: release its peer stores and increment this rank's slot
  * in every peer's arrival array (peer_slots_dev: device array of npeers IPC-mapped
  * u64 slot pointers). */

@@ -102,3 +102,11 @@ extern "C" int gdx_peer_wait(unsigned long long* slots, unsigned long long* expe
     note_launch();
     return check_launch("gdx_peer_wait");
 }
+
+// Copy-engine push of a contiguous block to a peer's IPC-mapped buffer (NVLink).
+extern "C" int gdx_memcpy_async(void* dst, const void* src, uint64_t bytes, gdx_stream stream) {
+    GDX_REQUIRE((dst && src) || bytes == 0, GDX_INPUT, "gdx_memcpy_async: null pointer");
+    if (!bytes) return GDX_OK;
+    GDX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_cuda(stream)));
+    return GDX_OK;
+}

@@ -244,7 +244,8 @@ class FullGraphTrainer:
         self.inv_deg = torch.where(deg > 0, 1.0 / deg.clamp(min=1), torch.zeros_like(deg)).float()
         self.gcn_s = (1.0 / torch.sqrt(deg + 1.0)).float()
         # per-row sub-range of locally owned sources: aggregated while the all-gather runs
-        use_p2p = (not self.subgraph_mode) and world > 1 and os.environ.get("GDX_EXCHANGE", "p2p") == "p2p"
+        xmode = os.environ.get("GDX_EXCHANGE", "p2p")
+        use_p2p = (not self.subgraph_mode) and world > 1 and xmode in ("p2p", "p2p-epilogue")
         self.overlap = (not self.subgraph_mode) and world > 1 and (
             use_p2p or os.environ.get("GDX_OVERLAP", "1") != "0")
         if self.overlap:
@@ -256,7 +257,8 @@ class FullGraphTrainer:
         self.Xsp = Split(self.nloc, F, d)
         self._refresh_input_splits()
         # row exchange: fused NVLink peer stores (default) or NCCL all-gather
-        self.p2p = P2PExchange(rank, world, pg, d) if use_p2p else None
+        self.p2p = P2PExchange(rank, world, pg, d, "epilogue" if xmode == "p2p-epilogue" else "ce") \
+            if use_p2p else None
         # layers
         sm = torch.cuda.get_device_properties(d).multi_processor_count
         self.layers = []
@@ -378,8 +380,7 @@ class FullGraphTrainer:
                 gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s, m=m_in, peers=self._peers(L.z_peers, 0))
             else:
                 gemm_tn(A, L.Wsp, c0=own, m=m_in, peers=self._peers(L.z_peers, 0))
-            if self.p2p is not None:
-                self.p2p.signal()
+            self._publish(own, L.z_peers)
             if cfg.kind == "sage":
                 self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=L.Hout, out_split=L.Hsp,
                                          self_coef=0.0, self_base=self.lo, post_scale=self.inv_deg,
@@ -397,7 +398,18 @@ class FullGraphTrainer:
         return self.layers[-1].Hout
 
     def _peers(self, deltas, target: int):
-        return None if (self.p2p is None or deltas is None) else (target, deltas)
+        if self.p2p is None or deltas is None or self.p2p.mode != "epilogue":
+            return None
+        return (target, deltas)
+
+    def _publish(self, own: torch.Tensor, deltas):
+        """After the producer of an exchanged buffer: make our rows visible to peers."""
+        if self.p2p is None:
+            return
+        if self.p2p.mode == "epilogue":
+            self.p2p.signal()
+        else:
+            self.p2p.push(own, deltas)
 
     def _grad_targets(self, l: int):
         """Where the prepared gradient of layer l's output goes: gs = g * dst_scale into the
@@ -436,8 +448,7 @@ class FullGraphTrainer:
                 gemm_tn(L.G, L.Wsp, c0=own, b_mn=True, mask=self.layers[l - 1].Hout,
                         row_scale=scale, out_split=split, split_unscaled=True, m=self.rows_out[l - 1],
                         peers=self._peers(self.layers[l - 1].d_peers, 0))
-                if self.p2p is not None:
-                    self.p2p.signal()
+                self._publish(own, self.layers[l - 1].d_peers)
             # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
             gemm_tn(L.G, A_in, c0=L.ws, split_k=L.split_k, a_mn=True, b_mn=True)
@@ -462,7 +473,7 @@ class FullGraphTrainer:
         self.loss_acc.zero_()
         logits = self.forward()
         own, scale, split = self._grad_targets(self.cfg.layers - 1)
-        if self.p2p is not None:
+        if self.p2p is not None and self.p2p.mode == "epilogue":
             Lz = self.layers[-1]
             deltas = (_lib.C.c_int64 * 7)(*Lz.d_peers)
             call("gdx_softmax_xent_fused_peers", logits.data_ptr(), logits.shape[1], self.loss_rows,
@@ -478,6 +489,8 @@ class FullGraphTrainer:
                  _lib.ptr(split.hi) if split is not None else None,
                  _lib.ptr(split.lo) if split is not None else None,
                  split.ld if split is not None else 0, self.loss_acc.data_ptr(), stream_handle())
+            if self.p2p is not None:
+                self._publish(own, self.layers[-1].d_peers)
         self.backward_and_step()  # (multi-GPU: the loss rides on the gradient all-reduce)
         if sync_loss:
             return float(self.loss_acc.item()) / self.loss_count
@@ -571,9 +584,16 @@ class P2PExchange:
 
     TIMEOUT_NS = 20_000_000_000  # a wedged peer traps after 20 s instead of hanging
 
-    def __init__(self, rank: int, world: int, pg, device):
+    def __init__(self, rank: int, world: int, pg, device, mode: str = "ce"):
+        """mode 'ce': the producer writes locally; copy engines push the owned rows to
+        every peer on a side stream, overlapping the local-source aggregation (no SMs
+        spent on the transfer).  mode 'epilogue': the GEMM / softmax epilogue itself
+        stores into the peers (bulk async copies of each finished tile)."""
         import torch.distributed as dist
         self.rank, self.world, self.pg, self.d = rank, world, pg, device
+        self.mode = mode
+        self.side = torch.cuda.Stream(device=device)
+        self.pushed = None
         self._owned, self._opened = [], []
         self.slots = self._alloc(8 * world)            # arrival slot per source rank
         self.expected = self._alloc(8)                 # rounds this rank has waited for
@@ -620,7 +640,22 @@ class P2PExchange:
     def signal(self):
         call("gdx_peer_signal", self.peer_slots_dev.data_ptr(), self.world - 1, stream_handle())
 
+    def push(self, own: torch.Tensor, deltas):
+        """'ce' mode: after the producer, copy the owned (contiguous) rows into every
+        peer's buffer on the side stream with copy engines, then signal the peers."""
+        main = torch.cuda.current_stream()
+        self.side.wait_stream(main)
+        nbytes = own.numel() * own.element_size()
+        with torch.cuda.stream(self.side):
+            for dl in deltas:
+                call("gdx_memcpy_async", own.data_ptr() + dl, own.data_ptr(), nbytes, stream_handle())
+            self.signal()
+        self.pushed = True
+
     def wait(self):
+        if self.pushed:  # our pushes finished (the side stream joins the main stream)
+            torch.cuda.current_stream().wait_stream(self.side)
+            self.pushed = None
         call("gdx_peer_wait", self.slots, self.expected, self.world, self.rank, self.TIMEOUT_NS,
              stream_handle())
 
