@@ -246,8 +246,9 @@ class FullGraphTrainer:
         # per-row sub-range of locally owned sources: aggregated while the all-gather runs
         xmode = os.environ.get("GDX_EXCHANGE", "p2p")
         use_p2p = (not self.subgraph_mode) and world > 1 and xmode in ("p2p", "p2p-epilogue")
+        self.p2p_split = use_p2p and os.environ.get("GDX_P2P_SPLIT", "1") != "0"
         self.overlap = (not self.subgraph_mode) and world > 1 and (
-            use_p2p or os.environ.get("GDX_OVERLAP", "1") != "0")
+            self.p2p_split or (not use_p2p and os.environ.get("GDX_OVERLAP", "1") != "0"))
         if self.overlap:
             self.seg_lo = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
             self.seg_hi = torch.empty(max(self.nloc, 1), dtype=torch.int64, device=d)
@@ -336,6 +337,9 @@ class FullGraphTrainer:
         locally owned source block is aggregated while NCCL moves the remote blocks,
         then the remote sources finish the rows with the fused epilogue.  rows:
         aggregate only the first `rows` rows (hop masking in subgraph mode)."""
+        if self.p2p is not None and not self.p2p_split:
+            self.p2p.wait()
+            return self._agg(self.csr, full, width, **epi)
         if self.p2p is not None:
             # the producer already pushed our rows into every peer and signalled;
             # aggregate the owned sources, wait for the peers' rows, finish the rest
@@ -573,14 +577,16 @@ class _RawCUDA:
 
 
 class P2PExchange:
-    """Row exchange fused into the producers over NVLink peer memory.
+    """Row exchange over NVLink peer memory, no NCCL on the data path.
 
     Each gathered buffer is a separate cudaMalloc allocation whose CUDA IPC handle is
-    shared with every rank; the producing GEMM / softmax epilogue stores each owned
-    row into the local buffer AND at the same offset in every peer's buffer
-    (peer_delta), then `signal()` bumps this rank's slot in every peer's arrival
-    array; `wait()` (before the remote-source aggregation) spins until every peer's
-    slot reached the round.  No all-gather kernel, no staging copy."""
+    shared with every rank.  After the producer (GEMM / softmax) has written this
+    rank's rows into its own buffer, the rows are pushed to the same offset in every
+    peer's buffer (peer_delta) -- by copy engines, one stream per peer so the copies
+    run concurrently and use no SMs ('ce'), or by the producer's epilogue itself
+    ('epilogue') -- and each peer's arrival slot for this rank is bumped.  `wait()`
+    (before the remote-source aggregation) spins until every peer's slot reached
+    the round."""
 
     TIMEOUT_NS = 20_000_000_000  # a wedged peer traps after 20 s instead of hanging
 
@@ -592,7 +598,7 @@ class P2PExchange:
         import torch.distributed as dist
         self.rank, self.world, self.pg, self.d = rank, world, pg, device
         self.mode = mode
-        self.side = torch.cuda.Stream(device=device)
+        self.sides = [torch.cuda.Stream(device=device) for _ in range(world - 1)]
         self.pushed = None
         self._owned, self._opened = [], []
         self.slots = self._alloc(8 * world)            # arrival slot per source rank
@@ -641,20 +647,23 @@ class P2PExchange:
         call("gdx_peer_signal", self.peer_slots_dev.data_ptr(), self.world - 1, stream_handle())
 
     def push(self, own: torch.Tensor, deltas):
-        """'ce' mode: after the producer, copy the owned (contiguous) rows into every
-        peer's buffer on the side stream with copy engines, then signal the peers."""
+        """'ce' mode: after the producer, copy the owned (contiguous) rows into each
+        peer's buffer on that peer's stream (copy engines), then signal that peer."""
         main = torch.cuda.current_stream()
-        self.side.wait_stream(main)
         nbytes = own.numel() * own.element_size()
-        with torch.cuda.stream(self.side):
-            for dl in deltas:
+        slot0 = self.peer_slots_dev.data_ptr()
+        for i, (dl, st) in enumerate(zip(deltas, self.sides)):
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
                 call("gdx_memcpy_async", own.data_ptr() + dl, own.data_ptr(), nbytes, stream_handle())
-            self.signal()
+                call("gdx_peer_signal", slot0 + 8 * i, 1, stream_handle())
         self.pushed = True
 
     def wait(self):
-        if self.pushed:  # our pushes finished (the side stream joins the main stream)
-            torch.cuda.current_stream().wait_stream(self.side)
+        if self.pushed:  # our pushes finished (the peer streams join the main stream)
+            main = torch.cuda.current_stream()
+            for st in self.sides:
+                main.wait_stream(st)
             self.pushed = None
         call("gdx_peer_wait", self.slots, self.expected, self.world, self.rank, self.TIMEOUT_NS,
              stream_handle())

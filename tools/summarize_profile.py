@@ -71,7 +71,7 @@ def main():
     rr = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rr[0], rr[1], rr[2:]
     idx = {h: i for i, h in enumerate(hdr)}
-    out = ["# ncu --set full --clock-control none, kernels aggregate_vec4 / gemm_tn_bf16x3 "
+    out = ["# ncu --set full --clock-control none, kernels aggregate_vec4 / gemm_bf16x3 "
            "captured inside python bench.py --steps 2 --warmup 3"]
     agg_dram = []
     for d in data:
