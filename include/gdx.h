@@ -271,6 +271,12 @@ int gdx_exclusive_scan_u64(const uint64_t* counts, uint64_t n, uint64_t* out, ui
 /* out[i*ld_out + c] = src[idx[i]*ld_src + c] for i < rows, c < cols (row gather). */
 int gdx_gather_rows(const float* src, uint64_t ld_src, const uint32_t* idx, uint32_t rows,
                     uint32_t cols, float* out, uint64_t ld_out, gdx_stream stream);
+/* Cooperative-batch feature LOAD (the LOAD step of the paper's Alg. 1 over a
+ * resident split-bf16 feature store): out_{hi,lo}[i] = src_{hi,lo}[idx[i]] for
+ * i < rows, whole 8-element vectors up to cols.  Pitches in elements, multiples of 8. */
+int gdx_gather_split_rows(const uint16_t* src_hi, const uint16_t* src_lo, uint64_t ld_src,
+                          const uint32_t* idx, uint32_t rows, uint32_t cols, uint16_t* out_hi,
+                          uint16_t* out_lo, uint64_t ld_out, gdx_stream stream);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,7 @@ _SIGS = {
     "gdx_order_by_hop": (C.c_int, [vp, u32, u32, vp, vp, vp, C.POINTER(u32), vp]),
     "gdx_local_csr": (C.c_int, [vp, vp, vp, u32, vp, vp, vp, vp, vp]),
     "gdx_gather_rows": (C.c_int, [vp, u64, vp, u32, u32, vp, u64, vp]),
+    "gdx_gather_split_rows": (C.c_int, [vp, vp, u64, vp, u32, u32, vp, vp, u64, vp]),
     "gdx_exclusive_scan_u64": (C.c_int, [vp, u64, vp, vp, vp]),
 }
 

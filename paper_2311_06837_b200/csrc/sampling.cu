@@ -268,6 +268,30 @@ __global__ void local_csr_kernel(const uint64_t* row_ptr, const uint32_t* col, c
     }
 }
 
+// Cooperative-batch feature LOAD: rows idx[i] of a split-bf16 store (hi and lo
+// planes, pitch ld_src) into the batch operand (pitch ld_out).  A warp per row,
+// 16-byte vectors (8 elements) per lane; both planes in one pass.
+__global__ void gather_split_rows_kernel(const uint16_t* __restrict__ src_hi,
+                                         const uint16_t* __restrict__ src_lo, uint64_t ld_src,
+                                         const uint32_t* __restrict__ idx, uint32_t rows,
+                                         uint32_t vecs, uint16_t* __restrict__ out_hi,
+                                         uint16_t* __restrict__ out_lo, uint64_t ld_out) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+        const uint64_t so = static_cast<uint64_t>(idx[r]) * ld_src, oo = static_cast<uint64_t>(r) * ld_out;
+        const uint4* sh = reinterpret_cast<const uint4*>(src_hi + so);
+        const uint4* sl = reinterpret_cast<const uint4*>(src_lo + so);
+        uint4* dh = reinterpret_cast<uint4*>(out_hi + oo);
+        uint4* dl = reinterpret_cast<uint4*>(out_lo + oo);
+        for (uint32_t v = lane; v < vecs; v += 32) {
+            const uint4 a = __ldg(sh + v), b = __ldg(sl + v);
+            dh[v] = a;
+            dl[v] = b;
+        }
+    }
+}
+
 __global__ void gather_rows_kernel(const float* src, uint64_t ld_src, const uint32_t* idx,
                                    uint32_t rows, uint32_t cols, float* out, uint64_t ld_out) {
     const uint64_t total = static_cast<uint64_t>(rows) * cols;
@@ -505,6 +529,25 @@ extern "C" int gdx_local_csr(const uint64_t* row_ptr, const uint32_t* col,
         row_ptr, col, local_to_global, local_n, local_of, counts, lptr, lcol);
     note_launch();
     return check_launch("gdx_local_csr");
+}
+
+extern "C" int gdx_gather_split_rows(const uint16_t* src_hi, const uint16_t* src_lo, uint64_t ld_src,
+                                     const uint32_t* idx, uint32_t rows, uint32_t cols,
+                                     uint16_t* out_hi, uint16_t* out_lo, uint64_t ld_out,
+                                     gdx_stream stream) {
+    GDX_REQUIRE(src_hi && src_lo && idx && out_hi && out_lo, GDX_INPUT,
+                "gdx_gather_split_rows: null pointer");
+    GDX_REQUIRE(ld_src % 8 == 0 && ld_out % 8 == 0 && ld_src >= cols && ld_out >= cols, GDX_INPUT,
+                "gdx_gather_split_rows: pitches must be multiples of 8 elements and >= cols");
+    GDX_REQUIRE(((reinterpret_cast<uintptr_t>(src_hi) | reinterpret_cast<uintptr_t>(src_lo) |
+                  reinterpret_cast<uintptr_t>(out_hi) | reinterpret_cast<uintptr_t>(out_lo)) & 15) == 0,
+                GDX_INPUT, "gdx_gather_split_rows: planes must be 16-byte aligned");
+    if (!rows || !cols) return GDX_OK;
+    const uint32_t vecs = (cols + 7) / 8;  // whole 16-byte vectors (pitch padding included)
+    gather_split_rows_kernel<<<grid_for(static_cast<uint64_t>(rows) * 32), 256, 0, as_cuda(stream)>>>(
+        src_hi, src_lo, ld_src, idx, rows, vecs, out_hi, out_lo, ld_out);
+    note_launch();
+    return check_launch("gdx_gather_split_rows");
 }
 
 extern "C" int gdx_gather_rows(const float* src, uint64_t ld_src, const uint32_t* idx, uint32_t rows,

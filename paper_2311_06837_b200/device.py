@@ -70,6 +70,12 @@ class Split:
         self.hi = torch.zeros(max(rows, 1) * self.ld, dtype=torch.int16, device=device)
         self.lo = torch.zeros(max(rows, 1) * self.ld, dtype=torch.int16, device=device)
 
+    def rows_view(self, rows: int) -> "Split":
+        """The first `rows` rows (same storage)."""
+        v = Split.__new__(Split)
+        v.rows, v.cols, v.ld, v.hi, v.lo = rows, self.cols, self.ld, self.hi, self.lo
+        return v
+
     def to_float(self) -> torch.Tensor:
         """fp32 value (for tests): hi + lo."""
         def f(t):

@@ -94,6 +94,15 @@ def agg_width(fout: int, rows: int) -> int:
     return 32 if fout <= 32 else (w8 + 31) // 32 * 32
 
 
+def _splitk_eff(split_k: int, k: int) -> int:
+    """Split-K count for a K of k rows with no empty split (<= split_k)."""
+    kb = -(-k // 64)
+    if kb <= 1:
+        return 1
+    per = -(-kb // min(split_k, kb))
+    return -(-kb // per)
+
+
 class _Layer:
     """Device state of one layer: W_cat (fp32 master + split copies), buffers."""
 
@@ -257,10 +266,16 @@ class FullGraphTrainer:
             self.nnz_local_src = int((self.seg_hi - self.seg_lo)[:self.nloc].sum().item())
         self.Xsp = Split(self.nloc, F, d)
         self._refresh_input_splits()
-        # row exchange: fused NVLink peer stores (default) or NCCL all-gather
-        self.p2p = P2PExchange(rank, world, pg, d, "epilogue" if xmode == "p2p-epilogue" else "ce") \
-            if use_p2p else None
-        # layers
+        self._init_model(xmode, use_p2p, weights, weight_seed)
+        torch.cuda.synchronize(d)
+
+    def _init_model(self, xmode, use_p2p, weights, weight_seed):
+        """Exchange, per-layer buffers (self.nloc local rows, self.nrows_gather gathered
+        rows), the flat gradient buffer and the weights."""
+        cfg, d = self.cfg, self.d
+        # row exchange: NVLink peer-memory push (default) or NCCL all-gather
+        self.p2p = P2PExchange(self.rank, self.world, self.pg, d,
+                               "epilogue" if xmode == "p2p-epilogue" else "ce") if use_p2p else None
         sm = torch.cuda.get_device_properties(d).multi_processor_count
         self.layers = []
         for l in range(cfg.layers):
@@ -281,7 +296,6 @@ class FullGraphTrainer:
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=d)
         self.keep_activations = False
         self.activations = []
-        torch.cuda.synchronize(d)
 
     # ---- state ----
     def _refresh_input_splits(self):
@@ -337,27 +351,27 @@ class FullGraphTrainer:
         locally owned source block is aggregated while NCCL moves the remote blocks,
         then the remote sources finish the rows with the fused epilogue.  rows:
         aggregate only the first `rows` rows (hop masking in subgraph mode)."""
+        csr = self.csr if rows is None or rows == self.csr.rows else self.csr.slice_rows(0, rows)
         if self.p2p is not None and not self.p2p_split:
             self.p2p.wait()
-            return self._agg(self.csr, full, width, **epi)
+            return self._agg(csr, full, width, **epi)
         if self.p2p is not None:
             # the producer already pushed our rows into every peer and signalled;
             # aggregate the owned sources, wait for the peers' rows, finish the rest
             P = self.partial[:, :pad4(width)] if self.partial.shape[1] != pad4(width) else self.partial
-            self._agg(self.csr, full, width, out=P, row_begin=self.seg_lo, row_end=self.seg_hi)
+            self._agg(csr, full, width, out=P, row_begin=self.seg_lo, row_end=self.seg_hi)
             self.p2p.wait()
-            return self._agg(self.csr, full, width, skip=(self.seg_lo, self.seg_hi), partial=P, **epi)
+            return self._agg(csr, full, width, skip=(self.seg_lo, self.seg_hi), partial=P, **epi)
         if not self.overlap:
             self.exchange.allgather_rows(full)
-            csr = self.csr if rows is None or rows == self.csr.rows else self.csr.slice_rows(0, rows)
             return self._agg(csr, full, width, **epi)
         work = self.exchange.allgather_rows_async(full)
         if work is None:  # gathered synchronously (unequal blocks)
-            return self._agg(self.csr, full, width, **epi)
+            return self._agg(csr, full, width, **epi)
         P = self.partial[:, :pad4(width)] if self.partial.shape[1] != pad4(width) else self.partial
-        self._agg(self.csr, full, width, out=P, row_begin=self.seg_lo, row_end=self.seg_hi)
+        self._agg(csr, full, width, out=P, row_begin=self.seg_lo, row_end=self.seg_hi)
         work.wait()
-        return self._agg(self.csr, full, width, skip=(self.seg_lo, self.seg_hi), partial=P, **epi)
+        return self._agg(csr, full, width, skip=(self.seg_lo, self.seg_hi), partial=P, **epi)
 
     # ---- collectives ----
     def _allgather_rows(self, full: torch.Tensor):
@@ -454,14 +468,17 @@ class FullGraphTrainer:
                         peers=self._peers(self.layers[l - 1].d_peers, 0))
                 self._publish(own, self.layers[l - 1].d_peers)
             # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
+            # (K = the rows that fed layer l; rows past them carry no gradient)
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
-            gemm_tn(L.G, A_in, c0=L.ws, split_k=L.split_k, a_mn=True, b_mn=True)
+            sk = _splitk_eff(L.split_k, r_in)
+            gemm_tn(L.G.rows_view(r_in), A_in.rows_view(r_in), c0=L.ws, split_k=sk, a_mn=True,
+                    b_mn=True)
             if self.world == 1:  # reduce split-K partials and apply SGD in one pass
-                call("gdx_splitk_reduce", L.ws.data_ptr(), L.split_k, L.nz * L.fin_ld, L.nz, L.fin,
+                call("gdx_splitk_reduce", L.ws.data_ptr(), sk, L.nz * L.fin_ld, L.nz, L.fin,
                      L.fin_ld, L.dW.data_ptr(), L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(),
                      L.Wsp.lo.data_ptr(), stream_handle())
             else:                # reduce partials; SGD after the epoch's single all-reduce
-                call("gdx_splitk_reduce", L.ws.data_ptr(), L.split_k, L.nz * L.fin_ld, L.nz, L.fin,
+                call("gdx_splitk_reduce", L.ws.data_ptr(), sk, L.nz * L.fin_ld, L.nz, L.fin,
                      L.fin_ld, L.dW.data_ptr(), None, 0.0, None, None, stream_handle())
         if self.world > 1:
             # one all-reduce for every layer's dW and the loss, then SGD (+ split refresh)

@@ -57,6 +57,47 @@ def main():
             case["ok"] = same and case["max_abs_loss_diff"] <= 1e-3
             out["ok"] &= case["ok"]
         out["cases"].append(case)
+    # cooperative batching (config 5 semantics): one server, `world` GPUs share each batch
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+    from test_cobatch import _oracle_batch, _plan
+    from paper_2311_06837_b200.cobatch import CobatchTrainer
+    dims = [48, 32, 32, 8]
+    g, hp, plan = _plan(4000, 10.0, 21, 1, world, 3, 3, G.SamplingConfig(1, 15, 3), dims)
+    cfg = ModelConfig("sage", dims, lr=0.5)
+    w0 = init_weights(cfg, 3)
+    tr = CobatchTrainer(g, cfg, plan, hp.server, hp.gpu, 0, rank=rank, world=world, weights=w0,
+                        pg=dist.group.WORLD)
+    got = []
+    for _ in range(2):
+        for i in range(len(plan.batches)):
+            tr.train_batch(i)
+            got.append(float(tr.loss_acc.item()) / len(plan.batches[i].target_vertices))
+    W = torch.from_numpy(np.concatenate([a.ravel() for a in tr.get_weights()])).to(dev)
+    Wmax, Wmin = W.clone(), W.clone()
+    dist.all_reduce(Wmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(Wmin, op=dist.ReduceOp.MIN)
+    same = bool(torch.equal(Wmax, Wmin))
+    case = {"kind": "sage-cobatch", "batches": len(plan.batches), "losses": got,
+            "weights_identical_across_ranks": same,
+            "rows_per_rank": [geo.nloc for geo in tr.geoms]}
+    if rank == 0:
+        import oracle as O
+        n = g.num_vertices()
+        x_all = O.make_features(n, dims[0], 1).astype(np.float32).astype(np.float64)
+        lab_all = O.make_labels(n, dims[-1], 2)
+        m = O.Model(O.SAGE, dims)
+        w = np.concatenate([a.astype(np.float32).astype(np.float64).ravel() for a in w0])
+        ref = []
+        for _ in range(2):
+            for b in plan.batches:
+                lc, x, lab, layer_rows, nt, _ = _oracle_batch(g, b, 3, x_all, lab_all)
+                ref.append(O.train_epoch_masked(lc, x, lab, m, w, 0.5, nt, float(nt), nthreads=8,
+                                                layer_rows=layer_rows)[0])
+        case["oracle"] = ref
+        case["max_abs_loss_diff"] = float(np.max(np.abs(np.array(got) - np.array(ref))))
+        case["ok"] = same and case["max_abs_loss_diff"] <= 1e-3
+        out["ok"] &= case["ok"]
+    out["cases"].append(case)
     if rank == 0:
         print(json.dumps(out), flush=True)
     dist.barrier()
