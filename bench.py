@@ -49,6 +49,12 @@ CONFIGS = {
                          workload="ogbn-products-shape full-graph 3-layer normalised GCN, features "
                                   "resident on every GPU (shared preload with one server) "
                                   "(BASELINE configs[3])"),
+    "papers-cobatch": dict(n=111059956, degree=14.55, seed=17, kind="sage", dims=[128, 64, 64, 172],
+                           mode="cobatch", eas=(1, 15, 3), batches=256, lr=0.1,
+                           workload="ogbn-papers100M-shape cooperative-batching mini-batch 3-layer "
+                                    "GraphSAGE-mean: one server, its GPUs share every batch "
+                                    "(split_batch), sampled closure EAS(m=1,k=15,seed=3), R batches "
+                                    "= R SGD steps per epoch (BASELINE configs[4])"),
 }
 
 
@@ -65,6 +71,7 @@ def parse():
     ap.add_argument("--config", default="reddit-sage", choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=0, help="override the vertex count (0: config's)")
     ap.add_argument("--degree", type=float, default=0.0)
+    ap.add_argument("--batches", type=int, default=0, help="cobatch R (0: config's)")
     return ap.parse_args()
 
 
@@ -229,6 +236,160 @@ def run_reference(args, world, rank):
     }), flush=True)
 
 
+def cobatch_cpu_baseline(tr, plan) -> dict:
+    """The oracle port's fp64 masked epoch on batch 0's local graph (the same rows,
+    levels and loss rows as the GPU step), timed once and scaled by the batch count."""
+    import torch
+    import oracle as O
+
+    geo = tr.geoms[0]
+    threads = os.cpu_count() or 1
+    lp = geo.csr.row_ptr.cpu().numpy().astype(np.uint64)
+    lc = geo.csr.col[:max(geo.nnz, 1)].cpu().numpy().view(np.uint32)[:geo.nnz]
+    csr = O.CSR(geo.nloc, lp, lc)
+    idx = geo.l2g.long()
+    ld = tr.Xall.ld
+
+    def plane(t):
+        return (t.view(-1, ld)[idx, :tr.F].to(torch.int32).bitwise_left_shift(16).view(torch.float32))
+    x = (plane(tr.Xall.hi) + plane(tr.Xall.lo)).double().cpu().numpy()
+    lab = tr.labels_all[idx].cpu().numpy()
+    model = O.Model({"sage": O.SAGE, "gcn": O.GCN, "sum": O.SUM}[tr.cfg.kind], tr.cfg.dims)
+    w = np.random.default_rng(0).uniform(-0.5, 0.5, model.weight_count())
+    t = time.perf_counter()
+    O.train_epoch_masked(csr, x, lab, model, w, 0.1, geo.loss_rows, float(geo.loss_count),
+                         nthreads=threads, layer_rows=list(geo.rows_out))
+    sec = time.perf_counter() - t
+    R = len(plan.batches)
+    return {"value": round(sec * 1e3 * R, 1), "unit": "ms", "cores": threads, "kind": "port",
+            "sample": (f"oracle port (fp64, OpenMP {threads} threads): the SGD step of batch 0 "
+                       f"({geo.nloc} rows, {geo.nnz} local edges) in {sec:.2f} s, x{R} batches "
+                       f"to an epoch")}
+
+
+def run_cobatch(args, C, world, rank, local, dev, pg):
+    """configs[4]: cooperative-batching epochs (R batches, one SGD step each)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200 import _lib
+    from paper_2311_06837_b200.cobatch import CobatchTrainer
+    from paper_2311_06837_b200.graph import Partition
+    from paper_2311_06837_b200.train import ModelConfig
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    R = args.batches or C["batches"]
+    dims = list(C["dims"])
+    L = len(dims) - 1
+    t0 = time.perf_counter()
+    g = G.gen_random_graph(args.n, args.degree, C["seed"])
+    n = g.num_vertices()
+    t_gen = time.perf_counter() - t0
+    # one server holding every vertex; its GPUs by partition_random with the
+    # hierarchical_partition(g, 1, world, "random", 4) seed (partition.cpp:226-259)
+    sp = Partition(np.zeros(n, np.uint32), 1)
+    ga = np.zeros(n, np.uint32)
+    _lib.call("gdx_host_partition_random", n, world, G.mix64(4 ^ 1), ga.ctypes.data)
+    gp = Partition(ga, world)
+    m, k, sseed = C["eas"]
+    scfg = G.SamplingConfig(m, k, sseed)
+    t0 = time.perf_counter()
+    sub = G.extract_sampled(g, sp, 0, scfg)
+    plan = G.plan_cobatch_fixed_r(sub, g, L, scfg, R, G.ModelSpec(L, dims[1], dims[0]),
+                                  target_split="random")
+    t_plan = time.perf_counter() - t0
+    cfg = ModelConfig(C["kind"], dims, lr=C["lr"])
+    t0 = time.perf_counter()
+    tr = CobatchTrainer(g, cfg, plan, sp, gp, 0, rank=rank, world=world, pg=pg)
+    t_geo = time.perf_counter() - t0
+    del sub
+    for _ in range(max(args.warmup, 3)):
+        tr.train_epoch(sync_loss=False)
+    barrier()
+    tr.enable_kernel_events(True)
+    tr.train_epoch(sync_loss=False)
+    barrier()
+    agg_ms_epoch, agg_launches, agg_bytes = tr.kernel_event_summary()
+    tr.enable_kernel_events(False)
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            tr.train_epoch(sync_loss=False)
+        e1.record()
+        barrier()
+    launches = _lib.launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    loss = tr.train_epoch(sync_loss=True)
+    t_ms = torch.tensor([ms, agg_ms_epoch], dtype=torch.float64, device=dev)
+    ed = torch.tensor([float(sum(geo.edges_per_step for geo in tr.geoms))], dtype=torch.float64,
+                      device=dev)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ed)
+    ms, agg_ms = float(t_ms[0]), float(t_ms[1])
+    edges_epoch = float(ed[0])
+    peak, peak_kind = load_peaks()
+    agg_avg_ms = agg_ms_epoch / agg_launches if agg_launches else None
+    achieved = (agg_bytes / agg_launches) / (agg_avg_ms * 1e-3) / 1e9 if agg_launches else None
+    rows = [geo.nloc for geo in tr.geoms]
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cobatch_cpu_baseline(tr, plan)
+        out = {
+            "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (tcgen05 GEMMs: bf16x3 split, fp32 accumulate)",
+            "data": f"synthetic: gen_random_graph({n}, {args.degree}, {C['seed']}) papers-shape "
+                    f"G(n,p), features/labels from the reference keyed RNG streams",
+            "config": {"workload": C["workload"], "name": args.config,
+                       "model": f"{cfg.kind} {'-'.join(map(str, dims))} ({L} layers), no bias, "
+                                f"SGD lr {cfg.lr}, one step per batch",
+                       "vertices": n, "directed_edges": g.num_edges(), "batches": R,
+                       "target_split": "split_targets_random (host min-cut of 111 M vertices "
+                                       "replaced; structure-free graph)",
+                       "batch_rows_per_rank": {"max": max(rows), "mean": int(np.mean(rows))},
+                       "global_batch": int(n / R),
+                       "parallelism": f"cooperative batch split x{world} (split_batch), "
+                                      f"per-layer NVLink row push inside the batch",
+                       "l2": "no flush: every batch streams its CSR and > 1 GB of rows"},
+            "epoch_ms": round(ms, 3),
+            "aggregation_edges_per_s": round(edges_epoch / (agg_ms * 1e-3), 1) if agg_ms else None,
+            "epoch_edges_per_s": round(edges_epoch / (ms * 1e-3), 1),
+            "loss_after": round(loss, 6),
+            "roofline": {
+                "bound": "hbm", "kernel": "gdx aggregate_vec4 (K1/K3 gather-reduce)",
+                "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "algorithmic_bytes_per_launch": int(agg_bytes / agg_launches) if agg_launches else None,
+                "avg_launch_ms": round(agg_avg_ms, 4) if agg_avg_ms else None,
+                "share_of_step": round(agg_ms / ms, 3) if ms else None},
+            "gpu_launches": int(launches / max(args.steps, 1)),
+            "cuda_graph": False,
+            "clocks": clk.summary(),
+            "e2e": None,
+            "e2e_note": "not measured for this config: host-side features would be 57 GB",
+            "cpu_baseline": cpu,
+            "setup_s": {"graph_generation": round(t_gen, 2), "plan": round(t_plan, 2),
+                        "batch_geometry": round(t_geo, 2)},
+        }
+        print(json.dumps(out), flush=True)
+    barrier()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     C = CONFIGS[args.config]
@@ -250,6 +411,10 @@ def main():
         opts.is_high_priority_stream = True  # collectives get SMs ahead of the aggregation
         dist.init_process_group("nccl", device_id=dev, pg_options=opts)
         pg = dist.group.WORLD
+
+    if C["mode"] == "cobatch":
+        run_cobatch(args, C, world, rank, local, dev, pg)
+        return
 
     import paper_2311_06837_b200 as G
     from paper_2311_06837_b200 import _lib

@@ -106,7 +106,12 @@ int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream);
 /* seg_lo[v], seg_hi[v] = sub-range of row v's (sorted) column ids inside [lo, hi). */
 int gdx_row_split(const uint64_t* row_ptr, const uint32_t* col, uint32_t rows, uint32_t lo,
                   uint32_t hi, uint64_t* seg_lo, uint64_t* seg_hi, gdx_stream stream);
-/* Tuning hook (benchmarks only): forces a kernel variant (unroll depth 4 or 8). */
+/* Kernel selection.  variant GDX_AGG_ROWS: one lane group per destination row
+ * (EPW rows per warp at once) -- for low-degree CSRs such as cooperative-batch
+ * subgraphs (a few in-batch edges per row), where the warp-per-row kernel is
+ * bound by the per-row row_ptr -> col -> row latency chain.  4 / 8: unroll depth
+ * of the warp-per-row kernel (tuning).  0 = gdx_aggregate. */
+#define GDX_AGG_ROWS 1
 int gdx_aggregate_variant(const gdx_aggregate_args* a, int variant, gdx_stream stream);
 
 /* ------------------------------------------------------------------------

@@ -76,8 +76,8 @@ def batch_closure(g: Graph, universe: np.ndarray, targets: np.ndarray, cfg: Samp
     tmask = _mask(g.num_vertices(), targets, dev)
     allowed = torch.from_numpy(np.ascontiguousarray(universe, np.uint8)).to(dev)
     mark = sampled_growth_device(g, tmask, allowed, cfg.max_hop, cfg.fanout, cfg.seed)
-    hop = mark.cpu().numpy().view(np.uint32)
-    return np.nonzero(hop != 0xFFFFFFFF)[0].astype(np.uint32)
+    # ascending ids of the claimed vertices (compacted on the device)
+    return torch.nonzero(mark != -1).flatten().to(torch.int32).cpu().numpy().view(np.uint32)
 
 
 def peel_mfg(g: Graph, batch_vertices: np.ndarray, targets: np.ndarray, layers: int) -> list:
@@ -114,24 +114,45 @@ def split_targets_mincut(g: Graph, targets: np.ndarray, r: int, seed: int) -> li
     return [np.sort(gids[p.assignment == k]).astype(np.uint32) for k in range(r)]
 
 
+def split_targets_random(targets: np.ndarray, r: int, seed: int) -> list:
+    """Scale variant of split_targets_mincut: partition_random (partition.cpp:51-61)
+    of the targets' induced subgraph -- the assignment depends only on the target
+    count, so the subgraph is never built.  For graphs whose host min-cut is too slow
+    (papers shape: 111 M vertices) and structure-free graphs, where min-cut finds no
+    locality anyway."""
+    t = np.asarray(targets, np.uint32)
+    if r <= 1 or len(t) <= 1:
+        return [t]
+    a = np.zeros(len(t), np.uint32)
+    call("gdx_host_partition_random", len(t), r, int(seed), a.ctypes.data)
+    return [t[a == k] for k in range(r)]
+
+
 def _build_cobatch(sub: DependencySubgraph, g: Graph, layers: int, cfg: SamplingConfig, r: int,
-                   model: ModelSpec) -> BatchPlan:
+                   model: ModelSpec, target_split: str = "mincut") -> BatchPlan:
     universe = np.zeros(g.num_vertices(), np.uint8)
     universe[sub.inner_vertices] = 1
     universe[sub.halo_vertices] = 1
     plan = BatchPlan(sub.server_id, "fetch_then_split", layers)
-    for group in split_targets_mincut(g, sub.inner_vertices, r, cfg.seed):
+    if target_split == "random":
+        groups = split_targets_random(sub.inner_vertices, r, cfg.seed)
+    elif target_split == "mincut":
+        groups = split_targets_mincut(g, sub.inner_vertices, r, cfg.seed)
+    else:
+        raise InputError(f"plan_cobatch: unknown target split {target_split!r}")
+    for group in groups:
         plan.batches.append(make_batch(g, universe, group, layers, cfg, model))
     return plan
 
 
 def plan_cobatch_fixed_r(sub: DependencySubgraph, g: Graph, layers: int, cfg: SamplingConfig,
-                         r: int, model: ModelSpec) -> BatchPlan:
-    """batch_plan.cpp:146-153."""
+                         r: int, model: ModelSpec, target_split: str = "mincut") -> BatchPlan:
+    """batch_plan.cpp:146-153.  target_split="random" swaps the host min-cut target
+    split for split_targets_random (papers-scale plans)."""
     if r == 0:
         raise InputError("plan_cobatch: batch count must be >= 1")
     capped = min(r, max(1, len(sub.inner_vertices)))
-    return _build_cobatch(sub, g, layers, cfg, capped, model)
+    return _build_cobatch(sub, g, layers, cfg, capped, model, target_split)
 
 
 def plan_cobatch(sub: DependencySubgraph, g: Graph, layers: int, cfg: SamplingConfig,

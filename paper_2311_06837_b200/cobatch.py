@@ -62,6 +62,7 @@ class BatchGeometry:
     seg_lo: torch.Tensor | None
     seg_hi: torch.Tensor | None
     mfg: list               # |{d <= L-l}| over the whole batch, l = 0..L (== peel_mfg)
+    edges_per_step: int     # CSR entries aggregated by this rank per step (fwd + bwd passes)
 
 
 def split_batch_share(vb: torch.Tensor, sp: torch.Tensor, gp: torch.Tensor, server: int,
@@ -74,6 +75,13 @@ def split_batch_share(vb: torch.Tensor, sp: torch.Tensor, gp: torch.Tensor, serv
         call("gdx_split_batch", vb.data_ptr(), nb, sp.data_ptr(), gp.data_ptr(), server, gpus,
              share.data_ptr(), work.data_ptr(), stream_handle())
     return share[:nb]
+
+
+def _dev_assign(p, device) -> torch.Tensor:
+    """Device int32 copy of a Partition's assignment (tensors pass through)."""
+    if isinstance(p, torch.Tensor):
+        return p
+    return torch.from_numpy(np.ascontiguousarray(p.assignment, np.uint32).view(np.int32)).to(device)
 
 
 def batch_geometry(g: Graph, targets: np.ndarray, vertices: np.ndarray, sp: Partition,
@@ -91,9 +99,7 @@ def batch_geometry(g: Graph, targets: np.ndarray, vertices: np.ndarray, sp: Part
     # peel levels = BFS distance from the targets inside the batch (unlimited fanout growth)
     mark = sampled_growth_device(g, tmask, in_batch, layers, kUnlimitedFanout, 0)
     d_b = mark[vb.long()]
-    owner = split_batch_share(vb, torch.from_numpy(sp.assignment.view(np.int32)).to(device),
-                              torch.from_numpy(gp.assignment.view(np.int32)).to(device),
-                              server, world)
+    owner = split_batch_share(vb, _dev_assign(sp, device), _dev_assign(gp, device), server, world)
     keep = d_b >= 0
     v_k, d_k, o_k = vb[keep].long(), d_b[keep].long(), owner[keep].long()
     mfg = [int((d_k <= layers - l).sum().item()) for l in range(layers + 1)]
@@ -145,8 +151,10 @@ def batch_geometry(g: Graph, targets: np.ndarray, vertices: np.ndarray, sp: Part
              rank * block + nloc, seg_lo.data_ptr(), seg_hi.data_ptr(), stream_handle())
         nnz_src = int((seg_hi - seg_lo)[:nloc].sum().item()) if nloc else 0
     del local_of, in_batch, tmask, mark
+    lp = lptr.cpu().numpy()
+    edges = int(sum(lp[r] for r in rows_out) + sum(lp[r] for r in rows_in))
     return BatchGeometry(csr, l2g, nloc, block, rows_in, rows_out, rows_out[-1] if layers else nloc,
-                         len(targets), nnz, nnz_src, inv_deg, gcn_s, seg_lo, seg_hi, mfg)
+                         len(targets), nnz, nnz_src, inv_deg, gcn_s, seg_lo, seg_hi, mfg, edges)
 
 
 class CobatchTrainer(FullGraphTrainer):
@@ -195,10 +203,11 @@ class CobatchTrainer(FullGraphTrainer):
         self.p2p_split = use_p2p and os.environ.get("GDX_P2P_SPLIT", "1") != "0"
         self.overlap = world > 1 and (
             self.p2p_split or (not use_p2p and os.environ.get("GDX_OVERLAP", "1") != "0"))
-        self.geoms = [batch_geometry(g, b.target_vertices, b.vertices, server_partition,
-                                     gpu_partition, server, rank, world, cfg.layers, d,
-                                     self.overlap)
+        spd, gpd = _dev_assign(server_partition, d), _dev_assign(gpu_partition, d)
+        self.geoms = [batch_geometry(g, b.target_vertices, b.vertices, spd, gpd, server, rank,
+                                     world, cfg.layers, d, self.overlap)
                       for b in plan.batches]
+        del spd, gpd
         # buffers sized for the largest batch
         self.nloc = max([geo.nloc for geo in self.geoms] + [1])
         self.cap_rows = self.nloc
@@ -236,14 +245,16 @@ class CobatchTrainer(FullGraphTrainer):
         if geo.nloc:
             torch.index_select(self.labels_all, 0, geo.l2g.long(), out=self.labels[:geo.nloc])
         # rows this batch does not produce must hold no gradient (buffers are reused
-        # across batches): own gradient rows past each layer's produced prefix, and the
-        # weight-gradient operand G
+        # across batches): own gradient rows past each layer's produced prefix and, for
+        # SAGE, the dP half of G on rows read but not produced (the dW GEMM's K covers
+        # rows_in; the aggregation rewrites the other half there every step)
         for l, L in enumerate(self.layers):
-            if geo.rows_out[l] < geo.nloc:
-                L.dfull[self.lo + geo.rows_out[l]:self.hi].zero_()
-            r = geo.rows_in[l]
-            L.G.hi[:r * L.G.ld].zero_()
-            L.G.lo[:r * L.G.ld].zero_()
+            r_out, r_in = geo.rows_out[l], geo.rows_in[l]
+            if r_out < geo.nloc:
+                L.dfull[self.lo + r_out:self.hi].zero_()
+            if self.cfg.kind == "sage" and r_out < r_in:
+                L.G.hi.view(-1, L.G.ld)[r_out:r_in, :L.w].zero_()
+                L.G.lo.view(-1, L.G.ld)[r_out:r_in, :L.w].zero_()
 
     def train_batch(self, i: int):
         self.bind(i)

@@ -226,6 +226,118 @@ __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
     }
 }
 
+// Low-degree rows (in-batch subgraphs: a few edges per row): the warp-per-row
+// kernel spends most of its time on the per-row dependency chain row_ptr ->
+// col -> row.  Here every LPE-lane group owns its own destination row, so a warp
+// walks EPW rows at once, and each group keeps UNROLL neighbour gathers in
+// flight; no shuffles, so groups diverge freely.
+template <int LPE, int NCH, bool EXACT, int UNROLL>
+__global__ void __launch_bounds__(256) aggregate_rows(const AggParams p) {
+    constexpr int EPW = pow2_floor(32 / LPE);
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / LPE;
+    const int lin = lane - sub * LPE;
+    if (sub >= EPW) return;
+    uint64_t pol_keep, pol_stream;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const uint64_t base = reinterpret_cast<uint64_t>(p.src) + 16 * lin;
+    const uint32_t ldb = p.ld_bytes;
+    bool chan_on[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) chan_on[c] = EXACT || (lin + c * LPE) < p.c4;
+    const uint64_t groups = static_cast<uint64_t>((gridDim.x * blockDim.x) >> 5) * EPW;
+    for (uint64_t r = static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * EPW + sub;
+         r < p.rows; r += groups) {
+        const uint32_t row = static_cast<uint32_t>(r);
+        const uint64_t beg = p.row_ptr[row];
+        const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
+        float4 acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int nseg = p.skip_lo ? 2 : 1;
+        for (int seg = 0; seg < nseg; ++seg) {
+            uint64_t e = beg, send = end;
+            if (p.skip_lo) {
+                if (seg == 0) send = p.skip_lo[row];
+                else e = p.skip_hi[row];
+            }
+            for (; e + UNROLL <= send; e += UNROLL) {
+                uint32_t nb[UNROLL];
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) nb[u] = ld_stream_u32(p.col + e + u, pol_stream);
+                float4 v[UNROLL][NCH];
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    const char* rp = row_addr(base, nb[u], ldb);
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+                        v[u][c] = chan_on[c] ? ld_row4(rp + 16 * LPE * c, pol_keep)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) add4(acc[c], v[u][c]);
+            }
+            for (; e < send; ++e) {
+                const char* rp = row_addr(base, ld_stream_u32(p.col + e, pol_stream), ldb);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c)
+                    if (chan_on[c]) add4(acc[c], ld_row4(rp + 16 * LPE * c, pol_keep));
+            }
+        }
+        const float scale = p.post_scale ? p.post_scale[row] : 1.f;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const uint32_t ch = lin + c * LPE;
+            if (!chan_on[c]) continue;
+            float4 rr = acc[c];
+            if (p.partial) {
+                const float4 q = ld_plain4(p.partial + row * p.ld_partial + 4 * ch);
+                rr.x += q.x;
+                rr.y += q.y;
+                rr.z += q.z;
+                rr.w += q.w;
+            }
+            if (p.self_coef != 0.f) {
+                const float4 q = ld_plain4(p.src + (p.self_base + row) * p.ld_src + 4 * ch);
+                rr.x += p.self_coef * q.x;
+                rr.y += p.self_coef * q.y;
+                rr.z += p.self_coef * q.z;
+                rr.w += p.self_coef * q.w;
+            }
+            rr.x *= scale;
+            rr.y *= scale;
+            rr.z *= scale;
+            rr.w *= scale;
+            if (p.add) {
+                const float4 q = ld_plain4(p.add + row * p.ld_add + 4 * ch);
+                rr.x += q.x;
+                rr.y += q.y;
+                rr.z += q.z;
+                rr.w += q.w;
+            }
+            if (p.relu) {
+                rr.x = fmaxf(rr.x, 0.f);
+                rr.y = fmaxf(rr.y, 0.f);
+                rr.z = fmaxf(rr.z, 0.f);
+                rr.w = fmaxf(rr.w, 0.f);
+            }
+            if (p.out) *reinterpret_cast<float4*>(p.out + row * p.ld_out + 4 * ch) = rr;
+            if (p.out_hi) {
+                ushort4 h, l;
+                split_bf16(rr.x, h.x, l.x);
+                split_bf16(rr.y, h.y, l.y);
+                split_bf16(rr.z, h.z, l.z);
+                split_bf16(rr.w, h.w, l.w);
+                *reinterpret_cast<ushort4*>(p.out_hi + row * p.ld_split + 4 * ch) = h;
+                *reinterpret_cast<ushort4*>(p.out_lo + row * p.ld_split + 4 * ch) = l;
+            }
+        }
+    }
+}
+
 // Any width / alignment: one warp per row, lanes stride over columns.
 __global__ void __launch_bounds__(256) aggregate_scalar(const AggParams p, uint32_t width) {
     const int lane = threadIdx.x & 31;
@@ -302,8 +414,42 @@ int pick_and_launch(const AggParams& p, cudaStream_t s) {
     return 0;
 }
 
-// Tuning hook: variant = unroll depth (4 or 8) for the exact 12/16-lane kernels.
+template <int LPE, int NCH, bool EXACT>
+void launch_rows(const AggParams& p, cudaStream_t s) {
+    constexpr int EPW = pow2_floor(32 / LPE);
+    uint64_t blocks = (static_cast<uint64_t>(p.rows) + 8 * EPW - 1) / (8 * EPW);
+    if (blocks > 65535ull * 64) blocks = 65535ull * 64;
+    aggregate_rows<LPE, NCH, EXACT, 4><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
+}
+
+int launch_rows_any(const AggParams& p, cudaStream_t s) {
+    switch (p.c4) {
+        case 1: launch_rows<1, 1, true>(p, s); return 0;
+        case 2: launch_rows<2, 1, true>(p, s); return 0;
+        case 4: launch_rows<4, 1, true>(p, s); return 0;
+        case 8: launch_rows<8, 1, true>(p, s); return 0;
+        case 12: launch_rows<12, 1, true>(p, s); return 0;
+        case 16: launch_rows<16, 1, true>(p, s); return 0;
+        case 32: launch_rows<32, 1, true>(p, s); return 0;
+        case 48: launch_rows<16, 3, true>(p, s); return 0;
+        case 64: launch_rows<32, 2, true>(p, s); return 0;
+        default: break;
+    }
+    const uint32_t c4 = p.c4;
+    if (c4 <= 4) launch_rows<4, 1, false>(p, s);
+    else if (c4 <= 8) launch_rows<8, 1, false>(p, s);
+    else if (c4 <= 16) launch_rows<16, 1, false>(p, s);
+    else if (c4 <= 32) launch_rows<32, 1, false>(p, s);
+    else if (c4 <= 64) launch_rows<32, 2, false>(p, s);
+    else if (c4 <= 128) launch_rows<32, 4, false>(p, s);
+    else launch_rows<32, 8, false>(p, s);
+    return 0;
+}
+
+// variant: 4 / 8 = unroll depth of the exact 12/16-lane warp-per-row kernels
+// (tuning); GDX_AGG_ROWS = the lane-group-per-row kernel for low-degree rows.
 int launch_variant(const AggParams& p, int variant, cudaStream_t s) {
+    if (variant == GDX_AGG_ROWS) return launch_rows_any(p, s);
     const bool u8 = variant == 8;
     if (p.c4 == 16) {
         if (u8) launch_vec<16, 1, true, 8>(p, s);

@@ -94,6 +94,18 @@ def agg_width(fout: int, rows: int) -> int:
     return 32 if fout <= 32 else (w8 + 31) // 32 * 32
 
 
+AGG_ROWS = 1  # gdx.h GDX_AGG_ROWS
+
+
+def agg_variant(width: int, nnz: int, rows: int) -> int:
+    """Aggregation kernel for a CSR: the lane-group-per-row kernel for low-degree rows
+    (measured B200, 6 M rows x 64: 1.8x at degree 2.6, 1.2x at 12, parity at 25) and
+    for 48-wide rows (12 lanes: 5% faster at degree 492); warp-per-row otherwise."""
+    if rows and nnz / rows < 20:
+        return AGG_ROWS
+    return AGG_ROWS if pad4(width) == 48 else 0
+
+
 def _splitk_eff(split_k: int, k: int) -> int:
     """Split-K count for a K of k rows with no empty split (<= split_k)."""
     kb = -(-k // 64)
@@ -324,6 +336,7 @@ class FullGraphTrainer:
         self._events = [] if on else None
 
     def _agg(self, csr, src, width, **kw):
+        kw.setdefault("variant", agg_variant(width, self.nnz_local, self.nloc))
         ev = getattr(self, "_events", None)
         if ev is None:
             return aggregate(csr, src, width, **kw)

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--n", type=int, default=232965)
     ap.add_argument("--degree", type=float, default=491.99)
+    ap.add_argument("--no-probe", action="store_true")
     args = ap.parse_args()
     import torch
     import paper_2311_06837_b200 as G
@@ -46,9 +47,12 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.reps
             alg = 4 * nnz + 8 * (n + 1) + 4 * w * nnz + 4 * w * n
-            res.append({"width": w, "unroll": variant, "ms": round(ms, 4),
+            res.append({"n": n, "deg": args.degree, "width": w, "variant": variant, "ms": round(ms, 4),
                         "gedges_per_s": round(nnz / ms / 1e6, 2),
                         "alg_GBps": round(alg / ms / 1e6, 1)})
+    if args.no_probe:
+        print(json.dumps(res))
+        return
     # bandwidth ceilings with the library's probe kernel: L2-resident (60 MB) and
     # HBM-resident (4 GB) buffers, coalesced stream and random 256 B row gathers
     from paper_2311_06837_b200._lib import call

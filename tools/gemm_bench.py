@@ -24,6 +24,11 @@ SHAPES = [
     ("products dH", 2449029, 64, 64, 0, 1, 1),
     ("products dW L2", 64, 64, 2449029, 1, 1, 296),
     ("reddit dH L2 fused(mask,scale,split)", 232965, 64, 128, 0, 1, -1),
+    ("papers cobatch L1 fwd", 6000000, 128, 128, 0, 0, 1),
+    ("papers cobatch L2 fwd", 6000000, 128, 64, 0, 0, 1),
+    ("papers cobatch L3 fwd", 6000000, 384, 64, 0, 0, 1),
+    ("papers cobatch dH L3", 6000000, 64, 384, 0, 1, 1),
+    ("papers cobatch dW L3", 384, 64, 6000000, 1, 1, 296),
 ]
 
 
@@ -33,7 +38,10 @@ def main():
 
     d = torch.device("cuda", 0)
     out = []
+    only = os.environ.get("GEMM_ONLY")
     for name, m, n, k, a_mn, b_mn, sk in SHAPES:
+        if only and only not in name:
+            continue
         A = D.Split(k, m, d) if a_mn else D.Split(m, k, d)
         B = D.Split(k, n, d) if b_mn else D.Split(n, k, d)
         for t in (A.hi, A.lo, B.hi, B.lo):

@@ -53,7 +53,13 @@ def main():
         return inner
 
     ACTIVE = [False]
-    T.gemm_tn = wrap("gemm", T.gemm_tn)
+    orig_gemm = T.gemm_tn
+
+    def gemm(A, B, **kw):
+        tag = "gemm_dW" if kw.get("split_k", 1) > 1 or kw.get("a_mn") else (
+            "gemm_dH" if kw.get("b_mn") else "gemm_fwd")
+        return wrap(tag, orig_gemm)(A, B, **kw)
+    T.gemm_tn = gemm
     orig_agg = T.FullGraphTrainer._agg
 
     def agg(self, csr, src, width, **kw):
@@ -71,8 +77,29 @@ def main():
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from bench import CONFIGS
     C = CONFIGS[cfgname]
-    g = G.gen_random_graph(C["n"], C["degree"], C["seed"])
-    tr = T.FullGraphTrainer(g, T.ModelConfig(C["kind"], C["dims"], lr=C["lr"]), rank=rank, world=world, pg=pg)
+    n = int(os.environ.get("GDX_N", C["n"]))
+    g = G.gen_random_graph(n, C["degree"], C["seed"])
+    cfg = T.ModelConfig(C["kind"], C["dims"], lr=C["lr"])
+    if C["mode"] == "cobatch":
+        # the first GDX_NB batches of an R-batch random-split plan (per-batch cost is what matters)
+        import numpy as np
+        from paper_2311_06837_b200 import batch_plan as BP
+        from paper_2311_06837_b200.cobatch import CobatchTrainer
+        from paper_2311_06837_b200.graph import Partition
+        R, NB = int(os.environ.get("GDX_R", C["batches"])), int(os.environ.get("GDX_NB", "4"))
+        L = len(C["dims"]) - 1
+        scfg = G.SamplingConfig(*C["eas"])
+        sp = Partition(np.zeros(n, np.uint32), 1)
+        ga = np.zeros(n, np.uint32)
+        G._lib.call("gdx_host_partition_random", n, world, G.mix64(4 ^ 1), ga.ctypes.data)
+        universe = np.ones(n, np.uint8)
+        plan = BP.BatchPlan(0, "fetch_then_split", L)
+        spec = BP.ModelSpec(L, C["dims"][1], C["dims"][0])
+        for grp in BP.split_targets_random(np.arange(n, dtype=np.uint32), R, scfg.seed)[:NB]:
+            plan.batches.append(BP.make_batch(g, universe, grp, L, scfg, spec))
+        tr = CobatchTrainer(g, cfg, plan, sp, Partition(ga, world), 0, rank=rank, world=world, pg=pg)
+    else:
+        tr = T.FullGraphTrainer(g, cfg, rank=rank, world=world, pg=pg)
     for _ in range(3):
         tr.train_epoch(sync_loss=False)
     torch.cuda.synchronize()
