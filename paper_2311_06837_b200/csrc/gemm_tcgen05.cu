@@ -108,19 +108,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t addr, uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -174,14 +161,14 @@ struct Epi {
     uint32_t npeers;        // fused exchange: peer copies of output `peer_target`
     int peer_target;
     int64_t peer_delta[7];
-    // bulk form (XCH kernels): the exchanged output is columns [xch_col0, xch_col0+xch_w)
-    // of the tile, stored at xch_base with row pitch xch_w (contiguous rows)
-    uint32_t xch_col0, xch_w;
-    float* xch_base;
+    int stage_stores;       // row-contiguous (smem-transposed) fp32 stores
 };
 
-constexpr uint32_t kXchCols = 64;                   // max exchanged columns per tile (bulk form)
-constexpr uint32_t kXchBytes = BM * kXchCols * 4;   // 32 KB staging tile
+// Store transpose buffer: per epilogue warp 32 rows x 16 fp32, row pitch 20 floats
+// (16-byte aligned rows; a quarter-warp's 8 float4 accesses hit distinct bank groups
+// in both the row-per-thread writes and the row-contiguous reads).
+constexpr uint32_t kStgPitch = 20;
+constexpr uint32_t kStgBytes = kEpiWarps * 32 * kStgPitch * 4;  // 20 KB
 
 // store one float4 locally and, for the exchanged output, into every peer buffer
 __device__ __forceinline__ void store4x(float* p, const float4& v, const Epi& ep, bool xchg) {
@@ -196,13 +183,14 @@ __device__ __forceinline__ void store1x(float* p, float v, const Epi& ep, bool x
         for (uint32_t r = 0; r < ep.npeers; ++r) *reinterpret_cast<float*>(reinterpret_cast<char*>(p) + ep.peer_delta[r]) = v;
 }
 
-template <int BN, int STAGES, bool XCH = false>
+template <int BN, int STAGES>
 struct Smem {
     static constexpr uint32_t kA = BM * BK * 2;  // bytes per A operand tile (hi or lo)
     static constexpr uint32_t kB = BN * BK * 2;
     static constexpr uint32_t kStage = 2 * kA + 2 * kB;
-    static constexpr uint32_t kStaging = XCH ? kXchBytes : 0;  // exchange staging tile
+    static constexpr uint32_t kStaging = kStgBytes;  // epilogue store transposes
     static constexpr uint32_t kBytes = STAGES * kStage + kStaging + 1024 /*align*/ + 512 /*barriers*/;
+    static_assert(kBytes <= 232448, "227 KB shared memory per CTA");
 };
 
 // Load one operand tile (rows x BK of a K-major matrix, or BK x rows of an
@@ -219,16 +207,16 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* ma
     }
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, bool XCH = false>
+template <int BN, int STAGES, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                 const Epi ep) {
-    using S = Smem<BN, STAGES, XCH>;
+    using S = Smem<BN, STAGES>;
     constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    float* staging = reinterpret_cast<float*>(smem + STAGES * S::kStage);  // XCH only
+    float* epi_stage = reinterpret_cast<float*>(smem + STAGES * S::kStage);  // store transposes
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage + S::kStaging);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2]
@@ -354,10 +342,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t row = mt * BM + lane_base + lane;
             const bool row_ok = row < ep.m;
             const float rs = (row_ok && ep.row_scale && ep.split_k <= 1) ? ep.row_scale[row] : 1.f;
-            if constexpr (XCH) {  // the staging tile is free once the previous bulk copy read it
-                if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-            }
 #pragma unroll 1
             for (int cb = 0; cb < kCols; cb += 32) {
                 uint32_t raw[32];
@@ -366,12 +350,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = has_k ? __uint_as_float(raw[j]) : 0.f;
-                if (!row_ok) continue;
 #pragma unroll
                 for (int h = 0; h < 32; h += 16) {
                     const uint32_t col0 = nt * BN + col_base + cb + h;
-                    if (col0 >= ep.n) continue;
+                    if (col0 >= ep.n) break;  // warp-uniform
                     float* vv = v + h;
+                    // Row-contiguous form of the main fp32 store (warp-uniform test): the
+                    // group's 32 rows x 16 columns go through smem and leave as 8 rows x 64 B
+                    // per store instruction instead of 32 rows x 16 B.
+                    float* fdst = nullptr;
+                    uint64_t fld = 0;
+                    bool fx = false;
+                    if (ep.stage_stores && ep.split_k <= 1 && col0 + 16 <= ep.n) {
+                        if (col0 + 16 <= ep.split && ep.c0 && ep.ldc0 % 4 == 0) {
+                            fdst = ep.c0 + col0;
+                            fld = ep.ldc0;
+                            fx = ep.npeers && ep.peer_target == 0;
+                        } else if (col0 >= ep.split && ep.c1 && ep.ldc1 % 4 == 0 && (col0 - ep.split) % 4 == 0) {
+                            fdst = ep.c1 + (col0 - ep.split);
+                            fld = ep.ldc1;
+                            fx = ep.npeers && ep.peer_target == 1;
+                        }
+                        if (fdst && (reinterpret_cast<uintptr_t>(fdst) & 15) != 0) fdst = nullptr;
+                    }
+                    if (!row_ok && !fdst) continue;
                     if (ep.split_k > 1) {
                         float* dst = ep.c0 + static_cast<uint64_t>(z) * ep.m * ep.ldc0 +
                                      static_cast<uint64_t>(row) * ep.ldc0 + col0;
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         continue;
                     }
-                    if (ep.mask) {  // ReLU backward: zero where the forward activation was not positive
+                    if (ep.mask && row_ok) {  // ReLU backward: zero where the forward activation was not positive
                         const float* mp = ep.mask + static_cast<uint64_t>(row) * ep.ld_mask + col0;
                         if (col0 + 16 <= ep.n && (ep.ld_mask % 4) == 0 &&
                             (reinterpret_cast<uintptr_t>(mp) & 15) == 0) {
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 if (col0 + j < ep.n && !(mp[j] > 0.f)) vv[j] = 0.f;
                         }
                     }
-                    if (ep.out_hi && ep.split_unscaled)
+                    if (ep.out_hi && ep.split_unscaled && row_ok)
                         store_split16(vv, ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0,
                                       ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0, col0, ep.n);
 #pragma unroll
@@ -412,18 +414,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                         vv[j] *= rs;
                         if (ep.relu) vv[j] = fmaxf(vv[j], 0.f);
                     }
-                    if constexpr (XCH) {  // exchanged columns go to the staging tile
-                        if (col0 >= ep.xch_col0 && col0 + 16 <= ep.xch_col0 + ep.xch_w) {
-                            float* st = staging + (lane_base + lane) * ep.xch_w + (col0 - ep.xch_col0);
+                    if (fdst) {
+                        float* srow = epi_stage + ((warp - 2) * 32 + lane) * kStgPitch;
+                        __syncwarp();
 #pragma unroll
-                            for (int j = 0; j < 16; j += 4)
-                                *reinterpret_cast<float4*>(st + j) = make_float4(vv[j], vv[j + 1], vv[j + 2], vv[j + 3]);
-                            if (ep.out_hi && !ep.split_unscaled)
-                                store_split16(vv, ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0,
-                                              ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0, col0, ep.n);
-                            continue;
+                        for (int j = 0; j < 16; j += 4)
+                            *reinterpret_cast<float4*>(srow + j) = make_float4(vv[j], vv[j + 1], vv[j + 2], vv[j + 3]);
+                        __syncwarp();
+                        const uint32_t sr = lane >> 2, sc = (lane & 3) * 4;
+                        const float* sbase = epi_stage + (warp - 2) * 32 * kStgPitch;
+#pragma unroll
+                        for (int pass = 0; pass < 4; ++pass) {
+                            const uint32_t r = pass * 8 + sr;
+                            const uint32_t orow = mt * BM + lane_base + r;
+                            if (orow < ep.m)
+                                store4x(fdst + static_cast<uint64_t>(orow) * fld + sc,
+                                        *reinterpret_cast<const float4*>(sbase + r * kStgPitch + sc), ep, fx);
                         }
+                        if (ep.out_hi && !ep.split_unscaled && row_ok)
+                            store_split16(vv, ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0,
+                                          ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0, col0, ep.n);
+                        continue;
                     }
+                    if (!row_ok) continue;
                     // a 16-column group entirely on one side of the split: 4 x 16 B stores
                     float* base = nullptr;
                     bool xchg = false;
@@ -463,32 +476,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
-            if constexpr (XCH) {
-                // staging complete: one thread pushes the tile's contiguous rows to the local
-                // buffer and to every peer over NVLink with bulk async copies
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-                if (threadIdx.x == 64) {
-                    const uint32_t m0 = mt * BM;
-                    const uint32_t valid = ep.m - m0 < BM ? ep.m - m0 : BM;
-                    const uint32_t bytes = valid * ep.xch_w * 4;
-                    float* dst = ep.xch_base + static_cast<uint64_t>(m0) * ep.xch_w;
-                    const uint32_t src = smem_u32(staging);
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                                 "r"(src), "r"(bytes)
-                                 : "memory");
-                    for (uint32_t r = 0; r < ep.npeers; ++r) {
-                        char* pd = reinterpret_cast<char*>(dst) + ep.peer_delta[r];
-                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(pd),
-                                     "r"(src), "r"(bytes)
-                                     : "memory");
-                    }
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                }
-            }
-        }
-        if constexpr (XCH) {  // all pushed bytes written before the kernel retires
-            if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -579,14 +566,14 @@ int operand_maps(CUtensorMap* hi, CUtensorMap* lo, const uint16_t* phi, const ui
 
 int g_num_sms = 0;
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, bool XCH = false>
+template <int BN, int STAGES, bool A_MN, bool B_MN>
 int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
     int rc;
     if ((rc = operand_maps(&ma_hi, &ma_lo, g->a_hi, g->a_lo, g->m, g->k, g->lda, A_MN, BM))) return rc;
     if ((rc = operand_maps(&mb_hi, &mb_lo, g->b_hi, g->b_lo, g->n, g->k, g->ldb, B_MN, BN))) return rc;
-    auto kern = gemm_bf16x3<BN, STAGES, A_MN, B_MN, XCH>;
-    const int bytes = Smem<BN, STAGES, XCH>::kBytes;
+    auto kern = gemm_bf16x3<BN, STAGES, A_MN, B_MN>;
+    const int bytes = Smem<BN, STAGES>::kBytes;
     static bool configured = false;  // per instantiation
     if (!configured) {
         GDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -604,33 +591,8 @@ int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     return check_launch("gdx_gemm_tn");
 }
 
-// Bulk-exchange form applies when the exchanged output of a (single) n-tile is a
-// contiguous block of rows <= 64 columns wide.
-bool bulk_exchange(const gdx_gemm_args* g, Epi& ep, int bn) {
-    if (!g->npeers || ep.n_tiles != 1 || g->split_k > 1 || static_cast<int>(g->n) > bn) return false;
-    float* base = g->peer_target == 1 ? g->c1 : g->c0;
-    const uint32_t col0 = g->peer_target == 1 ? g->split : 0;
-    const uint32_t w = g->peer_target == 1 ? g->n - g->split : g->split;
-    const uint64_t ld = g->peer_target == 1 ? g->ldc1 : g->ldc0;
-    if (!base || w == 0 || w > kXchCols || w % 16 != 0 || col0 % 16 != 0 || ld != w) return false;
-    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
-    for (uint32_t r = 0; r < g->npeers; ++r)
-        if (g->peer_delta[r] % 16 != 0) return false;
-    ep.xch_col0 = col0;
-    ep.xch_w = w;
-    ep.xch_base = base;
-    return true;
-}
-
 template <int BN, int STAGES>
-int launch_majors(const gdx_gemm_args* g, const Epi& ep_in, cudaStream_t s) {
-    Epi ep = ep_in;
-    if constexpr (BN <= 128) {
-        if (!g->a_mn_major && bulk_exchange(g, ep, BN)) {
-            if (g->b_mn_major) return launch_tc<BN, STAGES, false, true, true>(g, ep, s);
-            return launch_tc<BN, STAGES, false, false, true>(g, ep, s);
-        }
-    }
+int launch_majors(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     if (!g->a_mn_major && !g->b_mn_major) return launch_tc<BN, STAGES, false, false>(g, ep, s);
     if (g->a_mn_major && g->b_mn_major) return launch_tc<BN, STAGES, true, true>(g, ep, s);
     if (g->a_mn_major) return launch_tc<BN, STAGES, true, false>(g, ep, s);
@@ -658,7 +620,10 @@ Epi make_epi(const gdx_gemm_args* g, int bn) {
     Epi ep{g->m, g->n, g->c0, g->ldc0, g->c1, g->ldc1, g->split, g->row_scale, g->relu,
            g->out_hi, g->out_lo, g->ld_split, g->split_k ? g->split_k : 1,
            (g->k + BK - 1) / BK, (g->m + BM - 1) / BM, (g->n + bn - 1) / bn,
-           g->mask, g->ld_mask, g->split_unscaled, g->npeers, g->peer_target, {}, 0, 0, nullptr};
+           g->mask, g->ld_mask, g->split_unscaled, g->npeers, g->peer_target, {},
+           // measured (tools/gemm_bench.py): the transposed stores win on long
+           // write-bound GEMMs (6 M rows: 1.2-1.25x) and lose on short ones (233 K rows)
+           g->m >= (1u << 20) ? 1 : 0};
     for (int r = 0; r < 7; ++r) ep.peer_delta[r] = g->peer_delta[r];
     return ep;
 }
