@@ -250,6 +250,12 @@ class CobatchTrainer(FullGraphTrainer):
         # rows_in; the aggregation rewrites the other half there every step)
         for l, L in enumerate(self.layers):
             r_out, r_in = geo.rows_out[l], geo.rows_in[l]
+            if getattr(L, "agg_first", False):   # dA rows past the produced ones, dH_self
+                if r_out < geo.nloc:
+                    L.dAfull[self.lo + r_out:self.hi].zero_()
+                if r_out < r_in:
+                    L.dself[r_out:r_in].zero_()
+                continue
             if r_out < geo.nloc:
                 L.dfull[self.lo + r_out:self.hi].zero_()
             if self.cfg.kind == "sage" and r_out < r_in:

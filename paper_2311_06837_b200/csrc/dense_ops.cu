@@ -103,6 +103,40 @@ __global__ void grad_prepare_kernel(const float* dH, uint64_t ld_dh, const float
     }
 }
 
+// Vector form: c4 = width/4 threads per row, float4 loads/stores, ushort4 split stores.
+__global__ void grad_prepare_vec4(const float* __restrict__ dH, uint64_t ld_dh, const float* __restrict__ H,
+                                  uint64_t ld_h, uint32_t rows, uint32_t c4, uint32_t rows_per_block,
+                                  const float* __restrict__ dst_scale, float* g_out, uint64_t ld_gout,
+                                  float* gs, uint64_t ld_gs, uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g) {
+    const uint32_t sub = threadIdx.x / c4, c = threadIdx.x - sub * c4;
+    if (sub >= rows_per_block) return;
+    for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * rows_per_block + sub; r < rows;
+         r += static_cast<uint64_t>(gridDim.x) * rows_per_block) {
+        float4 g = *reinterpret_cast<const float4*>(dH + r * ld_dh + 4 * c);
+        if (H) {
+            const float4 h = __ldg(reinterpret_cast<const float4*>(H + r * ld_h + 4 * c));
+            if (!(h.x > 0.f)) g.x = 0.f;
+            if (!(h.y > 0.f)) g.y = 0.f;
+            if (!(h.z > 0.f)) g.z = 0.f;
+            if (!(h.w > 0.f)) g.w = 0.f;
+        }
+        if (g_out) *reinterpret_cast<float4*>(g_out + r * ld_gout + 4 * c) = g;
+        if (gs) {
+            const float sc = dst_scale ? dst_scale[r] : 1.f;
+            *reinterpret_cast<float4*>(gs + r * ld_gs + 4 * c) = make_float4(g.x * sc, g.y * sc, g.z * sc, g.w * sc);
+        }
+        if (g_hi) {
+            ushort4 hh, ll;
+            split_bf16(g.x, hh.x, ll.x);
+            split_bf16(g.y, hh.y, ll.y);
+            split_bf16(g.z, hh.z, ll.z);
+            split_bf16(g.w, hh.w, ll.w);
+            *reinterpret_cast<ushort4*>(g_hi + r * ld_g + 4 * c) = hh;
+            *reinterpret_cast<ushort4*>(g_lo + r * ld_g + 4 * c) = ll;
+        }
+    }
+}
+
 // One warp per row.  Optional fused outputs of the last layer's backward prep:
 // split-bf16 copy of g = dlogits and gs = g * row_scale.
 struct PeerDeltas {
@@ -297,8 +331,21 @@ extern "C" int gdx_grad_prepare(const float* dH, uint64_t ld_dh, const float* H,
     GDX_REQUIRE(dH, GDX_INPUT, "gdx_grad_prepare: null dH");
     GDX_REQUIRE(!g_hi == !g_lo, GDX_INPUT, "gdx_grad_prepare: g_hi/g_lo must pair");
     if (!rows || !width) return GDX_OK;
-    grad_prepare_kernel<<<grid_for(static_cast<uint64_t>(rows) * width), 256, 0, as_cuda(stream)>>>(
-        dH, ld_dh, H, ld_h, rows, width, dst_scale, g_out, ld_gout, gs, ld_gs, g_hi, g_lo, ld_g);
+    auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    auto a8 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 7) == 0; };
+    const bool vec = width % 4 == 0 && width <= 1024 && ld_dh % 4 == 0 && a16(dH) &&
+                     (!H || (ld_h % 4 == 0 && a16(H))) && (!g_out || (ld_gout % 4 == 0 && a16(g_out))) &&
+                     (!gs || (ld_gs % 4 == 0 && a16(gs))) && (!g_hi || (ld_g % 4 == 0 && a8(g_hi) && a8(g_lo)));
+    if (vec) {
+        const uint32_t c4 = width / 4, rpb = 256 / c4;
+        const uint64_t blocks = (static_cast<uint64_t>(rows) + rpb - 1) / rpb;
+        grad_prepare_vec4<<<static_cast<unsigned>(blocks < 65535ull * 32 ? blocks : 65535ull * 32), 256, 0,
+                            as_cuda(stream)>>>(dH, ld_dh, H, ld_h, rows, c4, rpb, dst_scale, g_out, ld_gout,
+                                               gs, ld_gs, g_hi, g_lo, ld_g);
+    } else {
+        grad_prepare_kernel<<<grid_for(static_cast<uint64_t>(rows) * width), 256, 0, as_cuda(stream)>>>(
+            dH, ld_dh, H, ld_h, rows, width, dst_scale, g_out, ld_gout, gs, ld_gs, g_hi, g_lo, ld_g);
+    }
     note_launch();
     return check_launch("gdx_grad_prepare");
 }

@@ -125,6 +125,7 @@ class _Layer:
         self.w = agg_width(fout, nfull)           # aggregation / row width of this layer
         self.nz = 2 * self.w if kind == "sage" else self.w   # GEMM N (W_cat rows)
         self.fin_ld = pad8(self.k)
+        self.upd_cols = fin                       # weight columns the SGD pass updates
         # master weights, row pitch == split pitch so the fused SGD can index both
         self.W = torch.zeros((self.nz, self.fin_ld), dtype=torch.float32, device=d)
         self.Wsp = Split(self.nz, self.k, d, ld=self.fin_ld)  # forward B (nz x k); MN-major B of dH
@@ -165,6 +166,69 @@ class _Layer:
         if self.kind == "sage":
             return [W[:self.fout, :self.fin].copy(), W[self.w:self.w + self.fout, :self.fin].copy()]
         return [W[:self.fout, :self.fin].copy()]
+
+
+class _AggFirstLayer:
+    """A widening SAGE output layer run aggregate-first (SURVEY §8a a5's order choice,
+    as forward_full does for widening layers): the exchange and the neighbour sum
+    run at the INPUT width and only the loss rows are transformed,
+        A = mean_{u in N(v)} H(u)          (H rows exchanged, fin_w wide)
+        logits = [H | A] [W_s | W_n]^T     (one GEMM, K = 2 fin_w, rows = loss rows)
+    backward:  dW = g^T [H | A];  [dH_self | dA] = g [W_s | W_n];
+               dH(u) = dH_self(u) + sum_{v in N(u)} dA(v) / deg(v)  (dA rows exchanged).
+    Same linear map as the transform-first layer; the transform-first order would
+    exchange and gather fout-wide rows of every input row instead."""
+
+    agg_first = True
+
+    def __init__(self, fin, fout, fin_w, nloc, nfull, d, splitk_target, p2p=None):
+        self.kind, self.fin, self.fout = "sage", fin, fout
+        self.w = fin_w                       # exchange / aggregation width (the input's)
+        self.k = 2 * fin_w                   # GEMM K: [H | A]
+        self.fin_ld = self.k
+        self.upd_cols = self.k               # both halves (padding columns stay zero)
+        self.nz = pad8(fout)                 # W' rows (logit columns)
+        self.W = torch.zeros((self.nz, self.fin_ld), dtype=torch.float32, device=d)
+        self.Wsp = Split(self.nz, self.k, d, ld=self.fin_ld)
+        self.dW = None
+        kb = max(1, math.ceil(nloc / 64))
+        ntiles = max(1, math.ceil(self.k / (256 if self.k > 128 else (128 if self.k > 64 else 64))))
+        self.split_k = max(1, min(kb, splitk_target // ntiles))
+        self.ws = torch.zeros((self.split_k * self.nz, self.fin_ld), dtype=torch.float32, device=d)
+        if p2p is None:
+            self.Xin_full = dense(nfull, fin_w, d)     # previous layer's output rows, gathered
+            self.dAfull = dense(nfull, fin_w, d)       # dA / deg rows, gathered
+            self.x_peers = self.da_peers = None
+        else:
+            self.Xin_full, self.x_peers = p2p.buffer(nfull, fin_w)
+            self.dAfull, self.da_peers = p2p.buffer(nfull, fin_w)
+        self.C = Split(nloc, self.k, d)                # [H | A] split operand
+        self.Hout = dense(nloc, self.nz, d)            # logits
+        self.Gl = Split(nloc, self.nz, d)              # g = dlogits (split)
+        self.dself = dense(nloc, fin_w, d)             # g W_s
+        self.dtmp = dense(nloc, fin_w, d)              # dH before the ReLU mask
+
+    def set_weights(self, mats):
+        ws, wn = mats
+        self.W.zero_()
+        self.W[:self.fout, :self.fin] = torch.from_numpy(ws.astype(np.float32))
+        self.W[:self.fout, self.w:self.w + self.fin] = torch.from_numpy(wn.astype(np.float32))
+        self.refresh_splits()
+
+    def refresh_splits(self):
+        self.Wsp.fill_from(self.W, self.fin_ld)
+
+    def get_weights(self):
+        W = self.W.double().cpu().numpy()
+        return [W[:self.fout, :self.fin].copy(), W[:self.fout, self.w:self.w + self.fin].copy()]
+
+    def w_cols(self, half: int) -> Split:
+        """MN-major B view of W' columns [half*fin_w, (half+1)*fin_w)."""
+        v = Split.__new__(Split)
+        v.rows, v.cols, v.ld = self.nz, self.w, self.fin_ld
+        v.hi = _Ptr(self.Wsp.hi.data_ptr() + 2 * half * self.w)
+        v.lo = _Ptr(self.Wsp.lo.data_ptr() + 2 * half * self.w)
+        return v
 
 
 class FullGraphTrainer:
@@ -291,6 +355,13 @@ class FullGraphTrainer:
         sm = torch.cuda.get_device_properties(d).multi_processor_count
         self.layers = []
         for l in range(cfg.layers):
+            if l == cfg.layers - 1 and l > 0 and cfg.kind == "sage" and \
+                    os.environ.get("GDX_AGG_FIRST", "1") != "0" and \
+                    agg_width(cfg.dims[l + 1], self.nrows_gather) > self.layers[-1].w:
+                self.layers.append(_AggFirstLayer(cfg.dims[l], cfg.dims[l + 1], self.layers[-1].w,
+                                                  self.nloc, self.nrows_gather, d, 2 * sm,
+                                                  p2p=self.p2p))
+                continue
             self.layers.append(_Layer(cfg.kind, cfg.dims[l], cfg.dims[l + 1], self.nloc,
                                       self.nrows_gather, d, 2 * sm, l == 0,
                                       self.layers[-1].w if l else None, p2p=self.p2p))
@@ -403,8 +474,19 @@ class FullGraphTrainer:
         acts = []
         for l, L in enumerate(self.layers):
             relu = l + 1 < cfg.layers
-            own = L.Zfull[self.lo:self.hi]
             m_in, r_out = self.rows_in[l], self.rows_out[l]
+            if getattr(L, "agg_first", False):
+                # the previous layer left its rows in L.Xin_full (own block) and their
+                # split copy in L.C[:, :w]; exchange them, average the neighbours into
+                # L.C[:, w:], then one GEMM over the produced rows
+                self._publish(L.Xin_full[self.lo:self.hi], L.x_peers)
+                self._exchange_aggregate(L.Xin_full, L.w, rows=r_out, out_split=_SplitView(L.C, L.w),
+                                         self_coef=0.0, self_base=self.lo, post_scale=self.inv_deg)
+                gemm_tn(L.C, L.Wsp, c0=L.Hout, m=r_out)
+                if self.keep_activations:
+                    acts.append(L.Hout[:self.nloc, :L.fout].clone())
+                continue
+            own = L.Zfull[self.lo:self.hi]
             if cfg.kind == "sage":
                 gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w, m=m_in, peers=self._peers(L.z_peers, 1))
             elif cfg.kind == "gcn":
@@ -412,21 +494,33 @@ class FullGraphTrainer:
             else:
                 gemm_tn(A, L.Wsp, c0=own, m=m_in, peers=self._peers(L.z_peers, 0))
             self._publish(own, L.z_peers)
+            nxt = self.layers[l + 1] if l + 1 < cfg.layers else None
+            if getattr(nxt, "agg_first", False):   # output rows feed an aggregate-first layer
+                out, out_split = nxt.Xin_full[self.lo:self.hi], _SplitView(nxt.C, 0)
+            else:
+                out, out_split = L.Hout, L.Hsp
             if cfg.kind == "sage":
-                self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=L.Hout, out_split=L.Hsp,
+                self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=out, out_split=out_split,
                                          self_coef=0.0, self_base=self.lo, post_scale=self.inv_deg,
                                          add=L.S, relu=relu)
             elif cfg.kind == "gcn":
-                self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=L.Hout, out_split=L.Hsp,
+                self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=out, out_split=out_split,
                                          self_coef=1.0, self_base=self.lo, post_scale=self.gcn_s, relu=relu)
             else:
-                self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=L.Hout, out_split=L.Hsp,
+                self._exchange_aggregate(L.Zfull, L.w, rows=r_out, out=out, out_split=out_split,
                                          self_coef=1.0, self_base=self.lo, relu=relu)
             A = L.Hsp
             if self.keep_activations:
-                acts.append(L.Hout[:self.nloc, :L.fout].clone())
+                acts.append(out[:self.nloc, :L.fout].clone())
         self.activations = acts
         return self.layers[-1].Hout
+
+    def _act(self, l: int) -> torch.Tensor:
+        """fp32 output rows of layer l (the ReLU mask of its backward)."""
+        nxt = self.layers[l + 1] if l + 1 < len(self.layers) else None
+        if getattr(nxt, "agg_first", False):
+            return nxt.Xin_full[self.lo:self.hi]
+        return self.layers[l].Hout
 
     def _peers(self, deltas, target: int):
         if self.p2p is None or deltas is None or self.p2p.mode != "epilogue":
@@ -460,8 +554,11 @@ class FullGraphTrainer:
         nL = cfg.layers
         for l in range(nL - 1, -1, -1):
             L = self.layers[l]
-            # dZ = agg^T(gs): SAGE -> G[:, w:2w]; GCN/SUM -> G (all columns)
             r_in = self.rows_in[l]   # dZ is needed for the rows that fed layer l
+            if getattr(L, "agg_first", False):
+                self._backward_agg_first(l)
+                continue
+            # dZ = agg^T(gs): SAGE -> G[:, w:2w]; GCN/SUM -> G (all columns)
             if cfg.kind == "sage":
                 Gn = _SplitView(L.G, L.w)
                 self._exchange_aggregate(L.dfull, L.w, rows=r_in, out_split=Gn, self_coef=0.0,
@@ -476,7 +573,7 @@ class FullGraphTrainer:
             # epilogue: ReLU backward with H_{l} as mask, scale, split -> layer l-1's inputs
             if l > 0:
                 own, scale, split = self._grad_targets(l - 1)
-                gemm_tn(L.G, L.Wsp, c0=own, b_mn=True, mask=self.layers[l - 1].Hout,
+                gemm_tn(L.G, L.Wsp, c0=own, b_mn=True, mask=self._act(l - 1),
                         row_scale=scale, out_split=split, split_unscaled=True, m=self.rows_out[l - 1],
                         peers=self._peers(self.layers[l - 1].d_peers, 0))
                 self._publish(own, self.layers[l - 1].d_peers)
@@ -486,26 +583,69 @@ class FullGraphTrainer:
             sk = _splitk_eff(L.split_k, r_in)
             gemm_tn(L.G.rows_view(r_in), A_in.rows_view(r_in), c0=L.ws, split_k=sk, a_mn=True,
                     b_mn=True)
-            if self.world == 1:  # reduce split-K partials and apply SGD in one pass
-                call("gdx_splitk_reduce", L.ws.data_ptr(), sk, L.nz * L.fin_ld, L.nz, L.fin,
-                     L.fin_ld, L.dW.data_ptr(), L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(),
-                     L.Wsp.lo.data_ptr(), stream_handle())
-            else:                # reduce partials; SGD after the epoch's single all-reduce
-                call("gdx_splitk_reduce", L.ws.data_ptr(), sk, L.nz * L.fin_ld, L.nz, L.fin,
-                     L.fin_ld, L.dW.data_ptr(), None, 0.0, None, None, stream_handle())
+            self._sgd_or_reduce(L, sk, L.upd_cols)
         if self.world > 1:
             # one all-reduce for every layer's dW and the loss, then SGD (+ split refresh)
             self.grad_flat[-1:].copy_(self.loss_acc)
             self._allreduce(self.grad_flat)
             self.loss_acc.copy_(self.grad_flat[-1:])
             for L in self.layers:
-                call("gdx_splitk_reduce", L.dW.data_ptr(), 1, 0, L.nz, L.fin, L.fin_ld, None,
+                call("gdx_splitk_reduce", L.dW.data_ptr(), 1, 0, L.nz, L.upd_cols, L.fin_ld, None,
                      L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(), L.Wsp.lo.data_ptr(), stream_handle())
+
+    def _sgd_or_reduce(self, L, sk: int, cols: int):
+        """Reduce layer L's split-K partials into dW; on one GPU also apply SGD (and
+        refresh the split copy) in the same pass."""
+        if self.world == 1:  # reduce split-K partials and apply SGD in one pass
+            call("gdx_splitk_reduce", L.ws.data_ptr(), sk, L.nz * L.fin_ld, L.nz, cols, L.fin_ld,
+                 L.dW.data_ptr(), L.W.data_ptr(), self.cfg.lr, L.Wsp.hi.data_ptr(), L.Wsp.lo.data_ptr(),
+                 stream_handle())
+        else:                # reduce partials; SGD after the epoch's single all-reduce
+            call("gdx_splitk_reduce", L.ws.data_ptr(), sk, L.nz * L.fin_ld, L.nz, cols, L.fin_ld,
+                 L.dW.data_ptr(), None, 0.0, None, None, stream_handle())
+
+    def _backward_agg_first(self, l: int):
+        """Backward of an aggregate-first layer (g = dlogits in L.Gl, split)."""
+        L = self.layers[l]
+        r = self.rows_out[l]
+        # [dH_self | dA/deg] = g [W_s | W_n] with the pre-update weights
+        gemm_tn(L.Gl, L.w_cols(0), c0=L.dself, b_mn=True, m=r)
+        own = L.dAfull[self.lo:self.hi]
+        gemm_tn(L.Gl, L.w_cols(1), c0=own, b_mn=True, row_scale=self.inv_deg, m=r)
+        self._publish(own, L.da_peers)
+        # dW' = g^T [H | A] over the produced rows (runs while the dA rows move)
+        sk = _splitk_eff(L.split_k, r)
+        gemm_tn(L.Gl.rows_view(r), L.C.rows_view(r), c0=L.ws, split_k=sk, a_mn=True, b_mn=True)
+        self._sgd_or_reduce(L, sk, L.upd_cols)
+        # dH(u) = dH_self(u) + sum_{v in N(u)} dA(v)/deg(v), over the rows that fed layer l
+        self._exchange_aggregate(L.dAfull, L.w, rows=self.rows_in[l], out=L.dtmp, self_coef=0.0,
+                                 self_base=self.lo, add=L.dself)
+        # ReLU backward + the previous layer's gradient targets (scaled rows to gather,
+        # unscaled split copy for its dW), then publish them
+        pown, scale, split = self._grad_targets(l - 1)
+        act = self._act(l - 1)
+        call("gdx_grad_prepare", L.dtmp.data_ptr(), L.dtmp.shape[1], act.data_ptr(), act.stride(0),
+             self.rows_out[l - 1], L.w, _lib.ptr(scale), None, 0, pown.data_ptr(), pown.stride(0),
+             _lib.ptr(split.hi) if split is not None else None,
+             _lib.ptr(split.lo) if split is not None else None, split.ld if split is not None else 0,
+             stream_handle())
+        self._publish(pown, self.layers[l - 1].d_peers)
 
     def train_epoch(self, sync_loss: bool = True):
         """Forward, loss, backward, SGD.  Returns the loss (host float) if sync_loss."""
         self.loss_acc.zero_()
         logits = self.forward()
+        Llast = self.layers[-1]
+        if getattr(Llast, "agg_first", False):
+            # g = dlogits, split only (its consumers are the layer's own GEMMs)
+            call("gdx_softmax_xent_fused", logits.data_ptr(), logits.shape[1], self.loss_rows,
+                 self.cfg.classes, self.labels.data_ptr(), 1.0 / self.loss_count, None, 0, None,
+                 None, 0, Llast.Gl.hi.data_ptr(), Llast.Gl.lo.data_ptr(), Llast.Gl.ld,
+                 self.loss_acc.data_ptr(), stream_handle())
+            self.backward_and_step()
+            if sync_loss:
+                return float(self.loss_acc.item()) / self.loss_count
+            return None
         own, scale, split = self._grad_targets(self.cfg.layers - 1)
         if self.p2p is not None and self.p2p.mode == "epilogue":
             Lz = self.layers[-1]

@@ -68,13 +68,14 @@ def _oracle_batch(g, batch, layers, x_all, lab_all):
     return lc, x_all[order], lab_all[order], layer_rows, len(batch.target_vertices), mfg
 
 
-@pytest.mark.parametrize("kind,r,m,k", [("sage", 3, 1, 15), ("gcn", 2, 2, 4), ("sum", 4, 1, 3)])
-def test_cobatch_training_matches_oracle(cuda, kind, r, m, k):
+@pytest.mark.parametrize("kind,r,m,k,out", [("sage", 3, 1, 15, 8), ("gcn", 2, 2, 4, 8),
+                                            ("sum", 4, 1, 3, 8), ("sage", 3, 1, 15, 72)])
+def test_cobatch_training_matches_oracle(cuda, kind, r, m, k, out):
     import paper_2311_06837_b200 as G
     from paper_2311_06837_b200.cobatch import CobatchTrainer
     from paper_2311_06837_b200.train import ModelConfig, init_weights
 
-    dims = [48, 32, 32, 8]
+    dims = [48, 32, 32, out]   # out = 72: widening output layer (aggregate-first)
     L = len(dims) - 1
     g, hp, plan = _plan(2500, 10.0, 21, 2, 1, r, L, G.SamplingConfig(m, k, 3), dims)
     lr = 1e-4 if kind == "sum" else 0.5

@@ -130,8 +130,10 @@ def _rand_csr(n, deg, seed):
     return O.gen_random_graph(n, deg, seed)
 
 
-@pytest.mark.parametrize("width", [1, 3, 4, 8, 12, 41, 44, 64, 128, 130, 256, 602])
-def test_aggregate_widths(gdx, cuda, width):
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("width", [1, 3, 4, 8, 12, 41, 44, 48, 64, 128, 130, 192, 256, 602])
+def test_aggregate_widths(gdx, cuda, width, variant):
+    """Warp-per-row (variant 0, auto) and lane-group-per-row (GDX_AGG_ROWS) kernels."""
     import torch
     from paper_2311_06837_b200.device import DeviceCSR
     g = _rand_csr(700, 9.0, width)
@@ -147,7 +149,7 @@ def test_aggregate_widths(gdx, cuda, width):
     out = gdx.dense(g.n, width, cuda)
     sp = gdx.Split(g.n, width, cuda)
     gdx.aggregate(dg, X, width, out=out, out_split=sp, self_coef=1.0,
-                  post_scale=torch.from_numpy(scale).to(cuda), add=Add, relu=True)
+                  post_scale=torch.from_numpy(scale).to(cuda), add=Add, relu=True, variant=variant)
     torch.cuda.synchronize()
     ro, ci = g.row_offsets.astype(np.int64), g.cols.astype(np.int64)
     xd = x.astype(np.float64)
@@ -216,3 +218,44 @@ def test_gemm_mask_epilogue_fused_backward(gdx, cuda):
     gref = np.where(mask > 0, dh, 0.0)
     close(sp.to_float().double().cpu().numpy(), gref)
     close(out[:m, :n].double().cpu().numpy(), gref * scale[:, None])
+
+
+@pytest.mark.parametrize("width", [64, 30])
+def test_grad_prepare(gdx, cuda, width):
+    """g = dH * (H > 0) -> split(g) and gs = g * scale (vector and scalar forms)."""
+    import torch
+    from paper_2311_06837_b200._lib import call
+    rng = np.random.default_rng(width)
+    n = 1000
+    dh = rng.uniform(-1, 1, (n, width)).astype(np.float32)
+    h = rng.uniform(-1, 1, (n, width)).astype(np.float32)
+    sc = rng.uniform(0.5, 2, n).astype(np.float32)
+    DH, H = (torch.from_numpy(a).to(cuda) for a in (dh, h))
+    S = torch.from_numpy(sc).to(cuda)
+    gs = torch.zeros(n, width, device=cuda)
+    sp = gdx.Split(n, width, cuda)
+    call("gdx_grad_prepare", DH.data_ptr(), width, H.data_ptr(), width, n, width, S.data_ptr(), None, 0,
+         gs.data_ptr(), width, sp.hi.data_ptr(), sp.lo.data_ptr(), sp.ld, gdx.stream_handle())
+    torch.cuda.synchronize()
+    g = np.where(h > 0, dh, 0).astype(np.float64)
+    close(sp.to_float().double().cpu().numpy(), g)
+    close(gs.double().cpu().numpy(), g * sc[:, None])
+
+
+def test_gather_split_rows_exact(gdx, cuda):
+    """The cooperative-batch LOAD: rows idx of a split store, bit-exact."""
+    import torch
+    from paper_2311_06837_b200._lib import call
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, (5000, 128)).astype(np.float32)
+    src = _split(gdx, x, cuda)
+    idx = np.sort(rng.choice(5000, 777, replace=False)).astype(np.int32)
+    I = torch.from_numpy(idx).to(cuda)
+    out = gdx.Split(777, 128, cuda)
+    call("gdx_gather_split_rows", src.hi.data_ptr(), src.lo.data_ptr(), src.ld, I.data_ptr(), 777, 128,
+         out.hi.data_ptr(), out.lo.data_ptr(), out.ld, gdx.stream_handle())
+    torch.cuda.synchronize()
+    a = src.hi.view(5000, src.ld)[I.long()].cpu().numpy()
+    b = out.hi.view(777, out.ld).cpu().numpy()
+    assert np.array_equal(a, b)
+    assert np.array_equal(src.lo.view(5000, src.ld)[I.long()].cpu().numpy(), out.lo.view(777, out.ld).cpu().numpy())

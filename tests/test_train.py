@@ -59,6 +59,16 @@ def test_ten_epoch_loss_parity(cuda, kind):
     assert lg[-1] < lg[0]  # it trains
 
 
+@pytest.mark.parametrize("agg_first", ["1", "0"])
+def test_widening_output_layer_parity(cuda, monkeypatch, agg_first):
+    """SAGE with more classes than hidden units (papers shape: 64 -> 172): the output
+    layer runs aggregate-first (exchange and gather at the input width); both orders
+    must match the oracle."""
+    monkeypatch.setenv("GDX_AGG_FIRST", agg_first)
+    lg, lr = run_pair("sage", 2500, 12.0, [40, 32, 32, 72], 4, 0.5)
+    assert np.all(np.abs(lg - lr) <= 1e-3), (lg, lr)
+
+
 def test_sum_model_matches_reference_forward(cuda):
     """The reference Sum model (ReLU between layers) through the trainer."""
     lg, lr = run_pair("sum", 1500, 6.0, [16, 16, 8], 3, 1e-4)

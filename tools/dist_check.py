@@ -32,7 +32,8 @@ def main():
 
     out = {"world": world, "ok": True, "cases": []}
     for kind, n, deg, dims, epochs in (("sage", 5001, 24.0, [96, 64, 64, 41], 5),
-                                       ("gcn", 3001, 10.0, [32, 32, 8], 4)):
+                                       ("gcn", 3001, 10.0, [32, 32, 8], 4),
+                                       ("sage", 3001, 12.0, [40, 32, 32, 72], 3)):
         g = G.gen_random_graph(n, deg, 5)
         cfg = ModelConfig(kind, dims, lr=0.5)
         w0 = init_weights(cfg, 3)
@@ -61,7 +62,7 @@ def main():
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
     from test_cobatch import _oracle_batch, _plan
     from paper_2311_06837_b200.cobatch import CobatchTrainer
-    dims = [48, 32, 32, 8]
+    dims = [48, 32, 32, 72]   # widening output layer: aggregate-first inside the batch
     g, hp, plan = _plan(4000, 10.0, 21, 1, world, 3, 3, G.SamplingConfig(1, 15, 3), dims)
     cfg = ModelConfig("sage", dims, lr=0.5)
     w0 = init_weights(cfg, 3)
