@@ -168,6 +168,19 @@ int gdx_device_free(void* p);
 int gdx_ipc_get_handle(const void* base, void* handle64);   /* 64-byte cudaIpcMemHandle */
 int gdx_ipc_open(const void* handle64, void** out);         /* lazy peer access enabled */
 int gdx_ipc_close(void* p);
+/* SM-driven push of `bytes` at src to src + peer_delta[r] (IPC-mapped peer buffers)
+ * for r < npeers, fused with gdx_peer_signal: the last of `ctas` CTAs releases the
+ * stores (system fence) and bumps our slot in every peer's arrival array.
+ * `done`: a device u32, zero before the first call (re-armed by the kernel). */
+int gdx_push_peers(const void* src, uint64_t bytes, const int64_t* peer_delta, uint32_t npeers,
+                   unsigned long long* const* peer_slots_dev, unsigned int* done, uint32_t ctas,
+                   gdx_stream stream);
+/* NVSwitch multicast push: `bytes` at src stored once through the buffer's multicast
+ * mapping (mc_dst = same offset in it; multimem.st), replicated by the switch into every
+ * GPU's copy; fused signal as gdx_push_peers. */
+int gdx_push_multicast(const void* src, uint64_t bytes, void* mc_dst, uint32_t npeers,
+                       unsigned long long* const* peer_slots_dev, unsigned int* done, uint32_t ctas,
+                       gdx_stream stream);
 /* One copy-engine push (cudaMemcpyAsync D2D; dst may be an IPC-mapped peer address). */
 int gdx_memcpy_async(void* dst, const void* src, uint64_t bytes, gdx_stream stream);
 /* After the producing kernel: release its peer stores and increment this rank's slot

@@ -21,6 +21,87 @@ __global__ void peer_signal_kernel(unsigned long long* const* peer_slots, uint32
     }
 }
 
+struct PushPeers {
+    uint32_t n;
+    int64_t delta[7];
+};
+
+// SM push of a contiguous block to the same offset in every peer buffer (NVLink
+// stores, 16 B per lane, 4 vectors in flight), fused with the arrival signal: the
+// last CTA to finish (device-scope counter) releases all CTAs' stores system-wide
+// and bumps our slot in every peer's arrival array, then re-arms the counter.
+__global__ void __launch_bounds__(512) push_peers_kernel(const uint4* __restrict__ src, uint64_t n16,
+                                                         PushPeers pp,
+                                                         unsigned long long* const* peer_slots,
+                                                         unsigned int* done) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < n16; i += 4 * stride) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(src + i + u * stride);
+        for (uint32_t r = 0; r < pp.n; ++r) {
+            uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<char*>(const_cast<uint4*>(src)) + pp.delta[r]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d[i + u * stride] = v[u];
+        }
+    }
+    for (; i < n16; i += stride) {
+        const uint4 v = __ldg(src + i);
+        for (uint32_t r = 0; r < pp.n; ++r)
+            reinterpret_cast<uint4*>(reinterpret_cast<char*>(const_cast<uint4*>(src)) + pp.delta[r])[i] = v;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(done, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            for (uint32_t r = 0; r < pp.n; ++r) atomicAdd_system(peer_slots[r], 1ull);
+            *done = 0;
+        }
+    }
+}
+
+// NVSwitch multicast push: every 16-byte vector of the block is read once locally
+// and stored ONCE to the multicast address (multimem.st); the switch replicates it
+// into every GPU's copy of the buffer, so the sender's NVLink egress is the block
+// size, not (world-1) x it.  Fused with the arrival signal like push_peers_kernel.
+__global__ void __launch_bounds__(512) push_multicast_kernel(const uint4* __restrict__ src, uint64_t n16,
+                                                             char* mc_dst, uint32_t npeers,
+                                                             unsigned long long* const* peer_slots,
+                                                             unsigned int* done) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < n16; i += 4 * stride) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(src + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc_dst + 16 * (i + u * stride)),
+                         "r"(v[u].x), "r"(v[u].y), "r"(v[u].z), "r"(v[u].w)
+                         : "memory");
+    }
+    for (; i < n16; i += stride) {
+        const uint4 v = __ldg(src + i);
+        asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc_dst + 16 * i), "r"(v.x),
+                     "r"(v.y), "r"(v.z), "r"(v.w)
+                     : "memory");
+    }
+    asm volatile("fence.proxy.alias;" ::: "memory");
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(done, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            for (uint32_t r = 0; r < npeers; ++r) atomicAdd_system(peer_slots[r], 1ull);
+            *done = 0;
+        }
+    }
+}
+
 // Round k of the exchange is complete when every other rank's slot reached k:
 // *expected += 1, then spin (acquire, system scope) on each slot; traps after
 // timeout_ns instead of hanging.
@@ -109,4 +190,39 @@ extern "C" int gdx_memcpy_async(void* dst, const void* src, uint64_t bytes, gdx_
     if (!bytes) return GDX_OK;
     GDX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_cuda(stream)));
     return GDX_OK;
+}
+
+// SM-driven push + signal (see push_peers_kernel); `done` is a zeroed device counter.
+extern "C" int gdx_push_peers(const void* src, uint64_t bytes, const int64_t* peer_delta, uint32_t npeers,
+                              unsigned long long* const* peer_slots_dev, unsigned int* done, uint32_t ctas,
+                              gdx_stream stream) {
+    GDX_REQUIRE(npeers <= 7, GDX_INPUT, "gdx_push_peers: at most 7 peers");
+    GDX_REQUIRE(npeers == 0 || (peer_slots_dev && done && peer_delta), GDX_INPUT, "gdx_push_peers: null pointer");
+    GDX_REQUIRE(bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0, GDX_INPUT,
+                "gdx_push_peers: 16-byte aligned whole vectors only");
+    if (!npeers) return GDX_OK;
+    PushPeers pp{npeers, {}};
+    for (uint32_t r = 0; r < npeers; ++r) {
+        GDX_REQUIRE(peer_delta[r] % 16 == 0, GDX_INPUT, "gdx_push_peers: peer offsets must be 16-byte aligned");
+        pp.delta[r] = peer_delta[r];
+    }
+    push_peers_kernel<<<ctas ? ctas : 1, 512, 0, as_cuda(stream)>>>(
+        reinterpret_cast<const uint4*>(src), bytes / 16, pp, peer_slots_dev, done);
+    note_launch();
+    return check_launch("gdx_push_peers");
+}
+
+// Multicast push + signal (see push_multicast_kernel).  mc_dst: the block's address in
+// the buffer's multicast mapping (same offset as src in the local mapping).
+extern "C" int gdx_push_multicast(const void* src, uint64_t bytes, void* mc_dst, uint32_t npeers,
+                                  unsigned long long* const* peer_slots_dev, unsigned int* done,
+                                  uint32_t ctas, gdx_stream stream) {
+    GDX_REQUIRE(src && mc_dst && done && (npeers == 0 || peer_slots_dev), GDX_INPUT,
+                "gdx_push_multicast: null pointer");
+    GDX_REQUIRE(bytes % 16 == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(mc_dst)) & 15) == 0,
+                GDX_INPUT, "gdx_push_multicast: 16-byte aligned whole vectors only");
+    push_multicast_kernel<<<ctas ? ctas : 1, 512, 0, as_cuda(stream)>>>(
+        reinterpret_cast<const uint4*>(src), bytes / 16, static_cast<char*>(mc_dst), npeers, peer_slots_dev, done);
+    note_launch();
+    return check_launch("gdx_push_multicast");
 }

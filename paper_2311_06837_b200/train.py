@@ -34,7 +34,7 @@ import torch
 from . import _lib
 from ._lib import call
 from .device import DeviceCSR, Split, aggregate, dense, gemm_tn, pad4, pad8, require_cuda, stream_handle
-from .errors import InputError
+from .errors import InputError, InternalError
 from .gnn import FEAT_TAG, WEIG_TAG
 from .graph import Graph, partition_contiguous
 
@@ -768,7 +768,24 @@ class P2PExchange:
         import torch.distributed as dist
         self.rank, self.world, self.pg, self.d = rank, world, pg, device
         self.mode = mode
-        self.sides = [torch.cuda.Stream(device=device) for _ in range(world - 1)]
+        # copy-engine streams: `ce_split` per peer (one copy engine sustains ~200 GB/s of
+        # NVLink writes; several in parallel approach the link rate)
+        self.ce_split = max(1, int(os.environ.get("GDX_CE_SPLIT", "1")))
+        # 'sm': one SM-driven push kernel (all peers, fused signal) on a side stream
+        # 'mc': buffers in torch symmetric memory with an NVSwitch multicast mapping; the
+        # push stores each vector once and the switch replicates it to every GPU
+        self.push_kind = os.environ.get("GDX_PUSH", "sm")
+        self._mc_bufs = []   # (local base, bytes, multicast base, handle)
+        if self.push_kind == "mc":
+            import torch.distributed._symmetric_memory as symm
+            self._symm = symm
+            try:
+                symm.enable_symm_mem_for_group(pg.group_name)
+            except Exception:  # newer torch enables it implicitly
+                pass
+        self.push_ctas = int(os.environ.get("GDX_PUSH_CTAS", "32"))
+        self.push_done = torch.zeros(1, dtype=torch.int32, device=device)
+        self.sides = [torch.cuda.Stream(device=device) for _ in range((world - 1) * self.ce_split)]
         self.pushed = None
         self._owned, self._opened = [], []
         self.slots = self._alloc(8 * world)            # arrival slot per source rank
@@ -807,6 +824,18 @@ class P2PExchange:
     def buffer(self, rows: int, cols: int):
         """Zeroed [rows, cols] fp32 buffer shared with every peer; returns
         (tensor, byte deltas to the same address in each peer's buffer)."""
+        if self.push_kind == "mc":
+            t = self._symm.empty((max(rows, 1), cols), dtype=torch.float32, device=self.d)
+            t.zero_()
+            hdl = self._symm.rendezvous(t, self.pg.group_name)
+            if not hdl.multicast_ptr:
+                raise InternalError("GDX_PUSH=mc: no NVSwitch multicast support on this system")
+            base = t.data_ptr()
+            # symmetric allocations may sit at an offset inside the mapped buffer
+            mc = hdl.multicast_ptr + (base - hdl.buffer_ptrs[self.rank])
+            self._mc_bufs.append((base, t.numel() * 4, mc, hdl, t))
+            deltas = [hdl.buffer_ptrs[r] - hdl.buffer_ptrs[self.rank] for r in range(self.world) if r != self.rank]
+            return t[:rows], deltas
         ptr = self._alloc(rows * cols * 4)
         t = torch.as_tensor(_RawCUDA(ptr, (rows, cols)), device=self.d)
         handles = self._gather_handle(ptr)
@@ -818,21 +847,52 @@ class P2PExchange:
 
     def push(self, own: torch.Tensor, deltas):
         """'ce' mode: after the producer, copy the owned (contiguous) rows into each
-        peer's buffer on that peer's stream (copy engines), then signal that peer."""
+        peer's buffer with copy engines (ce_split streams per peer, 256-byte aligned
+        pieces), then signal that peer once all its pieces landed."""
         main = torch.cuda.current_stream()
         nbytes = own.numel() * own.element_size()
-        slot0 = self.peer_slots_dev.data_ptr()
-        for i, (dl, st) in enumerate(zip(deltas, self.sides)):
+        if self.push_kind == "mc":
+            st = self.sides[0]
             st.wait_stream(main)
+            p = own.data_ptr()
+            mc = next(m + (p - b) for b, n, m, _, _ in self._mc_bufs if b <= p < b + n)
             with torch.cuda.stream(st):
-                call("gdx_memcpy_async", own.data_ptr() + dl, own.data_ptr(), nbytes, stream_handle())
+                call("gdx_push_multicast", p, nbytes, mc, len(deltas), self.peer_slots_dev.data_ptr(),
+                     self.push_done.data_ptr(), self.push_ctas, stream_handle())
+            self.pushed = [st]
+            return
+        if self.push_kind == "sm":
+            st = self.sides[0]
+            st.wait_stream(main)
+            d = (_lib.C.c_int64 * 7)(*deltas)
+            with torch.cuda.stream(st):
+                call("gdx_push_peers", own.data_ptr(), nbytes, d, len(deltas), self.peer_slots_dev.data_ptr(),
+                     self.push_done.data_ptr(), self.push_ctas, stream_handle())
+            self.pushed = [st]
+            return
+        K = self.ce_split
+        piece = ((nbytes + K - 1) // K + 255) // 256 * 256
+        slot0 = self.peer_slots_dev.data_ptr()
+        base = own.data_ptr()
+        for i, dl in enumerate(deltas):
+            sts = self.sides[i * K:(i + 1) * K]
+            for j, st in enumerate(sts):
+                st.wait_stream(main)
+                lo = min(nbytes, j * piece)
+                hi = min(nbytes, lo + piece)
+                if hi > lo:
+                    with torch.cuda.stream(st):
+                        call("gdx_memcpy_async", base + lo + dl, base + lo, hi - lo, stream_handle())
+            for st in sts[1:]:
+                sts[0].wait_stream(st)
+            with torch.cuda.stream(sts[0]):
                 call("gdx_peer_signal", slot0 + 8 * i, 1, stream_handle())
-        self.pushed = True
+        self.pushed = self.sides[:len(deltas) * K]
 
     def wait(self):
-        if self.pushed:  # our pushes finished (the peer streams join the main stream)
+        if self.pushed:  # our pushes finished (the push streams join the main stream)
             main = torch.cuda.current_stream()
-            for st in self.sides:
+            for st in self.pushed:
                 main.wait_stream(st)
             self.pushed = None
         call("gdx_peer_wait", self.slots, self.expected, self.world, self.rank, self.TIMEOUT_NS,
