@@ -750,13 +750,19 @@ class P2PExchange:
     """Row exchange over NVLink peer memory, no NCCL on the data path.
 
     Each gathered buffer is a separate cudaMalloc allocation whose CUDA IPC handle is
-    shared with every rank.  After the producer (GEMM / softmax) has written this
+    shared with every rank (or, for 'mc', a torch symmetric-memory allocation with an
+    NVSwitch multicast mapping).  After the producer (GEMM / softmax) has written this
     rank's rows into its own buffer, the rows are pushed to the same offset in every
-    peer's buffer (peer_delta) -- by copy engines, one stream per peer so the copies
-    run concurrently and use no SMs ('ce'), or by the producer's epilogue itself
-    ('epilogue') -- and each peer's arrival slot for this rank is bumped.  `wait()`
-    (before the remote-source aggregation) spins until every peer's slot reached
-    the round."""
+    peer's buffer and each peer's arrival slot for this rank is bumped:
+      'sm' (default): one push kernel, 16-byte NVLink stores to every peer, the last
+            CTA releases the stores and signals (680 GB/s received per GPU at N=4,
+            tools/xch_bench.py; NCCL all-gather 546, copy engines 366);
+      'ce': copy engines, one stream per peer, then a signal kernel;
+      'mc': multimem.st through the multicast mapping (one store, the switch
+            replicates; not faster: an all-gather is bound by each GPU's ingress);
+      'epilogue': the producing GEMM / softmax epilogue stores into the peers itself.
+    `wait()` (before the remote-source aggregation) spins until every peer's slot
+    reached the round."""
 
     TIMEOUT_NS = 20_000_000_000  # a wedged peer traps after 20 s instead of hanging
 
