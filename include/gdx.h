@@ -168,6 +168,10 @@ int gdx_device_free(void* p);
 int gdx_ipc_get_handle(const void* base, void* handle64);   /* 64-byte cudaIpcMemHandle */
 int gdx_ipc_open(const void* handle64, void** out);         /* lazy peer access enabled */
 int gdx_ipc_close(void* p);
+/* Per-source wait of a pipelined exchange: advance=1 starts the round (*expected += 1)
+ * before waiting; every wait then blocks until slots[src] >= *expected. */
+int gdx_peer_wait_src(unsigned long long* slots, unsigned long long* expected, uint32_t src, int advance,
+                      uint64_t timeout_ns, gdx_stream stream);
 /* SM-driven push of `bytes` at src to src + peer_delta[r] (IPC-mapped peer buffers)
  * for r < npeers, fused with gdx_peer_signal: the last of `ctas` CTAs releases the
  * stores (system fence) and bumps our slot in every peer's arrival array.

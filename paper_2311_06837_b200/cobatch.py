@@ -41,7 +41,7 @@ from .device import DeviceCSR, Split, dense, require_cuda, stream_handle
 from .errors import InputError
 from .extract import kUnlimitedFanout, sampled_growth_device
 from .graph import Graph, Partition
-from .train import FEAT_TAG, FullGraphTrainer, ModelConfig, RowExchange
+from .train import FEAT_TAG, FullGraphTrainer, ModelConfig, RowExchange, source_bounds
 
 
 @dataclass
@@ -63,6 +63,8 @@ class BatchGeometry:
     seg_hi: torch.Tensor | None
     mfg: list               # |{d <= L-l}| over the whole batch, l = 0..L (== peel_mfg)
     edges_per_step: int     # CSR entries aggregated by this rank per step (fwd + bwd passes)
+    src_bounds: list = None  # per-source column segments (pipelined exchange)
+    src_nnz: list = None
 
 
 def split_batch_share(vb: torch.Tensor, sp: torch.Tensor, gp: torch.Tensor, server: int,
@@ -150,11 +152,17 @@ def batch_geometry(g: Graph, targets: np.ndarray, vertices: np.ndarray, sp: Part
         call("gdx_row_split", lptr.data_ptr(), lcol.data_ptr(), nloc, rank * block,
              rank * block + nloc, seg_lo.data_ptr(), seg_hi.data_ptr(), stream_handle())
         nnz_src = int((seg_hi - seg_lo)[:nloc].sum().item()) if nloc else 0
+    src_bounds = src_nnz = None
+    if sort_sources:
+        src_bounds = source_bounds(lptr, lcol, nloc, block, world, device)
+        src_nnz = [int((src_bounds[q + 1] - src_bounds[q])[:nloc].sum().item()) if nloc else 0
+                   for q in range(world)]
     del local_of, in_batch, tmask, mark
     lp = lptr.cpu().numpy()
     edges = int(sum(lp[r] for r in rows_out) + sum(lp[r] for r in rows_in))
     return BatchGeometry(csr, l2g, nloc, block, rows_in, rows_out, rows_out[-1] if layers else nloc,
-                         len(targets), nnz, nnz_src, inv_deg, gcn_s, seg_lo, seg_hi, mfg, edges)
+                         len(targets), nnz, nnz_src, inv_deg, gcn_s, seg_lo, seg_hi, mfg, edges,
+                         src_bounds, src_nnz)
 
 
 class CobatchTrainer(FullGraphTrainer):
@@ -236,6 +244,7 @@ class CobatchTrainer(FullGraphTrainer):
         self.loss_rows, self.loss_count = geo.loss_rows, float(geo.loss_count)
         self.inv_deg, self.gcn_s = geo.inv_deg, geo.gcn_s
         self.seg_lo, self.seg_hi = geo.seg_lo, geo.seg_hi
+        self.src_bounds, self.src_nnz = geo.src_bounds, geo.src_nnz
         self.exchange = RowExchange(np.arange(self.world + 1, dtype=np.int64) * geo.block,
                                     self.rank, self.world, self.pg)
         # LOAD: input rows of this rank's block from the resident store

@@ -127,6 +127,29 @@ __global__ void peer_wait_kernel(unsigned long long* slots, unsigned long long* 
     __threadfence_system();
 }
 
+// Per-source wait (pipelined exchange): the round number lives in *expected; with
+// advance the round is started (*expected += 1) before waiting on slots[src].
+__global__ void peer_wait_src_kernel(unsigned long long* slots, unsigned long long* expected, uint32_t src,
+                                     int advance, unsigned long long timeout_ns) {
+    if (threadIdx.x != 0) return;
+    unsigned long long want = *expected;
+    if (advance) {
+        want += 1;
+        *expected = want;
+    }
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(slots + src) : "memory");
+        if (v >= want) break;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) __trap();
+        __nanosleep(64);
+    }
+}
+
 }  // namespace
 }  // namespace gdx
 
@@ -164,6 +187,14 @@ extern "C" int gdx_ipc_open(const void* handle64, void** out) {
 extern "C" int gdx_ipc_close(void* p) {
     if (p) GDX_CUDA(cudaIpcCloseMemHandle(p));
     return GDX_OK;
+}
+
+extern "C" int gdx_peer_wait_src(unsigned long long* slots, unsigned long long* expected, uint32_t src,
+                                 int advance, uint64_t timeout_ns, gdx_stream stream) {
+    GDX_REQUIRE(slots && expected, GDX_INPUT, "gdx_peer_wait_src: null pointer");
+    peer_wait_src_kernel<<<1, 32, 0, as_cuda(stream)>>>(slots, expected, src, advance, timeout_ns);
+    note_launch();
+    return check_launch("gdx_peer_wait_src");
 }
 
 extern "C" int gdx_peer_signal(unsigned long long* const* peer_slots_dev, uint32_t npeers, gdx_stream stream) {

@@ -97,6 +97,18 @@ def agg_width(fout: int, rows: int) -> int:
 AGG_ROWS = 1  # gdx.h GDX_AGG_ROWS
 
 
+def source_bounds(row_ptr: torch.Tensor, col: torch.Tensor, rows: int, block: int, world: int,
+                  device) -> list:
+    """Per-row start of each source rank's column block [q*block, (q+1)*block) in a CSR
+    with ascending columns: world+1 int64 arrays (bounds[q][v] .. bounds[q+1][v] are
+    row v's sources owned by rank q)."""
+    b = [torch.empty(max(rows, 1), dtype=torch.int64, device=device) for _ in range(world + 1)]
+    for q in range(world):
+        call("gdx_row_split", row_ptr.data_ptr(), col.data_ptr(), rows, q * block, (q + 1) * block,
+             b[q].data_ptr(), b[q + 1].data_ptr(), stream_handle())
+    return b
+
+
 def agg_variant(width: int, nnz: int, rows: int) -> int:
     """Aggregation kernel for a CSR: the lane-group-per-row kernel for low-degree rows
     (measured B200, 6 M rows x 64: 1.8x at degree 2.6, 1.2x at 12, parity at 25) and
@@ -340,6 +352,11 @@ class FullGraphTrainer:
             call("gdx_row_split", self.csr.row_ptr.data_ptr(), self.csr.col.data_ptr(), self.nloc,
                  self.lo, self.hi, self.seg_lo.data_ptr(), self.seg_hi.data_ptr(), stream_handle())
             self.nnz_local_src = int((self.seg_hi - self.seg_lo)[:self.nloc].sum().item())
+            # per-source segments for the pipelined (ring-order) exchange
+            self.src_bounds = source_bounds(self.csr.row_ptr, self.csr.col, self.nloc, self.block,
+                                            world, d)
+            self.src_nnz = [int((self.src_bounds[q + 1] - self.src_bounds[q])[:self.nloc].sum().item())
+                            for q in range(world)]
         self.Xsp = Split(self.nloc, F, d)
         self._refresh_input_splits()
         self._init_model(xmode, use_p2p, weights, weight_seed)
@@ -406,7 +423,7 @@ class FullGraphTrainer:
     def enable_kernel_events(self, on: bool):
         self._events = [] if on else None
 
-    def _agg(self, csr, src, width, **kw):
+    def _agg(self, csr, src, width, nnz_hint=None, **kw):
         kw.setdefault("variant", agg_variant(width, self.nnz_local, self.nloc))
         ev = getattr(self, "_events", None)
         if ev is None:
@@ -416,7 +433,9 @@ class FullGraphTrainer:
         aggregate(csr, src, width, **kw)
         b.record()
         rows = csr.rows
-        if "row_begin" in kw:               # local-source pass of a split aggregation
+        if nnz_hint is not None:            # one source block of a pipelined exchange
+            nnz = nnz_hint
+        elif "row_begin" in kw:             # local-source pass of a split aggregation
             nnz = self.nnz_local_src
         elif "skip" in kw:                  # remote-source pass (+ partial read)
             nnz = self.nnz_local - self.nnz_local_src
@@ -439,6 +458,23 @@ class FullGraphTrainer:
         if self.p2p is not None and not self.p2p_split:
             self.p2p.wait()
             return self._agg(csr, full, width, **epi)
+        if self.p2p is not None and self.p2p.ring:
+            # pipelined: peers push to us one at a time (ring order), so source block q
+            # is aggregated as soon as it landed while the next one is in flight
+            P = self.partial[:, :pad4(width)] if self.partial.shape[1] != pad4(width) else self.partial
+            b, r, N = self.src_bounds, self.rank, self.world
+            self._agg(csr, full, width, nnz_hint=self.src_nnz[r], out=P, row_begin=b[r], row_end=b[r + 1])
+            for step in range(1, N):
+                q = (r - step) % N
+                self.p2p.wait_src(q, first=step == 1)
+                if step < N - 1:
+                    self._agg(csr, full, width, nnz_hint=self.src_nnz[q], row_begin=b[q],
+                              row_end=b[q + 1], partial=P, out=P)
+                else:
+                    self._agg(csr, full, width, nnz_hint=self.src_nnz[q], row_begin=b[q],
+                              row_end=b[q + 1], partial=P, **epi)
+            self.p2p.join()
+            return None
         if self.p2p is not None:
             # the producer already pushed our rows into every peer and signalled;
             # aggregate the owned sources, wait for the peers' rows, finish the rest
@@ -790,6 +826,11 @@ class P2PExchange:
             except Exception:  # newer torch enables it implicitly
                 pass
         self.push_ctas = int(os.environ.get("GDX_PUSH_CTAS", "32"))
+        # ring order (GDX_P2P_RING=1): push to rank+1, rank+2, ... one peer at a time and
+        # aggregate each source block as it lands.  Measured slower at N=4 (Reddit 3.41 vs
+        # 3.09 ms, products 10.96 vs 10.25 ms): one GPU pair gets well under the GPU's
+        # NVLink ingress, so the all-peer push wins; kept as an option.
+        self.ring = self.push_kind == "sm" and world > 2 and os.environ.get("GDX_P2P_RING", "0") != "0"
         self.push_done = torch.zeros(1, dtype=torch.int32, device=device)
         self.sides = [torch.cuda.Stream(device=device) for _ in range((world - 1) * self.ce_split)]
         self.pushed = None
@@ -867,6 +908,19 @@ class P2PExchange:
                      self.push_done.data_ptr(), self.push_ctas, stream_handle())
             self.pushed = [st]
             return
+        if self.push_kind == "sm" and self.ring:
+            st = self.sides[0]
+            st.wait_stream(main)
+            slot0 = self.peer_slots_dev.data_ptr()
+            with torch.cuda.stream(st):
+                for step in range(1, self.world):
+                    q = (self.rank + step) % self.world
+                    i = q if q < self.rank else q - 1
+                    d = (_lib.C.c_int64 * 7)(deltas[i])
+                    call("gdx_push_peers", own.data_ptr(), nbytes, d, 1, slot0 + 8 * i,
+                         self.push_done.data_ptr(), self.push_ctas, stream_handle())
+            self.pushed = [st]
+            return
         if self.push_kind == "sm":
             st = self.sides[0]
             st.wait_stream(main)
@@ -894,6 +948,20 @@ class P2PExchange:
             with torch.cuda.stream(sts[0]):
                 call("gdx_peer_signal", slot0 + 8 * i, 1, stream_handle())
         self.pushed = self.sides[:len(deltas) * K]
+
+    def wait_src(self, src: int, first: bool):
+        """Pipelined wait: block the stream until source rank `src`'s rows of this round
+        landed (first=True starts the round)."""
+        call("gdx_peer_wait_src", self.slots, self.expected, src, int(first), self.TIMEOUT_NS,
+             stream_handle())
+
+    def join(self):
+        """Order the stream after our own pushes (before the pushed rows are rewritten)."""
+        if self.pushed:
+            main = torch.cuda.current_stream()
+            for st in self.pushed:
+                main.wait_stream(st)
+            self.pushed = None
 
     def wait(self):
         if self.pushed:  # our pushes finished (the push streams join the main stream)
