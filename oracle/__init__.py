@@ -177,6 +177,10 @@ def ref() -> C.CDLL:
         L.grr_plan_free.argtypes = [vp]
         L.grr_simulate_cobatch_moved.argtypes = [vp, _u32p, _u32p, C.c_uint32, C.c_uint32,
                                                  C.c_uint32, C.POINTER(vp), _u64p, _u64p]
+        L.grr_simulate_epoch.argtypes = [vp, _u32p, _u32p, C.c_uint32, C.c_uint32, C.c_double,
+                                         C.c_double, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32,
+                                         C.c_int, C.c_uint32, C.c_uint32, C.c_uint64,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _ref = L
     return _ref
 

@@ -336,4 +336,47 @@ int grr_simulate_cobatch_moved(void* g, const std::uint32_t* sp, const std::uint
     });
 }
 
+// ---- simulator calibration: simulate_epoch (sim.cpp:165-283) with
+// caller-supplied rates.  strategy: 0 baseline, 1 shared preload, 2 preload+EAS.
+// totals[5] = compute, internal, external, grad sync, total (s); workers[6*i..] =
+// compute_s, internal_s, external_s, sync_s, internal_moved, external_moved.
+int grr_simulate_epoch(void* g, const std::uint32_t* sp, const std::uint32_t* gp, std::uint32_t servers,
+                       std::uint32_t gpus, double compute_vps, double internal_bw_vps,
+                       double external_bw_vps, std::uint32_t layers, std::uint32_t hidden,
+                       std::uint32_t feature, int strategy, std::uint32_t max_hop, std::uint32_t fanout,
+                       std::uint64_t sseed, double* totals, double* workers) {
+    return guarded([&] {
+        const Graph& gr = *static_cast<Graph*>(g);
+        Partition spp = make_partition(sp, gr.num_vertices(), servers);
+        Partition gpp = make_partition(gp, gr.num_vertices(), servers * gpus);
+        ClusterSpec c;
+        c.num_servers = servers;
+        c.gpus_per_server = gpus;
+        c.compute_vps = compute_vps;
+        c.internal_bw_vps = internal_bw_vps;
+        c.external_bw_vps = external_bw_vps;
+        ModelSpec m{layers, hidden, feature, 1.5};
+        Strategy st = strategy == 0 ? Strategy::FullGraphBaseline
+                                    : (strategy == 1 ? Strategy::SharedPreload : Strategy::PreloadEas);
+        std::optional<SamplingConfig> cfg;
+        if (strategy == 2) cfg = SamplingConfig{max_hop, fanout, sseed};
+        CostBreakdown b = simulate_epoch(gr, spp, gpp, c, m, st, cfg);
+        totals[0] = b.compute_s;
+        totals[1] = b.internal_comm_s;
+        totals[2] = b.external_comm_s;
+        totals[3] = b.grad_sync_s;
+        totals[4] = b.total_s;
+        for (std::size_t i = 0; i < b.workers.size(); ++i) {
+            const WorkerCost& w = b.workers[i];
+            double* o = workers + 6 * i;
+            o[0] = w.compute_s;
+            o[1] = w.internal_s;
+            o[2] = w.external_s;
+            o[3] = w.sync_s;
+            o[4] = static_cast<double>(w.internal_moved);
+            o[5] = static_cast<double>(w.external_moved);
+        }
+    });
+}
+
 }  // extern "C"
