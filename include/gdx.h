@@ -179,6 +179,12 @@ int gdx_peer_wait_src(unsigned long long* slots, unsigned long long* expected, u
 int gdx_push_peers(const void* src, uint64_t bytes, const int64_t* peer_delta, uint32_t npeers,
                    unsigned long long* const* peer_slots_dev, unsigned int* done, uint32_t ctas,
                    gdx_stream stream);
+/* Sparse push: rows idx[off[r] .. off[r+1]) of this rank's block (row pitch row_bytes)
+ * to the same offsets in peer r's buffer (base + peer_delta[r]), then signal as
+ * gdx_push_peers.  For exchanges where each peer reads only part of the block. */
+int gdx_push_rows(const void* base, uint64_t row_bytes, const uint32_t* idx, const uint64_t* off,
+                  const int64_t* peer_delta, uint32_t npeers, unsigned long long* const* peer_slots_dev,
+                  unsigned int* done, uint32_t ctas, gdx_stream stream);
 /* NVSwitch multicast push: `bytes` at src stored once through the buffer's multicast
  * mapping (mc_dst = same offset in it; multimem.st), replicated by the switch into every
  * GPU's copy; fused signal as gdx_push_peers. */

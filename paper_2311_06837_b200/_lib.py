@@ -75,6 +75,7 @@ _SIGS = {
     "gdx_push_peers": (C.c_int, [vp, u64, vp, u32, vp, vp, u32, vp]),
     "gdx_peer_wait_src": (C.c_int, [vp, vp, u32, C.c_int, u64, vp]),
     "gdx_push_multicast": (C.c_int, [vp, u64, vp, u32, vp, vp, u32, vp]),
+    "gdx_push_rows": (C.c_int, [vp, u64, vp, vp, vp, u32, vp, vp, u32, vp]),
     "gdx_peer_wait": (C.c_int, [vp, vp, u32, u32, u64, vp]),
     "gdx_softmax_xent_fused": (C.c_int, [vp, u64, u32, u32, vp, C.c_float, vp, u64, vp, vp, u64, vp, vp,
                                          u64, vp, vp]),

@@ -65,6 +65,7 @@ class BatchGeometry:
     edges_per_step: int     # CSR entries aggregated by this rank per step (fwd + bwd passes)
     src_bounds: list = None  # per-source column segments (pipelined exchange)
     src_nnz: list = None
+    send_rows: tuple = None  # (u32 row indices of this block, per-peer offsets) for sparse pushes
 
 
 def split_batch_share(vb: torch.Tensor, sp: torch.Tensor, gp: torch.Tensor, server: int,
@@ -216,6 +217,9 @@ class CobatchTrainer(FullGraphTrainer):
                                      world, cfg.layers, d, self.overlap)
                       for b in plan.batches]
         del spd, gpd
+        if world > 1 and os.environ.get("GDX_SPARSE_PUSH", "1") != "0":
+            for geo in self.geoms:
+                self._exchange_needs(geo)
         # buffers sized for the largest batch
         self.nloc = max([geo.nloc for geo in self.geoms] + [1])
         self.cap_rows = self.nloc
@@ -227,6 +231,37 @@ class CobatchTrainer(FullGraphTrainer):
         self.total_targets = sum(len(b.target_vertices) for b in plan.batches)
         self.current = None
         torch.cuda.synchronize(d)
+
+    def _exchange_needs(self, geo: BatchGeometry):
+        """Which rows of this rank's block each peer's CSR references (the simulator's
+        per-GPU 'deps', sim.cpp:241-250): every rank lists the rows it reads from each
+        source block, one all_to_all hands each list to its source.  Kept only when it
+        saves at least 10% of the full-block push."""
+        import torch.distributed as dist
+        d, r, W, B = self.d, self.rank, self.world, geo.block
+        cols = geo.csr.col[:geo.nnz].long()
+        need = []
+        for q in range(W):
+            if q == r:
+                need.append(torch.zeros(0, dtype=torch.int32, device=d))
+                continue
+            c = cols[(cols >= q * B) & (cols < (q + 1) * B)]
+            need.append((torch.unique(c) - q * B).to(torch.int32))
+        counts = torch.tensor([t.numel() for t in need], dtype=torch.int64, device=d)
+        got = torch.empty_like(counts)
+        dist.all_to_all_single(got, counts, group=self.pg)
+        send = torch.cat(need) if counts.sum() else torch.zeros(1, dtype=torch.int32, device=d)
+        recv = torch.empty(max(int(got.sum()), 1), dtype=torch.int32, device=d)
+        dist.all_to_all_single(recv[:int(got.sum())], send[:int(counts.sum())],
+                               output_split_sizes=got.tolist(), input_split_sizes=counts.tolist(),
+                               group=self.pg)
+        g = got.tolist()
+        off = [0]
+        for q in range(W):
+            if q != r:
+                off.append(off[-1] + g[q])
+        if off[-1] <= 0.9 * (W - 1) * geo.nloc:
+            geo.send_rows = (recv, off)
 
     def _refresh_input_splits(self):  # inputs arrive split (LOAD); nothing to refresh
         pass
@@ -245,6 +280,7 @@ class CobatchTrainer(FullGraphTrainer):
         self.inv_deg, self.gcn_s = geo.inv_deg, geo.gcn_s
         self.seg_lo, self.seg_hi = geo.seg_lo, geo.seg_hi
         self.src_bounds, self.src_nnz = geo.src_bounds, geo.src_nnz
+        self.send_rows = geo.send_rows
         self.exchange = RowExchange(np.arange(self.world + 1, dtype=np.int64) * geo.block,
                                     self.rank, self.world, self.pg)
         # LOAD: input rows of this rank's block from the resident store

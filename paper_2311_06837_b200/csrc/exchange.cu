@@ -63,6 +63,60 @@ __global__ void __launch_bounds__(512) push_peers_kernel(const uint4* __restrict
     }
 }
 
+struct PushRows {
+    uint32_t n;
+    int64_t delta[7];
+    uint64_t off[8];  // rows idx[off[r] .. off[r+1]) go to peer r
+};
+
+// Sparse push: only the rows each peer's CSR references (cooperative batches on
+// low-degree subgraphs need about half of a block).  Row k of the list for peer r is
+// copied to the same offset in peer r's buffer; 16-byte vectors, consecutive threads
+// cover one row, so every row is one coalesced burst.  Fused signal as above.
+__global__ void __launch_bounds__(512) push_rows_kernel(const char* __restrict__ base, uint32_t vpr,
+                                                        uint64_t row_bytes, const uint32_t* __restrict__ idx,
+                                                        PushRows pr, unsigned long long* const* peer_slots,
+                                                        unsigned int* done) {
+    // lane group of vpr lanes per row (rpw rows per warp), 4 rows in flight per group
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t rpw = vpr >= 32 ? 1 : 32 / vpr;
+    const uint32_t sub = vpr >= 32 ? 0 : lane / vpr;
+    const uint32_t v0 = vpr >= 32 ? lane : lane - sub * vpr;
+    const bool on = sub < rpw;
+    const uint64_t groups = static_cast<uint64_t>((gridDim.x * blockDim.x) >> 5) * rpw;
+    const uint64_t g0 = static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * rpw + sub;
+    // all peers at once (one GPU pair alone gets well under the NVLink ingress): item t
+    // copies row t of every peer's list
+    uint64_t tmax = 0;
+    for (uint32_t r = 0; r < pr.n; ++r) tmax = max(tmax, pr.off[r + 1] - pr.off[r]);
+    for (uint64_t t = g0; on && t < tmax; t += groups) {
+        uint64_t o[7];
+        bool ok[7];
+#pragma unroll
+        for (int r = 0; r < 7; ++r) {
+            ok[r] = r < static_cast<int>(pr.n) && t < pr.off[r + 1] - pr.off[r];
+            o[r] = ok[r] ? static_cast<uint64_t>(__ldg(idx + pr.off[r] + t)) * row_bytes : 0;
+        }
+        for (uint32_t v = v0; v < vpr; v += 32) {
+#pragma unroll
+            for (int r = 0; r < 7; ++r)
+                if (ok[r])
+                    *reinterpret_cast<uint4*>(const_cast<char*>(base) + o[r] + pr.delta[r] + 16 * v) =
+                        __ldg(reinterpret_cast<const uint4*>(base + o[r] + 16 * v));
+        }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(done, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            for (uint32_t r = 0; r < pr.n; ++r) atomicAdd_system(peer_slots[r], 1ull);
+            *done = 0;
+        }
+    }
+}
+
 // NVSwitch multicast push: every 16-byte vector of the block is read once locally
 // and stored ONCE to the multicast address (multimem.st); the switch replicates it
 // into every GPU's copy of the buffer, so the sender's NVLink egress is the block
@@ -256,4 +310,29 @@ extern "C" int gdx_push_multicast(const void* src, uint64_t bytes, void* mc_dst,
         reinterpret_cast<const uint4*>(src), bytes / 16, static_cast<char*>(mc_dst), npeers, peer_slots_dev, done);
     note_launch();
     return check_launch("gdx_push_multicast");
+}
+
+// Sparse push + signal (see push_rows_kernel).  base: this rank's block; idx: row
+// indices within it, concatenated per peer with offsets off[0..npeers].
+extern "C" int gdx_push_rows(const void* base, uint64_t row_bytes, const uint32_t* idx, const uint64_t* off,
+                             const int64_t* peer_delta, uint32_t npeers, unsigned long long* const* peer_slots_dev,
+                             unsigned int* done, uint32_t ctas, gdx_stream stream) {
+    GDX_REQUIRE(npeers <= 7, GDX_INPUT, "gdx_push_rows: at most 7 peers");
+    GDX_REQUIRE(npeers == 0 || (base && off && peer_delta && peer_slots_dev && done), GDX_INPUT,
+                "gdx_push_rows: null pointer");
+    GDX_REQUIRE(row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0, GDX_INPUT,
+                "gdx_push_rows: rows must be whole 16-byte vectors");
+    if (!npeers) return GDX_OK;
+    PushRows pr{npeers, {}, {}};
+    for (uint32_t r = 0; r < npeers; ++r) {
+        GDX_REQUIRE(peer_delta[r] % 16 == 0, GDX_INPUT, "gdx_push_rows: peer offsets must be 16-byte aligned");
+        pr.delta[r] = peer_delta[r];
+    }
+    for (uint32_t r = 0; r <= npeers; ++r) pr.off[r] = off[r];
+    GDX_REQUIRE(pr.off[npeers] == 0 || idx, GDX_INPUT, "gdx_push_rows: null index list");
+    push_rows_kernel<<<ctas ? ctas : 1, 512, 0, as_cuda(stream)>>>(
+        static_cast<const char*>(base), static_cast<uint32_t>(row_bytes / 16), row_bytes, idx, pr,
+        peer_slots_dev, done);
+    note_launch();
+    return check_launch("gdx_push_rows");
 }

@@ -570,7 +570,7 @@ class FullGraphTrainer:
         if self.p2p.mode == "epilogue":
             self.p2p.signal()
         else:
-            self.p2p.push(own, deltas)
+            self.p2p.push(own, deltas, rows=getattr(self, "send_rows", None))
 
     def _grad_targets(self, l: int):
         """Where the prepared gradient of layer l's output goes: gs = g * dst_scale into the
@@ -892,12 +892,25 @@ class P2PExchange:
     def signal(self):
         call("gdx_peer_signal", self.peer_slots_dev.data_ptr(), self.world - 1, stream_handle())
 
-    def push(self, own: torch.Tensor, deltas):
+    def push(self, own: torch.Tensor, deltas, rows=None):
         """'ce' mode: after the producer, copy the owned (contiguous) rows into each
         peer's buffer with copy engines (ce_split streams per peer, 256-byte aligned
         pieces), then signal that peer once all its pieces landed."""
         main = torch.cuda.current_stream()
         nbytes = own.numel() * own.element_size()
+        if rows is not None and self.push_kind in ("sm", "mc"):
+            # sparse: only the rows each peer reads (row lists from the batch geometry)
+            idx, off = rows
+            st = self.sides[0]
+            st.wait_stream(main)
+            d = (_lib.C.c_int64 * 7)(*deltas)
+            o = (_lib.C.c_uint64 * 8)(*off)
+            with torch.cuda.stream(st):
+                call("gdx_push_rows", own.data_ptr(), own.stride(0) * own.element_size(), idx.data_ptr(), o, d,
+                     len(deltas), self.peer_slots_dev.data_ptr(), self.push_done.data_ptr(),
+                     max(self.push_ctas, 64), stream_handle())
+            self.pushed = [st]
+            return
         if self.push_kind == "mc":
             st = self.sides[0]
             st.wait_stream(main)

@@ -75,6 +75,17 @@ def main():
                 x.wait()
             ms = timed(step)
             out["modes"][f"{kind}{c or ''}"] = {"ms": round(ms, 3), "GBps": round(recv / ms / 1e6, 1)}
+        if kind == "sm":  # sparse push of a random half of the rows to every peer
+            g = torch.Generator(device="cpu").manual_seed(rank)
+            half = torch.sort(torch.randperm(B, generator=g)[:B // 2])[0].to(torch.int32).to(dev)
+            idx = torch.cat([half] * (world - 1))
+            off = [i * (B // 2) for i in range(world)]
+
+            def step_sparse():
+                x.push(own, deltas, rows=(idx, off))
+                x.wait()
+            ms = timed(step_sparse)
+            out["modes"]["sm_rows_half"] = {"ms": round(ms, 3), "GBps": round(recv / 2 / ms / 1e6, 1)}
         torch.cuda.synchronize()
         dist.barrier()
     if rank == 0:
