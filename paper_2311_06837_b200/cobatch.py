@@ -80,6 +80,38 @@ def split_batch_share(vb: torch.Tensor, sp: torch.Tensor, gp: torch.Tensor, serv
     return share[:nb]
 
 
+def exchange_row_needs(cols: torch.Tensor, block: int, rank: int, world: int, pg):
+    """Which rows of this rank's block each peer's CSR references -- the reference
+    simulator's per-GPU 'deps' (sim.cpp:241-250).  Every rank lists the rows it reads
+    from each source block (cols: its CSR columns in padded ids), one all_to_all hands
+    each list to its source.  Returns (row indices within this rank's block, int32,
+    concatenated over the peers r != rank in ascending order; offsets, len world)."""
+    import torch.distributed as dist
+    d = cols.device
+    c = cols.long()
+    need = []
+    for q in range(world):
+        if q == rank:
+            need.append(torch.zeros(0, dtype=torch.int32, device=d))
+            continue
+        sel = c[(c >= q * block) & (c < (q + 1) * block)]
+        need.append((torch.unique(sel) - q * block).to(torch.int32))
+    counts = torch.tensor([t.numel() for t in need], dtype=torch.int64, device=d)
+    got = torch.empty_like(counts)
+    dist.all_to_all_single(got, counts, group=pg)
+    ns, nr = int(counts.sum()), int(got.sum())
+    send = torch.cat(need) if ns else torch.zeros(1, dtype=torch.int32, device=d)
+    recv = torch.empty(max(nr, 1), dtype=torch.int32, device=d)
+    dist.all_to_all_single(recv[:nr], send[:ns], output_split_sizes=got.tolist(),
+                           input_split_sizes=counts.tolist(), group=pg)
+    g = got.tolist()
+    off = [0]
+    for q in range(world):
+        if q != rank:
+            off.append(off[-1] + g[q])
+    return recv, off
+
+
 def _dev_assign(p, device) -> torch.Tensor:
     """Device int32 copy of a Partition's assignment (tensors pass through)."""
     if isinstance(p, torch.Tensor):
@@ -233,34 +265,10 @@ class CobatchTrainer(FullGraphTrainer):
         torch.cuda.synchronize(d)
 
     def _exchange_needs(self, geo: BatchGeometry):
-        """Which rows of this rank's block each peer's CSR references (the simulator's
-        per-GPU 'deps', sim.cpp:241-250): every rank lists the rows it reads from each
-        source block, one all_to_all hands each list to its source.  Kept only when it
-        saves at least 10% of the full-block push."""
-        import torch.distributed as dist
-        d, r, W, B = self.d, self.rank, self.world, geo.block
-        cols = geo.csr.col[:geo.nnz].long()
-        need = []
-        for q in range(W):
-            if q == r:
-                need.append(torch.zeros(0, dtype=torch.int32, device=d))
-                continue
-            c = cols[(cols >= q * B) & (cols < (q + 1) * B)]
-            need.append((torch.unique(c) - q * B).to(torch.int32))
-        counts = torch.tensor([t.numel() for t in need], dtype=torch.int64, device=d)
-        got = torch.empty_like(counts)
-        dist.all_to_all_single(got, counts, group=self.pg)
-        send = torch.cat(need) if counts.sum() else torch.zeros(1, dtype=torch.int32, device=d)
-        recv = torch.empty(max(int(got.sum()), 1), dtype=torch.int32, device=d)
-        dist.all_to_all_single(recv[:int(got.sum())], send[:int(counts.sum())],
-                               output_split_sizes=got.tolist(), input_split_sizes=counts.tolist(),
-                               group=self.pg)
-        g = got.tolist()
-        off = [0]
-        for q in range(W):
-            if q != r:
-                off.append(off[-1] + g[q])
-        if off[-1] <= 0.9 * (W - 1) * geo.nloc:
+        """Sparse-push row lists of one batch (see exchange_row_needs); kept only when
+        they save at least 10% of the full-block push."""
+        recv, off = exchange_row_needs(geo.csr.col[:geo.nnz], geo.block, self.rank, self.world, self.pg)
+        if off[-1] <= 0.9 * (self.world - 1) * geo.nloc:
             geo.send_rows = (recv, off)
 
     def _refresh_input_splits(self):  # inputs arrive split (LOAD); nothing to refresh

@@ -62,3 +62,55 @@ def test_trainer_block_layout():
     B = -(-n // world)
     offs = np.minimum(np.arange(world + 1) * B, n)
     assert offs[-1] == n and np.all(np.diff(offs)[:-1] == B) and 0 < offs[-1] - offs[-2] <= B
+
+
+def _needs_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2311_06837_b200.cobatch import exchange_row_needs
+    B = 50
+    rng = np.random.default_rng(rank)
+    cols = torch.from_numpy(rng.integers(0, world * B, 400).astype(np.int32))
+    recv, off = exchange_row_needs(cols, B, rank, world, dist.group.WORLD)
+    allcols = [None] * world
+    dist.all_gather_object(allcols, cols.numpy())
+    # what each peer reads from my block, computed here from its columns
+    exp = []
+    for p in range(world):
+        if p == rank:
+            continue
+        c = allcols[p]
+        exp.append(np.unique(c[(c >= rank * B) & (c < (rank + 1) * B)]) - rank * B)
+    got = [recv[off[i]:off[i + 1]].numpy() for i in range(world - 1)]
+    q.put((rank, all(np.array_equal(a, b) for a, b in zip(got, exp)), off))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sparse_push_row_lists_gloo(world):
+    """The cooperative-batch sparse push's row lists (all_to_all of per-source needs)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_needs_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+
+
+def test_kernel_selection_helpers():
+    from paper_2311_06837_b200.train import AGG_ROWS, _splitk_eff, agg_variant
+    assert agg_variant(64, 114_624_474, 232_965) == 0          # Reddit 64-wide: warp per row
+    assert agg_variant(48, 114_624_474, 232_965) == AGG_ROWS   # 48-wide rows
+    assert agg_variant(64, 15_600_000, 6_000_000) == AGG_ROWS  # cobatch: 2.6 edges per row
+    for sk, k in [(96, 232965), (296, 100), (7, 64), (5, 0), (300, 6_000_000)]:
+        e = _splitk_eff(sk, k)
+        kb = -(-k // 64)
+        assert 1 <= e <= max(1, min(sk, kb))
+        if kb > 1:
+            per = -(-kb // e)
+            assert (e - 1) * per < kb           # no empty split
