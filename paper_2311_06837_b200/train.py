@@ -97,6 +97,14 @@ def agg_width(fout: int, rows: int) -> int:
 AGG_ROWS = 1  # gdx.h GDX_AGG_ROWS
 
 
+class _nullctx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
+
+
 def source_bounds(row_ptr: torch.Tensor, col: torch.Tensor, rows: int, block: int, world: int,
                   device) -> list:
     """Per-row start of each source rank's column block [q*block, (q+1)*block) in a CSR
@@ -617,9 +625,15 @@ class FullGraphTrainer:
             # (K = the rows that fed layer l; rows past them carry no gradient)
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
             sk = _splitk_eff(L.split_k, r_in)
-            gemm_tn(L.G.rows_view(r_in), A_in.rows_view(r_in), c0=L.ws, split_k=sk, a_mn=True,
-                    b_mn=True)
-            self._sgd_or_reduce(L, sk, L.upd_cols)
+            ws = self._wstream()
+            if ws is not None:  # overlap with the next layer's (L2-bound) aggregation
+                ws.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(ws) if ws is not None else _nullctx():
+                gemm_tn(L.G.rows_view(r_in), A_in.rows_view(r_in), c0=L.ws, split_k=sk, a_mn=True,
+                        b_mn=True)
+                self._sgd_or_reduce(L, sk, L.upd_cols)
+        if getattr(self, "_ws", None) is not None:
+            torch.cuda.current_stream().wait_stream(self._ws)
         if self.world > 1:
             # one all-reduce for every layer's dW and the loss, then SGD (+ split refresh)
             self.grad_flat[-1:].copy_(self.loss_acc)
@@ -628,6 +642,14 @@ class FullGraphTrainer:
             for L in self.layers:
                 call("gdx_splitk_reduce", L.dW.data_ptr(), 1, 0, L.nz, L.upd_cols, L.fin_ld, None,
                      L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(), L.Wsp.lo.data_ptr(), stream_handle())
+
+    def _wstream(self):
+        """Side stream for the weight-gradient GEMMs (GDX_DW_OVERLAP=1), else None."""
+        if os.environ.get("GDX_DW_OVERLAP", "0") == "0":
+            return None
+        if getattr(self, "_ws", None) is None:
+            self._ws = torch.cuda.Stream(device=self.d)
+        return self._ws
 
     def _sgd_or_reduce(self, L, sk: int, cols: int):
         """Reduce layer L's split-K partials into dW; on one GPU also apply SGD (and
