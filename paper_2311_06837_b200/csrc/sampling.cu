@@ -276,15 +276,21 @@ __global__ void gather_split_rows_kernel(const uint16_t* __restrict__ src_hi,
                                          const uint32_t* __restrict__ idx, uint32_t rows,
                                          uint32_t vecs, uint16_t* __restrict__ out_hi,
                                          uint16_t* __restrict__ out_lo, uint64_t ld_out) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
-        const uint64_t so = static_cast<uint64_t>(idx[r]) * ld_src, oo = static_cast<uint64_t>(r) * ld_out;
+    // a group of `vecs` lanes per row (32/vecs rows per warp when a row is <= 16 vectors)
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t rpw = vecs >= 32 ? 1 : 32 / vecs;
+    const uint32_t sub = vecs >= 32 ? 0 : lane / vecs;
+    const uint32_t v0 = vecs >= 32 ? lane : lane - sub * vecs;
+    if (sub >= rpw) return;
+    const uint64_t groups = static_cast<uint64_t>((gridDim.x * blockDim.x) >> 5) * rpw;
+    for (uint64_t r = static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * rpw + sub; r < rows;
+         r += groups) {
+        const uint64_t so = static_cast<uint64_t>(idx[r]) * ld_src, oo = r * ld_out;
         const uint4* sh = reinterpret_cast<const uint4*>(src_hi + so);
         const uint4* sl = reinterpret_cast<const uint4*>(src_lo + so);
         uint4* dh = reinterpret_cast<uint4*>(out_hi + oo);
         uint4* dl = reinterpret_cast<uint4*>(out_lo + oo);
-        for (uint32_t v = lane; v < vecs; v += 32) {
+        for (uint32_t v = v0; v < vecs; v += 32) {
             const uint4 a = __ldg(sh + v), b = __ldg(sl + v);
             dh[v] = a;
             dl[v] = b;

@@ -199,11 +199,13 @@ def test_labels_bit_exact(cuda):
     assert np.array_equal(out.cpu().numpy(), O.make_labels(5000, 41, 11))
 
 
-def test_gemm_mask_epilogue_fused_backward(gdx, cuda):
-    """dH GEMM epilogue of the trainer: ReLU-backward mask, unscaled split copy, row scale."""
+@pytest.mark.parametrize("m", [517, 1_100_003])
+def test_gemm_mask_epilogue_fused_backward(gdx, cuda, m):
+    """dH GEMM epilogue of the trainer: ReLU-backward mask, unscaled split copy, row scale
+    (m >= 1M takes the smem-staged, row-contiguous epilogue)."""
     import torch
     rng = np.random.default_rng(11)
-    m, n, k = 517, 64, 96
+    n, k = 64, 96
     g = rng.uniform(-1, 1, (m, k))
     w = rng.uniform(-1, 1, (k, n))          # stored [k][n]: MN-major B
     mask = rng.uniform(-1, 1, (m, n)).astype(np.float32)
@@ -214,10 +216,35 @@ def test_gemm_mask_epilogue_fused_backward(gdx, cuda):
     gdx.gemm_tn(A, B, c0=out, b_mn=True, mask=torch.from_numpy(mask).to(cuda),
                 row_scale=torch.from_numpy(scale).to(cuda), out_split=sp, split_unscaled=True)
     torch.cuda.synchronize()
-    dh = g.astype(np.float32).astype(np.float64) @ w.astype(np.float32).astype(np.float64)
-    gref = np.where(mask > 0, dh, 0.0)
-    close(sp.to_float().double().cpu().numpy(), gref)
-    close(out[:m, :n].double().cpu().numpy(), gref * scale[:, None])
+    rows = np.unique(np.concatenate([rng.integers(0, m, 4000), np.arange(max(0, m - 300), m)]))
+    dh = g[rows].astype(np.float32).astype(np.float64) @ w.astype(np.float32).astype(np.float64)
+    gref = np.where(mask[rows] > 0, dh, 0.0)
+    ri = torch.from_numpy(rows).to(cuda)
+    close(sp.to_float()[ri].double().cpu().numpy(), gref)
+    close(out[ri, :n].double().cpu().numpy(), gref * scale[rows, None])
+
+
+@pytest.mark.parametrize("relu", [False, True])
+def test_gemm_staged_split_outputs(gdx, cuda, relu):
+    """Long forward GEMM (staged epilogue): c0/c1 column split + scaled split copy."""
+    import torch
+    rng = np.random.default_rng(5)
+    m, n, k, split = 1_050_001, 128, 64, 64
+    a = rng.uniform(-1, 1, (m, k))
+    b = rng.uniform(-1, 1, (n, k))
+    A, B = _split(gdx, a, cuda), _split(gdx, b, cuda)
+    c0, c1 = gdx.dense(m, split, cuda), gdx.dense(m, n - split, cuda)
+    sp = gdx.Split(m, n, cuda)
+    gdx.gemm_tn(A, B, c0=c0, c1=c1, split=split, relu=relu, out_split=sp)
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([rng.integers(0, m, 4000), np.arange(m - 200, m)]))
+    ref = a[rows].astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T
+    if relu:
+        ref = np.maximum(ref, 0)
+    ri = torch.from_numpy(rows).to(cuda)
+    close(c0[ri, :split].double().cpu().numpy(), ref[:, :split])
+    close(c1[ri, :n - split].double().cpu().numpy(), ref[:, split:])
+    close(sp.to_float()[ri].double().cpu().numpy(), ref)
 
 
 @pytest.mark.parametrize("width", [64, 30])

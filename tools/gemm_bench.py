@@ -29,6 +29,8 @@ SHAPES = [
     ("papers cobatch L3 fwd", 6000000, 384, 64, 0, 0, 1),
     ("papers cobatch dH L3", 6000000, 64, 384, 0, 1, 1),
     ("papers cobatch dW L3", 384, 64, 6000000, 1, 1, 296),
+    ("papers cobatch dH L2 fused(mask,scale,split)", 6000000, 64, 128, 0, 1, -1),
+    ("products dH fused(mask,scale,split)", 2449029, 64, 64, 0, 1, -1),
 ]
 
 
