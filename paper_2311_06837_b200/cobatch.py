@@ -222,6 +222,7 @@ class CobatchTrainer(FullGraphTrainer):
         self.n, self.F = n, cfg.dims[0]
         F = self.F
         self.subgraph_mode = False
+        self.is_cobatch = True
         self.plan = plan
         # the resident feature store (every vertex, split bf16) and labels: the
         # preloaded inputs each batch LOADs its rows from

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--n", type=int, default=232965)
     ap.add_argument("--degree", type=float, default=491.99)
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--slices", default="", help="also time row slices [0, r) (multi-GPU shard sizes)")
     args = ap.parse_args()
     import torch
     import paper_2311_06837_b200 as G
@@ -50,6 +51,23 @@ def main():
             res.append({"n": n, "deg": args.degree, "width": w, "variant": variant, "ms": round(ms, 4),
                         "gedges_per_s": round(nnz / ms / 1e6, 2),
                         "alg_GBps": round(alg / ms / 1e6, 1)})
+    for r in [int(x) for x in args.slices.split(",") if x]:
+        w = 64
+        src = torch.randn(n, w, device=d)
+        out = dense(r, w, d)
+        sub = dg.slice_rows(0, r)
+        nnz_r = int(sub.row_ptr[-1].item() - sub.row_ptr[0].item())
+        for _ in range(3):
+            aggregate(sub, src, w, out=out, self_coef=1.0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.reps):
+            aggregate(sub, src, w, out=out, self_coef=1.0)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.reps
+        res.append({"slice_rows": r, "nnz": nnz_r, "ms": round(ms, 4), "gedges_per_s": round(nnz_r / ms / 1e6, 2)})
     if args.no_probe:
         print(json.dumps(res))
         return
