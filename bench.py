@@ -75,6 +75,23 @@ def parse():
     return ap.parse_args()
 
 
+def bind_numa(local: int) -> list:
+    """Pin this rank to the CPUs of its GPU's NUMA node (NVML affinity), so the pinned
+    host buffers of the end-to-end feature stream are allocated (first touch) next to
+    the GPU's PCIe root.  Returns the CPU list (empty if NVML is unavailable)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = [64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1]
+        if cpus and os.environ.get("GDX_NUMA_BIND", "1") != "0":
+            os.sched_setaffinity(0, cpus)
+        return cpus
+    except Exception:
+        return []
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -405,6 +422,8 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        bind_numa(local)
     pg = None
     if world > 1:
         opts = dist.ProcessGroupNCCL.Options()
