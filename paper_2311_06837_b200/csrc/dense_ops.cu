@@ -350,6 +350,96 @@ extern "C" int gdx_grad_prepare(const float* dH, uint64_t ld_dh, const float* H,
     return check_launch("gdx_grad_prepare");
 }
 
+// Vector form for classes <= 4*GL: GL lanes per row (32/GL rows per warp), 4 logits
+// per lane held in registers, group-local shuffles; float4 / ushort4 stores.  Padding
+// columns (classes .. 4*GL) get g = 0.
+template <int GL>
+__global__ void __launch_bounds__(256) softmax_xent_vec(const float* __restrict__ logits, uint64_t ld,
+                                                        uint32_t rows, uint32_t classes,
+                                                        const int32_t* __restrict__ labels, float inv_count,
+                                                        const float* __restrict__ row_scale, float* gs,
+                                                        uint64_t ld_gs, uint16_t* g_hi, uint16_t* g_lo,
+                                                        uint64_t ld_g, uint32_t out_cols, double* loss_sum) {
+    constexpr int RPW = 32 / GL;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / GL, gl = lane - sub * GL;
+    const uint32_t c0 = 4 * gl;
+    const unsigned gmask = (GL == 32) ? 0xffffffffu : (((1u << GL) - 1u) << (sub * GL));
+    const uint64_t groups = static_cast<uint64_t>((gridDim.x * blockDim.x) >> 5) * RPW;
+    double local = 0.0;
+    for (uint64_t r = static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RPW + sub; r < rows;
+         r += groups) {
+        float z[4];
+        const float* zr = logits + r * ld;
+        if (c0 + 4 <= classes) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(zr + c0));
+            z[0] = q.x; z[1] = q.y; z[2] = q.z; z[3] = q.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) z[j] = (c0 + j < classes) ? zr[c0 + j] : -INFINITY;
+        }
+        float mx = fmaxf(fmaxf(z[0], z[1]), fmaxf(z[2], z[3]));
+#pragma unroll
+        for (int o = GL / 2; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, o));
+        float e[4], sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            e[j] = (c0 + j < classes) ? expf(z[j] - mx) : 0.f;
+            sum += e[j];
+        }
+#pragma unroll
+        for (int o = GL / 2; o; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o);
+        const float inv = 1.f / sum;
+        const int32_t y = labels[r];
+        const float rs = row_scale ? row_scale[r] : 1.f;
+        float g[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            g[j] = (c0 + j < classes) ? (e[j] * inv - (static_cast<int32_t>(c0 + j) == y ? 1.f : 0.f)) * inv_count
+                                      : 0.f;
+        if (c0 < out_cols) {
+            if (gs)
+                *reinterpret_cast<float4*>(gs + r * ld_gs + c0) = make_float4(g[0] * rs, g[1] * rs, g[2] * rs, g[3] * rs);
+            if (g_hi) {
+                ushort4 hh, ll;
+                split_bf16(g[0], hh.x, ll.x);
+                split_bf16(g[1], hh.y, ll.y);
+                split_bf16(g[2], hh.z, ll.z);
+                split_bf16(g[3], hh.w, ll.w);
+                *reinterpret_cast<ushort4*>(g_hi + r * ld_g + c0) = hh;
+                *reinterpret_cast<ushort4*>(g_lo + r * ld_g + c0) = ll;
+            }
+        }
+        // loss: lse - z[y], by the lane holding column y
+        if (static_cast<uint32_t>(y) >= c0 && static_cast<uint32_t>(y) < c0 + 4)
+            local += static_cast<double>(mx + logf(sum) - z[y - c0]);
+    }
+    if (local != 0.0) atomicAdd(loss_sum, local);
+}
+
+// launches the vector form when the shapes allow; returns false otherwise
+bool softmax_vec_launch(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes, const int32_t* labels,
+                        float inv_count, float* dlogits, const float* row_scale, float* gs, uint64_t ld_gs,
+                        uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g, double* loss_sum, uint32_t npeers,
+                        cudaStream_t st) {
+    auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    auto a8 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 7) == 0; };
+    if (dlogits || npeers || classes > 128 || ld % 4 || !a16(logits)) return false;
+    const uint32_t cols = (classes + 3) / 4 * 4;  // whole float4 groups written
+    if (gs && (ld_gs % 4 || !a16(gs) || ld_gs < cols)) return false;
+    if (g_hi && (ld_g % 4 || !a8(g_hi) || !a8(g_lo) || ld_g < cols)) return false;
+    const uint64_t rpb = classes <= 64 ? 16 : 8;  // rows per 256-thread block
+    uint64_t blocks = (static_cast<uint64_t>(rows) + rpb - 1) / rpb;
+    if (blocks > 65535ull * 32) blocks = 65535ull * 32;
+    if (classes <= 64)
+        softmax_xent_vec<16><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+            logits, ld, rows, classes, labels, inv_count, row_scale, gs, ld_gs, g_hi, g_lo, ld_g, cols, loss_sum);
+    else
+        softmax_xent_vec<32><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+            logits, ld, rows, classes, labels, inv_count, row_scale, gs, ld_gs, g_hi, g_lo, ld_g, cols, loss_sum);
+    return true;
+}
+
 extern "C" int gdx_softmax_xent(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
                                 const int32_t* labels, float inv_count, float* dlogits,
                                 uint64_t ld_d, double* loss_sum, gdx_stream stream) {
@@ -373,10 +463,13 @@ extern "C" int gdx_softmax_xent_fused(const float* logits, uint64_t ld, uint32_t
     GDX_REQUIRE(!g_hi == !g_lo, GDX_INPUT, "gdx_softmax_xent_fused: g_hi/g_lo must pair");
     GDX_REQUIRE(classes >= 1, GDX_INPUT, "gdx_softmax_xent_fused: classes must be >= 1");
     if (!rows) return GDX_OK;
-    const uint64_t threads = static_cast<uint64_t>(rows) * 32;
-    softmax_xent_kernel<<<grid_for(threads), 256, 0, as_cuda(stream)>>>(
-        logits, ld, rows, classes, labels, inv_count, dlogits, ld_d, row_scale, gs, ld_gs, g_hi, g_lo,
-        ld_g, loss_sum, PeerDeltas{});
+    if (!softmax_vec_launch(logits, ld, rows, classes, labels, inv_count, dlogits, row_scale, gs, ld_gs, g_hi,
+                            g_lo, ld_g, loss_sum, 0, as_cuda(stream))) {
+        const uint64_t threads = static_cast<uint64_t>(rows) * 32;
+        softmax_xent_kernel<<<grid_for(threads), 256, 0, as_cuda(stream)>>>(
+            logits, ld, rows, classes, labels, inv_count, dlogits, ld_d, row_scale, gs, ld_gs, g_hi, g_lo,
+            ld_g, loss_sum, PeerDeltas{});
+    }
     note_launch();
     return check_launch("gdx_softmax_xent_fused");
 }

@@ -286,3 +286,37 @@ def test_gather_split_rows_exact(gdx, cuda):
     b = out.hi.view(777, out.ld).cpu().numpy()
     assert np.array_equal(a, b)
     assert np.array_equal(src.lo.view(5000, src.ld)[I.long()].cpu().numpy(), out.lo.view(777, out.ld).cpu().numpy())
+
+
+@pytest.mark.parametrize("classes,ld", [(1, 8), (8, 8), (41, 48), (47, 64), (64, 64), (72, 72),
+                                        (128, 128), (172, 176)])
+def test_softmax_xent_fused(gdx, cuda, classes, ld):
+    """Fused loss head: loss sum, g = (softmax - onehot)/count as split copy and as
+    gs = g * row_scale (vector form up to 128 classes, warp form beyond)."""
+    import torch
+    from paper_2311_06837_b200._lib import call
+    rng = np.random.default_rng(classes)
+    n = 3001
+    z = rng.normal(0, 2, (n, classes)).astype(np.float32)
+    y = rng.integers(0, classes, n).astype(np.int32)
+    sc = rng.uniform(0.5, 2, n).astype(np.float32)
+    Z = torch.zeros(n, ld, device=cuda)
+    Z[:, :classes] = torch.from_numpy(z).to(cuda)
+    Y, S = torch.from_numpy(y).to(cuda), torch.from_numpy(sc).to(cuda)
+    gs = torch.zeros(n, ld, device=cuda)
+    sp = gdx.Split(n, ld, cuda)
+    loss = torch.zeros(1, dtype=torch.float64, device=cuda)
+    call("gdx_softmax_xent_fused", Z.data_ptr(), ld, n, classes, Y.data_ptr(), 1.0 / n, None, 0, S.data_ptr(),
+         gs.data_ptr(), ld, sp.hi.data_ptr(), sp.lo.data_ptr(), sp.ld, loss.data_ptr(), gdx.stream_handle())
+    torch.cuda.synchronize()
+    zd = z.astype(np.float64)
+    m = zd.max(1, keepdims=True)
+    lse = m[:, 0] + np.log(np.exp(zd - m).sum(1))
+    p = np.exp(zd - lse[:, None])
+    g = p.copy()
+    g[np.arange(n), y] -= 1.0
+    g /= n
+    assert abs(float(loss.item()) - float((lse - zd[np.arange(n), y]).sum())) <= 1e-4 * n
+    close(sp.to_float()[:, :classes].double().cpu().numpy(), g)
+    close(gs[:, :classes].double().cpu().numpy(), g * sc[:, None])
+    assert float(gs[:, classes:].abs().max().item() if ld > classes else 0.0) == 0.0
