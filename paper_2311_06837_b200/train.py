@@ -531,9 +531,6 @@ class FullGraphTrainer:
                          partial=P, npartial=2 * S, partial_stride=n * P.stride(0), **epi)
 
     # ---- collectives ----
-    def _allgather_rows(self, full: torch.Tensor):
-        self.exchange.allgather_rows(full)
-
     def _allreduce(self, t: torch.Tensor):
         """Gradient all-reduce over every rank (both modes)."""
         if self.world > 1:
@@ -812,10 +809,6 @@ class FullGraphTrainer:
         if sync_loss:
             return float(self.loss_acc.item()) / self.loss_count
         return None
-
-    def aggregation_edges_per_epoch(self) -> int:
-        """Edges aggregated by this rank in one epoch: L forward + L backward passes."""
-        return 2 * self.cfg.layers * self.nnz_local
 
 
 class FeatureStream:
