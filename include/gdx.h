@@ -101,8 +101,6 @@ typedef struct gdx_aggregate_args {
     uint16_t* out_hi;         /* nullable split-bf16 copy [rows x ld_split] */
     uint16_t* out_lo;
     uint64_t ld_split;
-    uint32_t npartial;        /* partial slices added (0 = 1): partial + s*partial_stride, s < npartial */
-    uint64_t partial_stride;  /* elements between partial slices */
 } gdx_aggregate_args;
 int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream);
 /* seg_lo[v], seg_hi[v] = sub-range of row v's (sorted) column ids inside [lo, hi). */

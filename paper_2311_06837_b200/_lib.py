@@ -27,7 +27,6 @@ class AggregateArgs(C.Structure):
         ("src", vp), ("ld_src", u64), ("self_coef", C.c_float), ("self_base", u64),
         ("post_scale", vp), ("add", vp), ("ld_add", u64), ("relu", C.c_int),
         ("out", vp), ("ld_out", u64), ("out_hi", vp), ("out_lo", vp), ("ld_split", u64),
-        ("npartial", u32), ("partial_stride", u64),
     ]
 
 

@@ -86,27 +86,9 @@ struct AggParams {
     uint16_t* out_hi;
     uint16_t* out_lo;
     uint64_t ld_split;
-    uint32_t npartial;
-    uint64_t partial_stride;
 };
 
-// sum of the partial slices of one float4 column group
-__device__ __forceinline__ float4 partial_sum4(const AggParams& p, uint64_t row, uint32_t ch);
-
 constexpr int pow2_floor(int x) { return x >= 32 ? 32 : x >= 16 ? 16 : x >= 8 ? 8 : x >= 4 ? 4 : x >= 2 ? 2 : 1; }
-
-__device__ __forceinline__ float4 partial_sum4(const AggParams& p, uint64_t row, uint32_t ch) {
-    const float* q = p.partial + row * p.ld_partial + 4 * ch;
-    float4 r = ld_plain4(q);
-    for (uint32_t s = 1; s < p.npartial; ++s) {
-        const float4 t = ld_plain4(q + s * p.partial_stride);
-        r.x += t.x;
-        r.y += t.y;
-        r.z += t.z;
-        r.w += t.w;
-    }
-    return r;
-}
 
 // LPE lanes cover one neighbour row (NCH float4 chunks each); EPW = pow2 rows per
 // warp step; EXACT: c4 == LPE*NCH (no column masks).
@@ -140,9 +122,9 @@ __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
         const int nseg = p.skip_lo ? 2 : 1;
         for (int seg = 0; seg < nseg; ++seg) {
         uint64_t sbeg = beg, send = end;
-        if (p.skip_lo) {  // pieces of a row may start or end inside the skipped range
-            if (seg == 0) send = min(end, p.skip_lo[row]);
-            else sbeg = max(beg, p.skip_hi[row]);
+        if (p.skip_lo) {
+            if (seg == 0) send = p.skip_lo[row];
+            else sbeg = p.skip_hi[row];
         }
         // index chunks of 32 are software-pipelined: chunk k+1's column ids are in
         // flight while chunk k's rows are gathered.
@@ -200,7 +182,7 @@ __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
             if (!chan_on[c]) continue;
             float4 r = acc[c];
             if (p.partial) {
-                const float4 q = partial_sum4(p, row, ch);
+                const float4 q = ld_plain4(p.partial + row * p.ld_partial + 4 * ch);
                 r.x += q.x;
                 r.y += q.y;
                 r.z += q.z;
@@ -277,8 +259,8 @@ __global__ void __launch_bounds__(256) aggregate_rows(const AggParams p) {
         for (int seg = 0; seg < nseg; ++seg) {
             uint64_t e = beg, send = end;
             if (p.skip_lo) {
-                if (seg == 0) send = min(end, p.skip_lo[row]);
-                else e = max(beg, p.skip_hi[row]);
+                if (seg == 0) send = p.skip_lo[row];
+                else e = p.skip_hi[row];
             }
             for (; e + UNROLL <= send; e += UNROLL) {
                 uint32_t nb[UNROLL];
@@ -312,7 +294,7 @@ __global__ void __launch_bounds__(256) aggregate_rows(const AggParams p) {
             if (!chan_on[c]) continue;
             float4 rr = acc[c];
             if (p.partial) {
-                const float4 q = partial_sum4(p, row, ch);
+                const float4 q = ld_plain4(p.partial + row * p.ld_partial + 4 * ch);
                 rr.x += q.x;
                 rr.y += q.y;
                 rr.z += q.z;
@@ -364,16 +346,14 @@ __global__ void __launch_bounds__(256) aggregate_scalar(const AggParams p, uint3
          row += warps_total) {
         const uint64_t beg = p.row_ptr[row];
         const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
-        const uint64_t s0 = p.skip_lo ? min(end, p.skip_lo[row]) : end,
-                       s1 = p.skip_hi ? max(beg, p.skip_hi[row]) : end;
+        const uint64_t s0 = p.skip_lo ? p.skip_lo[row] : end, s1 = p.skip_hi ? p.skip_hi[row] : end;
         const float scale = p.post_scale ? p.post_scale[row] : 1.f;
         for (uint32_t c = lane; c < width; c += 32) {
             float acc = p.self_coef != 0.f ? p.self_coef * p.src[(p.self_base + row) * p.ld_src + c]
                                            : 0.f;
             for (uint64_t e = beg; e < s0; ++e) acc += p.src[static_cast<uint64_t>(p.col[e]) * p.ld_src + c];
             for (uint64_t e = s1; e < end; ++e) acc += p.src[static_cast<uint64_t>(p.col[e]) * p.ld_src + c];
-            if (p.partial)
-                for (uint32_t s = 0; s < p.npartial; ++s) acc += p.partial[row * p.ld_partial + s * p.partial_stride + c];
+            if (p.partial) acc += p.partial[row * p.ld_partial + c];
             acc *= scale;
             if (p.add) acc += p.add[row * p.ld_add + c];
             if (p.relu) acc = fmaxf(acc, 0.f);
@@ -504,13 +484,10 @@ int aggregate_impl(const gdx_aggregate_args* a, int variant, gdx_stream stream) 
     if (a->rows == 0) return GDX_OK;
     GDX_REQUIRE(!a->skip_lo == !a->skip_hi, GDX_INPUT, "gdx_aggregate: skip_lo/skip_hi must pair");
     GDX_REQUIRE(!a->partial || a->ld_partial >= a->width, GDX_INPUT, "gdx_aggregate: ld_partial < width");
-    GDX_REQUIRE(!a->partial || a->npartial <= 1 || a->partial_stride % 4 == 0 || a->width % 4 != 0, GDX_INPUT,
-                "gdx_aggregate: partial_stride must keep 16-byte alignment");
     AggParams p{a->row_ptr, a->row_end, a->skip_lo, a->skip_hi, a->partial, a->ld_partial, a->col,
                 a->rows, a->width / 4, a->src, a->ld_src,
                 static_cast<uint32_t>(a->ld_src * 4), a->self_coef, a->self_base, a->post_scale,
-                a->add, a->ld_add, a->relu, a->out, a->ld_out, a->out_hi, a->out_lo, a->ld_split,
-                a->npartial ? a->npartial : 1u, a->partial_stride};
+                a->add, a->ld_add, a->relu, a->out, a->ld_out, a->out_hi, a->out_lo, a->ld_split};
     const bool vec = a->width % 4 == 0 && a->ld_src % 4 == 0 && aligned16(a->src) && a->width <= 4096 &&
                      a->ld_src * 4 < (1ull << 32) &&
                      (!a->add || (a->ld_add % 4 == 0 && aligned16(a->add))) &&

@@ -414,7 +414,9 @@ __global__ void __launch_bounds__(256) softmax_xent_vec(const float* __restrict_
         if (static_cast<uint32_t>(y) >= c0 && static_cast<uint32_t>(y) < c0 + 4)
             local += static_cast<double>(mx + logf(sum) - z[y - c0]);
     }
-    if (local != 0.0) atomicAdd(loss_sum, local);
+    // one atomic per warp (per-row atomics on one address serialise)
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if (lane == 0 && local != 0.0) atomicAdd(loss_sum, local);
 }
 
 // launches the vector form when the shapes allow; returns false otherwise
@@ -428,9 +430,11 @@ bool softmax_vec_launch(const float* logits, uint64_t ld, uint32_t rows, uint32_
     const uint32_t cols = (classes + 3) / 4 * 4;  // whole float4 groups written
     if (gs && (ld_gs % 4 || !a16(gs) || ld_gs < cols)) return false;
     if (g_hi && (ld_g % 4 || !a8(g_hi) || !a8(g_lo) || ld_g < cols)) return false;
-    const uint64_t rpb = classes <= 64 ? 16 : 8;  // rows per 256-thread block
+    const uint64_t rpb = classes <= 64 ? 16 : 8;  // rows per 256-thread block and step
+    // grid-stride with a bounded grid: the loss is one fp64 atomic per warp, and
+    // ~10^6 atomics on one address would serialise
     uint64_t blocks = (static_cast<uint64_t>(rows) + rpb - 1) / rpb;
-    if (blocks > 65535ull * 32) blocks = 65535ull * 32;
+    if (blocks > static_cast<uint64_t>(kNumSMs) * 8) blocks = static_cast<uint64_t>(kNumSMs) * 8;
     if (classes <= 64)
         softmax_xent_vec<16><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
             logits, ld, rows, classes, labels, inv_count, row_scale, gs, ld_gs, g_hi, g_lo, ld_g, cols, loss_sum);

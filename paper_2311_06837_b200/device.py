@@ -102,8 +102,7 @@ def dense(rows: int, cols: int, device, zero: bool = True) -> torch.Tensor:
 
 def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_split: Split | None = None,
               self_coef: float = 0.0, self_base: int = 0, post_scale=None, add=None, relu=False,
-              row_end=None, row_begin=None, skip=None, partial=None, npartial: int = 1,
-              partial_stride: int = 0, stream=None, variant: int = 0):
+              row_end=None, row_begin=None, skip=None, partial=None, stream=None, variant: int = 0):
     """K1/K3 (see include/gdx.h gdx_aggregate).  row_begin/row_end override the CSR
     row bounds; skip = (seg_lo, seg_hi) excludes a per-row sub-range; partial adds
     precomputed partial sums before the epilogue."""
@@ -115,7 +114,6 @@ def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_spli
         a.skip_lo, a.skip_hi = skip[0].data_ptr(), skip[1].data_ptr()
     if partial is not None:
         a.partial, a.ld_partial = partial.data_ptr(), partial.stride(0)
-        a.npartial, a.partial_stride = npartial, partial_stride
     a.col = g.col.data_ptr()
     a.rows = g.rows
     a.width = width

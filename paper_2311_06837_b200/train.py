@@ -400,10 +400,7 @@ class FullGraphTrainer:
         if weights is None:
             weights = init_weights(cfg, weight_seed)
         self.set_weights(weights)
-        self.pieces = self._build_pieces() if (self.overlap and not self.subgraph_mode and
-                                               not getattr(self, "is_cobatch", False)) else None
-        prow = self.nloc * (2 * self.pieces["S"] if self.pieces else 1)
-        self.partial = dense(prow, max(L.w for L in self.layers), d) if self.overlap else None
+        self.partial = dense(self.nloc, max(L.w for L in self.layers), d) if self.overlap else None
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=d)
         self.keep_activations = False
         self.activations = []
@@ -486,8 +483,6 @@ class FullGraphTrainer:
                               row_end=b[q + 1], partial=P, **epi)
             self.p2p.join()
             return None
-        if self.pieces is not None and csr.rows == self.nloc:
-            return self._pieces_aggregate(csr, full, width, epi)
         if self.p2p is not None:
             # the producer already pushed our rows into every peer and signalled;
             # aggregate the owned sources, wait for the peers' rows, finish the rest
@@ -505,30 +500,6 @@ class FullGraphTrainer:
         self._agg(csr, full, width, out=P, row_begin=self.seg_lo, row_end=self.seg_hi)
         work.wait()
         return self._agg(csr, full, width, skip=(self.seg_lo, self.seg_hi), partial=P, **epi)
-
-    def _pieces_aggregate(self, csr, full, width, epi):
-        """Split aggregation over edge pieces (see _build_pieces): local pieces while the
-        rows move, remote pieces after the wait, then the epilogue pass over 2S slices."""
-        pc, n = self.pieces, self.nloc
-        S = pc["S"]
-        P = self.partial[:, :pad4(width)] if self.partial.shape[1] != pad4(width) else self.partial
-        vc = pc["csr_v"]
-        work = None
-        if self.p2p is None:
-            work = self.exchange.allgather_rows_async(full)
-        nl = self.nnz_local_src
-        self._agg(vc, full, width, nnz_hint=nl, variant=agg_variant(width, nl, S * n), out=P[:S * n],
-                  row_begin=pc["lb"], row_end=pc["le"])
-        if self.p2p is not None:
-            self.p2p.wait()
-        elif work is not None:
-            work.wait()
-        nr = self.nnz_local - nl
-        self._agg(vc, full, width, nnz_hint=nr, variant=agg_variant(width, nr, S * n), out=P[S * n:2 * S * n],
-                  row_begin=pc["rb"], row_end=pc["re"], skip=(pc["slo"], pc["shi"]))
-        rp = csr.row_ptr
-        return self._agg(csr, full, width, nnz_hint=0, variant=AGG_ROWS, row_begin=rp, row_end=rp,
-                         partial=P, npartial=2 * S, partial_stride=n * P.stride(0), **epi)
 
     # ---- collectives ----
     def _allreduce(self, t: torch.Tensor):
@@ -668,41 +639,6 @@ class FullGraphTrainer:
             for L in self.layers:
                 call("gdx_splitk_reduce", L.dW.data_ptr(), 1, 0, L.nz, L.upd_cols, L.fin_ld, None,
                      L.W.data_ptr(), cfg.lr, L.Wsp.hi.data_ptr(), L.Wsp.lo.data_ptr(), stream_handle())
-
-    def _build_pieces(self):
-        """Split every row's local-source range and remote-source range into S equal
-        edge pieces, each aggregated as its own (virtual) row into a partial slice; a
-        final pass adds the 2S slices and applies the epilogue (deterministic order).
-        Motivation: a Reddit shard at N=8 has ~3 rows per resident warp and smaller
-        launches run slower per edge (tools/agg_bench.py --slices: 75.8 G edges/s at
-        233 K rows, 65.2 at 29 K)."""
-        # opt-in (GDX_AGG_PIECES=S): measured slower at N=2/4 (Reddit 6.20 vs 5.77 ms,
-        # 3.81 vs 3.18 ms; products N=4 11.0 vs 10.1 ms) -- the partial-slice traffic and
-        # the extra short virtual rows cost more than the last-wave loss they remove
-        S = int(os.environ.get("GDX_AGG_PIECES", "1"))
-        if S <= 1:
-            return None
-        d, n = self.d, self.nloc
-        rp = self.csr.row_ptr[:n + 1]
-        beg, end = rp[:-1], rp[1:]
-        lo, hi = self.seg_lo[:n], self.seg_hi[:n]
-        s = torch.arange(S, device=d, dtype=torch.int64)[:, None]
-        L = (hi - lo)[None, :]
-        lb = (lo[None, :] + (L * s) // S).reshape(-1).contiguous()
-        le = (lo[None, :] + (L * (s + 1)) // S).reshape(-1).contiguous()
-        left = (lo - beg)[None, :]
-        R = left + (end - hi)[None, :]
-        t0, t1 = (R * s) // S, (R * (s + 1)) // S
-
-        def emap(t):
-            return torch.where(t < left, beg[None, :] + t, hi[None, :] + (t - left))
-        rb = emap(t0)
-        re = torch.where(t1 > t0, emap(t1 - 1) + 1, rb)
-        return {"S": S, "lb": lb, "le": le, "rb": rb.reshape(-1).contiguous(),
-                "re": re.reshape(-1).contiguous(),
-                "slo": lo[None, :].expand(S, n).reshape(-1).contiguous(),
-                "shi": hi[None, :].expand(S, n).reshape(-1).contiguous(),
-                "csr_v": DeviceCSR(lb, self.csr.col, S * n)}
 
     def _wstream(self):
         """Side stream for the weight-gradient GEMMs (GDX_DW_OVERLAP=1), else None."""
