@@ -33,8 +33,12 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
-constexpr int kThreads = 320;  // 2 role warps + 8 epilogue warps
-constexpr int kEpiWarps = 8;
+// Epilogue warps per CTA (template EW): 8 = two per 32-lane TMEM quarter, each half the
+// columns, with a 20 KB store-transpose buffer; 16 = four per quarter, no buffer.
+// Measured (tools/gemm_bench.py): 16 warps hide the fused dH epilogue's mask loads
+// (Reddit 0.127 -> 0.092 ms, products 1.10 -> 0.90 ms) but lose on plain stores
+// (products L2 forward 0.28 -> 0.32 ms), so EW = 16 is used when a mask is fused.
+constexpr int kThreadsFor(int ew) { return 64 + 32 * ew; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -168,7 +172,7 @@ struct Epi {
 // (16-byte aligned rows; a quarter-warp's 8 float4 accesses hit distinct bank groups
 // in both the row-per-thread writes and the row-contiguous reads).
 constexpr uint32_t kStgPitch = 20;
-constexpr uint32_t kStgBytes = kEpiWarps * 32 * kStgPitch * 4;  // 20 KB
+constexpr uint32_t kStgBytesFor(int ew) { return ew <= 8 ? ew * 32 * kStgPitch * 4 : 0; }  // 20 KB at 8
 
 // store one float4 locally and, for the exchanged output, into every peer buffer
 __device__ __forceinline__ void store4x(float* p, const float4& v, const Epi& ep, bool xchg) {
@@ -183,12 +187,12 @@ __device__ __forceinline__ void store1x(float* p, float v, const Epi& ep, bool x
         for (uint32_t r = 0; r < ep.npeers; ++r) *reinterpret_cast<float*>(reinterpret_cast<char*>(p) + ep.peer_delta[r]) = v;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EW>
 struct Smem {
     static constexpr uint32_t kA = BM * BK * 2;  // bytes per A operand tile (hi or lo)
     static constexpr uint32_t kB = BN * BK * 2;
     static constexpr uint32_t kStage = 2 * kA + 2 * kB;
-    static constexpr uint32_t kStaging = kStgBytes;  // epilogue store transposes
+    static constexpr uint32_t kStaging = kStgBytesFor(EW);  // epilogue store transposes
     static constexpr uint32_t kBytes = STAGES * kStage + kStaging + 1024 /*align*/ + 512 /*barriers*/;
     static_assert(kBytes <= 232448, "227 KB shared memory per CTA");
 };
@@ -207,12 +211,14 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* ma
     }
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EW>
+__global__ void __launch_bounds__(kThreadsFor(EW), 1)
     gemm_bf16x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                 const Epi ep) {
-    using S = Smem<BN, STAGES>;
+    using S = Smem<BN, STAGES, EW>;
+    constexpr int kEpiWarps = EW;
+    constexpr uint32_t kStgBytes = kStgBytesFor(EW);
     constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -329,8 +335,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
         // ---------------- epilogue warps 2..9 ----------------
         const uint32_t lane_base = 32 * (warp & 3);       // TMEM lanes this warp may access
-        constexpr int kCols = BN / 2;                     // columns per epilogue warp
-        const uint32_t col_base = (warp - 2) / 4 * kCols;  // which half of the tile
+        constexpr int kCols = BN / (kEpiWarps / 4);       // columns per epilogue warp
+        constexpr int kChunk = kCols < 32 ? kCols : 32;   // columns per TMEM load
+        const uint32_t col_base = (warp - 2) / 4 * kCols;  // which part of the tile
         uint32_t tl = 0;
         for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
             uint32_t mt, nt, z;
@@ -343,15 +350,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool row_ok = row < ep.m;
             const float rs = (row_ok && ep.row_scale && ep.split_k <= 1) ? ep.row_scale[row] : 1.f;
 #pragma unroll 1
-            for (int cb = 0; cb < kCols; cb += 32) {
+            for (int cb = 0; cb < kCols; cb += kChunk) {
                 uint32_t raw[32];
-                tmem_ld32_nowait(tmem + (lane_base << 16) + acc * BN + col_base + cb, raw);
+                if constexpr (kChunk == 32) {
+                    tmem_ld32_nowait(tmem + (lane_base << 16) + acc * BN + col_base + cb, raw);
+                } else {
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                        : "=r"(raw[0]), "=r"(raw[1]), "=r"(raw[2]), "=r"(raw[3]), "=r"(raw[4]), "=r"(raw[5]),
+                          "=r"(raw[6]), "=r"(raw[7]), "=r"(raw[8]), "=r"(raw[9]), "=r"(raw[10]), "=r"(raw[11]),
+                          "=r"(raw[12]), "=r"(raw[13]), "=r"(raw[14]), "=r"(raw[15])
+                        : "r"(tmem + (lane_base << 16) + acc * BN + col_base + cb));
+                }
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = has_k ? __uint_as_float(raw[j]) : 0.f;
+                for (int j = 0; j < kChunk; ++j) v[j] = has_k ? __uint_as_float(raw[j]) : 0.f;
 #pragma unroll
-                for (int h = 0; h < 32; h += 16) {
+                for (int h = 0; h < kChunk; h += 16) {
                     const uint32_t col0 = nt * BN + col_base + cb + h;
                     if (col0 >= ep.n) break;  // warp-uniform
                     float* vv = v + h;
@@ -361,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float* fdst = nullptr;
                     uint64_t fld = 0;
                     bool fx = false;
-                    if (ep.stage_stores && ep.split_k <= 1 && col0 + 16 <= ep.n) {
+                    if (kStgBytes && ep.stage_stores && ep.split_k <= 1 && col0 + 16 <= ep.n) {
                         if (col0 + 16 <= ep.split && ep.c0 && ep.ldc0 % 4 == 0) {
                             fdst = ep.c0 + col0;
                             fld = ep.ldc0;
@@ -566,14 +582,14 @@ int operand_maps(CUtensorMap* hi, CUtensorMap* lo, const uint16_t* phi, const ui
 
 int g_num_sms = 0;
 
-template <int BN, int STAGES, bool A_MN, bool B_MN>
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EW>
 int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
     int rc;
     if ((rc = operand_maps(&ma_hi, &ma_lo, g->a_hi, g->a_lo, g->m, g->k, g->lda, A_MN, BM))) return rc;
     if ((rc = operand_maps(&mb_hi, &mb_lo, g->b_hi, g->b_lo, g->n, g->k, g->ldb, B_MN, BN))) return rc;
-    auto kern = gemm_bf16x3<BN, STAGES, A_MN, B_MN>;
-    const int bytes = Smem<BN, STAGES>::kBytes;
+    auto kern = gemm_bf16x3<BN, STAGES, A_MN, B_MN, EW>;
+    const int bytes = Smem<BN, STAGES, EW>::kBytes;
     static bool configured = false;  // per instantiation
     if (!configured) {
         GDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -586,17 +602,24 @@ int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     }
     const uint64_t tiles = static_cast<uint64_t>(ep.m_tiles) * ep.n_tiles * ep.split_k;
     const unsigned grid = static_cast<unsigned>(tiles < static_cast<uint64_t>(g_num_sms) ? tiles : g_num_sms);
-    kern<<<grid, kThreads, bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, ep);
+    kern<<<grid, kThreadsFor(EW), bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, ep);
     note_launch();
     return check_launch("gdx_gemm_tn");
 }
 
+template <int BN, int STAGES, int EW>
+int launch_majors_ew(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
+    if (!g->a_mn_major && !g->b_mn_major) return launch_tc<BN, STAGES, false, false, EW>(g, ep, s);
+    if (g->a_mn_major && g->b_mn_major) return launch_tc<BN, STAGES, true, true, EW>(g, ep, s);
+    if (g->a_mn_major) return launch_tc<BN, STAGES, true, false, EW>(g, ep, s);
+    return launch_tc<BN, STAGES, false, true, EW>(g, ep, s);
+}
+
 template <int BN, int STAGES>
 int launch_majors(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
-    if (!g->a_mn_major && !g->b_mn_major) return launch_tc<BN, STAGES, false, false>(g, ep, s);
-    if (g->a_mn_major && g->b_mn_major) return launch_tc<BN, STAGES, true, true>(g, ep, s);
-    if (g->a_mn_major) return launch_tc<BN, STAGES, true, false>(g, ep, s);
-    return launch_tc<BN, STAGES, false, true>(g, ep, s);
+    // the fused ReLU-backward epilogue (mask loads) runs with 16 epilogue warps
+    if (g->mask && !g->a_mn_major && g->b_mn_major) return launch_tc<BN, STAGES, false, true, 16>(g, ep, s);
+    return launch_majors_ew<BN, STAGES, 8>(g, ep, s);
 }
 
 int validate(const gdx_gemm_args* g) {

@@ -60,7 +60,7 @@ def test_hot_aggregation_registers(frag):
     assert regs and max(regs) <= 40, (frag, regs)
 
 
-@pytest.mark.parametrize("frag", HOT + ["gemm_bf16x3ILi128ELi3ELb0ELb0E", "gemm_bf16x3ILi64ELi4ELb0ELb1E"])
+@pytest.mark.parametrize("frag", HOT + ["gemm_bf16x3ILi128ELi3ELb0ELb0ELi8E", "gemm_bf16x3ILi64ELi4ELb0ELb1ELi16E"])
 def test_hot_kernels_no_local_memory_in_loops(frag):
     n = sum(1 for line in _sass(frag) if re.search(r"\b(LDL|STL)\b", line))
     assert n <= 2, (frag, n)
