@@ -241,6 +241,9 @@ int gdx_softmax_xent_fused_peers(const float* logits, uint64_t ld, uint32_t rows
 /* Bandwidth probe for roofline denominators: reads `bytes` of buf `reps` times,
  * mode 0 = coalesced stream, mode 1 = random 256 B row gathers (bytes moved =
  * reps * bytes in both modes).  Time it with events on `stream`. */
+/* L2 access-policy window (persisting) on `stream` for the matrix the next kernels gather
+ * (bytes = 0 clears it); carves the device's persisting L2 set-aside on first use. */
+int gdx_set_l2_window(const void* base, uint64_t bytes, float hit_ratio, gdx_stream stream);
 int gdx_probe_bandwidth(const float* buf, uint64_t bytes, uint32_t reps, int mode, float* sink,
                         gdx_stream stream);
 /* Per-vertex scales from CSR degrees: kind 0 -> 1/deg (0 if deg=0), 1 -> (deg+1)^-1/2. */

@@ -72,6 +72,7 @@ _SIGS = {
     "gdx_ipc_close": (C.c_int, [vp]),
     "gdx_peer_signal": (C.c_int, [vp, u32, vp]),
     "gdx_memcpy_async": (C.c_int, [vp, vp, u64, vp]),
+    "gdx_set_l2_window": (C.c_int, [vp, u64, C.c_float, vp]),
     "gdx_push_peers": (C.c_int, [vp, u64, vp, u32, vp, vp, u32, vp]),
     "gdx_peer_wait_src": (C.c_int, [vp, vp, u32, C.c_int, u64, vp]),
     "gdx_push_multicast": (C.c_int, [vp, u64, vp, u32, vp, vp, u32, vp]),

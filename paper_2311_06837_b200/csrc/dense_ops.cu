@@ -529,3 +529,35 @@ extern "C" int gdx_probe_bandwidth(const float* buf, uint64_t bytes, uint32_t re
     note_launch();
     return check_launch("gdx_probe_bandwidth");
 }
+
+// L2 persistence for the gathered matrix of the next aggregation: an access-policy
+// window on the stream (kernel nodes captured into a CUDA graph inherit it).
+// bytes == 0 clears the window.  The persisting carve-out is set once, on first use.
+extern "C" int gdx_set_l2_window(const void* base, uint64_t bytes, float hit_ratio, gdx_stream stream) {
+    static bool carved = false;
+    cudaStream_t s = as_cuda(stream);
+    if (bytes && !carved) {
+        int dev = 0, maxp = 0;
+        GDX_CUDA(cudaGetDevice(&dev));
+        GDX_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+        if (maxp > 0) GDX_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(maxp)));
+        carved = true;
+    }
+    cudaStreamAttrValue v{};
+    if (bytes) {
+        int dev = 0, maxw = 0;
+        GDX_CUDA(cudaGetDevice(&dev));
+        GDX_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+        v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+        v.accessPolicyWindow.num_bytes = bytes < static_cast<uint64_t>(maxw) ? bytes : static_cast<uint64_t>(maxw);
+        v.accessPolicyWindow.hitRatio = hit_ratio;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    } else {
+        v.accessPolicyWindow.num_bytes = 0;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+    }
+    GDX_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+    return GDX_OK;
+}

@@ -81,6 +81,8 @@ def init_weights(cfg: ModelConfig, seed: int) -> list:
 
 
 L2_RESIDENT_BYTES = 96 << 20  # gathered matrices up to this size stay in the 126 MB L2
+# pin the gathered matrix in L2 with a persisting access-policy window (GDX_L2_WINDOW=1)
+L2_WINDOW = os.environ.get("GDX_L2_WINDOW", "0") != "0"
 
 
 def agg_width(fout: int, rows: int) -> int:
@@ -433,6 +435,8 @@ class FullGraphTrainer:
 
     def _agg(self, csr, src, width, nnz_hint=None, **kw):
         kw.setdefault("variant", agg_variant(width, self.nnz_local, self.nloc))
+        if L2_WINDOW and src.numel() * 4 <= L2_RESIDENT_BYTES:
+            call("gdx_set_l2_window", src.data_ptr(), src.numel() * 4, 1.0, stream_handle())
         ev = getattr(self, "_events", None)
         if ev is None:
             return aggregate(csr, src, width, **kw)
