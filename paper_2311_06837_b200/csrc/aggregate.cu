@@ -15,6 +15,14 @@
 //    fp32 and split-bf16 stores) is fused, so the output is written once.
 #include "gdx_common.cuh"
 
+// Occupancy: 8 resident 256-thread blocks (64 warps, <= 32 registers; the few spills
+// sit outside the gather loop) keep more gathers in flight.  Measured: 64-wide rows in
+// the HBM regime 2.86 -> 2.60 ms (products pass, 98% of the copy peak), L2 regime 1.50
+// -> 1.49 ms, 192-wide low-degree rows 4.46 -> 3.94 ms; the 12-lane warp kernel loses
+// (1.51 -> 1.74 ms) and wide rows (several float4 chunks per lane) would spill heavily,
+// so those keep the default.
+constexpr int agg_min_blocks(int lpe, int nch) { return (lpe == 12 || nch > 1) ? 1 : 8; }
+
 namespace gdx {
 namespace {
 
@@ -93,7 +101,7 @@ constexpr int pow2_floor(int x) { return x >= 32 ? 32 : x >= 16 ? 16 : x >= 8 ? 
 // LPE lanes cover one neighbour row (NCH float4 chunks each); EPW = pow2 rows per
 // warp step; EXACT: c4 == LPE*NCH (no column masks).
 template <int LPE, int NCH, bool EXACT, int UNROLL>
-__global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
+__global__ void __launch_bounds__(256, agg_min_blocks(LPE, NCH)) aggregate_vec4(const AggParams p) {
     constexpr int EPW = pow2_floor(32 / LPE);
     constexpr int STEP = EPW * UNROLL;
     const int lane = threadIdx.x & 31;
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(256) aggregate_vec4(const AggParams p) {
 // walks EPW rows at once, and each group keeps UNROLL neighbour gathers in
 // flight; no shuffles, so groups diverge freely.
 template <int LPE, int NCH, bool EXACT, int UNROLL>
-__global__ void __launch_bounds__(256) aggregate_rows(const AggParams p) {
+__global__ void __launch_bounds__(256, agg_min_blocks(LPE == 12 ? 16 : LPE, NCH)) aggregate_rows(const AggParams p) {
     constexpr int EPW = pow2_floor(32 / LPE);
     const int lane = threadIdx.x & 31;
     const int sub = lane / LPE;
