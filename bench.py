@@ -535,7 +535,8 @@ def main():
         e2e = {"value": round(float(e2e_ms[0]), 3), "unit": "ms",
                "h2d_bytes_per_step": int(xh.numel() * 4 + lh.numel() * 4) * world,
                "d2h_bytes_per_step": 8 * world,
-               "pipelining": "step i+1's feature H2D overlaps step i's compute (double buffer)"}
+               "pipelining": "step i+1's feature H2D overlaps step i's compute (double buffer)",
+               "h2d_ms_per_step": round(fs.copy_ms(), 3)}
 
     l2_peak = probe_l2_peak(torch, dev)
     edges_total = g.num_edges()

@@ -767,6 +767,14 @@ class FeatureStream:
         self.free = [torch.cuda.Event() for _ in range(2)]
         self.issued = 0
         self.consumed = 0
+        # per-copy timing events on the copy stream (H2D duration under overlap)
+        self.copy_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
+
+    def copy_ms(self) -> float:
+        """Mean duration of the issued copies (call after they completed)."""
+        if not self.copy_events:
+            return 0.0
+        return sum(a.elapsed_time(b) for a, b in self.copy_events) / len(self.copy_events)
 
     def prefetch(self, x_host: torch.Tensor, labels_host: torch.Tensor | None = None):
         i = self.issued % 2
@@ -775,9 +783,14 @@ class FeatureStream:
             cs.wait_event(self.free[i])
         cs.wait_stream(torch.cuda.current_stream()) if self.issued == 0 else None
         with torch.cuda.stream(cs):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
             self.stage[i][:self.tr.nloc, :self.tr.F].copy_(x_host, non_blocking=True)
             if labels_host is not None:
                 self.labels[i][:self.tr.nloc].copy_(labels_host, non_blocking=True)
+            e1.record(cs)
+            self.copy_events.append((e0, e1))
             self.ready[i].record(cs)
         self.issued += 1
 
