@@ -760,7 +760,7 @@ class FeatureStream:
     def __init__(self, tr: "FullGraphTrainer"):
         self.tr = tr
         d = tr.d
-        self.stage = [dense(tr.nloc, tr.F, d) for _ in range(2)]
+        self.stage = [torch.empty((tr.nloc, tr.F), dtype=torch.float32, device=d) for _ in range(2)]
         self.labels = [torch.empty_like(tr.labels) for _ in range(2)]
         self.copy_stream = torch.cuda.Stream(device=d)
         self.ready = [torch.cuda.Event() for _ in range(2)]
@@ -786,7 +786,16 @@ class FeatureStream:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(cs)
-            self.stage[i][:self.tr.nloc, :self.tr.F].copy_(x_host, non_blocking=True)
+            # the stage is contiguous [nloc, F] (the host layout), so this is ONE DMA at
+            # the PCIe rate; consume() splits it with ld = F.  (Copying into the 16-byte
+            # padded view instead makes torch stage a temporary and repack it with a
+            # kernel that competes with the running epoch for SMs: 10.1 ms alone ->
+            # 14-16 ms; a pitched cudaMemcpy2DAsync with 2408-byte rows ran at 17 GB/s.)
+            if x_host.shape != (self.tr.nloc, self.tr.F) or x_host.dtype != torch.float32:
+                raise InputError(f"FeatureStream: features must be float32 [{self.tr.nloc}, {self.tr.F}]")
+            if not x_host.is_pinned() or not x_host.is_contiguous():
+                raise InputError("FeatureStream: features must be pinned, contiguous host memory")
+            self.stage[i].copy_(x_host, non_blocking=True)
             if labels_host is not None:
                 self.labels[i][:self.tr.nloc].copy_(labels_host, non_blocking=True)
             e1.record(cs)
@@ -799,7 +808,7 @@ class FeatureStream:
         cur = torch.cuda.current_stream()
         cur.wait_event(self.ready[i])
         tr = self.tr
-        tr.Xsp.fill_from(self.stage[i], self.stage[i].shape[1])
+        tr.Xsp.fill_from(self.stage[i], tr.F)
         if with_labels:
             tr.labels.copy_(self.labels[i])
         self.free[i].record(cur)

@@ -126,3 +126,33 @@ def test_subgraph_training_matches_oracle(cuda, kind, m, k):
         loss, grads = O.train_epoch_masked(lc, x, lab, model, w, lr, n_inner, float(n_inner),
                                            nthreads=4, layer_rows=layer_rows)
         assert abs(lg - loss) <= 1e-3, (e, lg, loss)
+
+
+def test_feature_stream_matches_resident_features(cuda):
+    """End-to-end feature loading (bench e2e): features streamed from pinned host memory
+    (one contiguous DMA per step, split with ld = F into the padded GEMM operand) train
+    like the resident features."""
+    import torch
+
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.errors import InputError
+    from paper_2311_06837_b200.train import FeatureStream, FullGraphTrainer, ModelConfig, init_weights
+
+    g = G.gen_random_graph(2000, 12.0, 9)
+    cfg = ModelConfig("sage", [101, 64, 41], lr=0.5)   # odd width: operand pitch != host row
+    w0 = init_weights(cfg, 3)
+    ref = FullGraphTrainer(g, cfg, weights=w0)
+    tr = FullGraphTrainer(g, cfg, weights=w0)
+    xh = ref.X[:ref.nloc, :ref.F].cpu().contiguous().pin_memory()
+    lh = ref.labels[:ref.nloc].cpu().pin_memory()
+    tr.X[:tr.nloc, :tr.F].zero_()
+    fs = FeatureStream(tr)
+    for _ in range(3):
+        fs.prefetch(xh, lh)
+        fs.consume()
+        torch.testing.assert_close(fs.stage[(fs.consumed - 1) % 2][:tr.nloc, :tr.F].cpu(), xh.cpu(),
+                                   rtol=0, atol=0)
+        a, b = tr.train_epoch(), ref.train_epoch()
+        assert abs(a - b) <= 1e-6 * abs(b), (a, b)   # loss atomics: summation order only
+    with pytest.raises(InputError):
+        fs.prefetch(xh.cpu().clone(), lh)   # pageable host memory is rejected

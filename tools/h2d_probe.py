@@ -10,6 +10,43 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
+def _load(kind: str, dev):
+    """A concurrent load on a side stream: 'l2' gathers random 256-byte rows of a 60 MB
+    (L2-resident) matrix like the aggregation; 'hbm' streams a 4 GB device copy."""
+    if kind == "l2":
+        src = torch.randn(233_000, 64, device=dev)
+        idx = torch.randint(0, 233_000, (8_000_000,), device=dev)
+        return lambda: torch.index_select(src, 0, idx)
+    a = torch.empty(1 << 30, dtype=torch.float32, device=dev)
+    b = torch.empty_like(a)
+    return lambda: b.copy_(a)
+
+
+def probe_under_load(kind: str, nbytes: int = 562 << 20, reps: int = 3):
+    dev = torch.device("cuda:0")
+    n = nbytes // 4
+    h = torch.empty(n, dtype=torch.float32).pin_memory()
+    d = torch.empty(n, dtype=torch.float32, device=dev)
+    work = _load(kind, dev)
+    ls = torch.cuda.Stream(device=dev)
+    cs = torch.cuda.Stream(device=dev)
+    best = 0.0
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        with torch.cuda.stream(ls):
+            for _ in range(40):
+                work()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(cs):
+            e0.record(cs)
+            d.copy_(h, non_blocking=True)
+            e1.record(cs)
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return round(best, 1)
+
+
 def probe(nbytes: int = 562 << 20, reps: int = 5):
     dev = torch.device("cuda:0")
     n = nbytes // 4
@@ -41,4 +78,8 @@ def probe(nbytes: int = 562 << 20, reps: int = 5):
 
 
 if __name__ == "__main__":
-    print(json.dumps(probe()))
+    r = probe()
+    if "--load" in sys.argv:
+        r["under_l2_gather_gbs"] = probe_under_load("l2")
+        r["under_hbm_stream_gbs"] = probe_under_load("hbm")
+    print(json.dumps(r))
