@@ -78,6 +78,7 @@ def port() -> C.CDLL:
         L.gro_from_edges.argtypes = [_u32p, C.c_uint64, C.c_uint32, _u64p, _u32p]
         L.gro_partition_random.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, _u32p]
         L.gro_make_features.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, _f64p]
+        L.gro_feature_rows.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64, _f64p, C.c_int]
         L.gro_make_layer_weights.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, _f64p]
         L.gro_forward_full.argtypes = [C.c_uint32, _u64p, _u32p, _f64p, C.c_uint32, _f64p,
                                        C.c_uint32, C.c_uint32, _f64p, C.c_int]
@@ -243,6 +244,14 @@ def make_features(n: int, dim: int, seed: int) -> np.ndarray:
     return out.reshape(n, dim)
 
 
+def feature_rows(ids, dim: int, seed: int, nthreads: int = 0) -> np.ndarray:
+    """Rows `ids` of make_features(n, dim, seed) without generating the rest."""
+    ids = np.ascontiguousarray(ids, np.uint32)
+    out = np.zeros(max(len(ids), 1) * dim, np.float64)
+    port().gro_feature_rows(ids.ctypes.data, len(ids), dim, seed, out, nthreads or (os.cpu_count() or 1))
+    return out[:len(ids) * dim].reshape(len(ids), dim)
+
+
 def make_layer_weights(layers: int, F: int, H: int, seed: int) -> list[np.ndarray]:
     total = sum(H * (F if l == 0 else H) for l in range(layers))
     out = np.zeros(max(total, 1), np.float64)
@@ -253,6 +262,24 @@ def make_layer_weights(layers: int, F: int, H: int, seed: int) -> list[np.ndarra
         ws.append(out[off:off + H * i].reshape(H, i).copy())
         off += H * i
     return ws
+
+
+def stream_weights(shapes, seed: int, fp32: bool = True, init: str = "uniform") -> list[np.ndarray]:
+    """Matrices of the given (rows, cols) shapes filled by consecutive U(-.5,.5) draws
+    of the weight stream (seed, "weig") -- make_layer_weights' stream
+    (reference_gnn.cpp:18-32) continued across matrices, which is how the engine's
+    init_weights lays out SAGE's W_self / W_neigh pairs.  fp32: round to the fp32
+    values the engine trains from."""
+    total = sum(int(r) * int(c) for r, c in shapes)
+    flat = make_layer_weights(1, max(total, 1), 1, seed)[0].reshape(-1)
+    out, off = [], 0
+    for r, c in shapes:
+        w = flat[off:off + r * c].reshape(r, c)
+        if init == "he":      # the engine's ModelConfig.init == 'he' (train.init_scale)
+            w = w * (2.0 * np.sqrt(6.0 / c))
+        out.append(w.astype(np.float32).astype(np.float64) if fp32 else w.copy())
+        off += r * c
+    return out
 
 
 def _flat(ws) -> np.ndarray:

@@ -223,6 +223,23 @@ void gro_make_features(uint32_t n, uint32_t dim, uint64_t seed, double* out) {
     for (uint64_t i = 0; i < total; ++i) out[i] = uniform(&r, -0.5, 0.5);
 }
 
+/* Rows ids[0..count) of make_features' matrix (reference_gnn.cpp:11-16) without
+ * generating the others: row v's values are draws v*dim .. v*dim+dim-1 of the one
+ * stream, and SplitMix64 draw i is reached by adding (i+1)*gamma to the keyed state
+ * (the stream is a counter).  For feature matrices too large for host memory
+ * (papers shape: 111 M x 128). */
+void gro_feature_rows(const uint32_t* ids, uint64_t count, uint32_t dim, uint64_t seed,
+                      double* out, int nthreads) {
+    gro_rng r0;
+    gro_rng_init(&r0, seed, 0x66656174ULL, 0);
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
+    for (uint64_t i = 0; i < count; ++i) {
+        gro_rng r;
+        r.state = r0.state + (uint64_t)ids[i] * dim * GAMMA;
+        for (uint32_t c = 0; c < dim; ++c) out[i * dim + c] = uniform(&r, -0.5, 0.5);
+    }
+}
+
 /* reference_gnn.cpp:18-32: layer 0 is hidden x feature_dim, the rest hidden x hidden */
 void gro_make_layer_weights(uint32_t layers, uint32_t F, uint32_t H, uint64_t seed,
                             double* out) {

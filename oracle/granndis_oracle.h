@@ -60,6 +60,8 @@ void gro_partition_random(uint32_t n, uint32_t parts, uint64_t seed, uint32_t* a
 
 /* ---- reference_gnn.cpp -------------------------------------------------- */
 void gro_make_features(uint32_t n, uint32_t dim, uint64_t seed, double* out);
+void gro_feature_rows(const uint32_t* ids, uint64_t count, uint32_t dim, uint64_t seed,
+                      double* out, int nthreads);
 void gro_make_layer_weights(uint32_t layers, uint32_t feature_dim, uint32_t hidden_dim,
                             uint64_t seed, double* out);
 /* out: n x (layers ? hidden : F).  nthreads>1 keeps per-row order, so bit-identical. */

@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 from ._lib import AggregateArgs, GemmArgs, call, ptr
-from .errors import InternalError
+from .errors import InputError, InternalError
 
 
 def pad4(x: int) -> int:
@@ -150,10 +150,13 @@ def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None,
     g.m = mA if m is None else m
     g.n = nB
     g.k = kA
+    for c in (c0, c1):
+        if c is not None and (c.dim() != 2 or c.stride(1) != 1):
+            raise InputError("gemm_tn: outputs must be 2-D row-major views (unit column stride)")
     g.c0 = ptr(c0)
-    g.ldc0 = c0.shape[-1] if c0 is not None else 0
+    g.ldc0 = c0.stride(0) if c0 is not None else 0
     g.c1 = ptr(c1)
-    g.ldc1 = c1.shape[-1] if c1 is not None else 0
+    g.ldc1 = c1.stride(0) if c1 is not None else 0
     g.split = nB if split is None else split
     g.row_scale = ptr(row_scale)
     g.relu = int(relu)

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import math
 import os
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -46,6 +47,10 @@ class ModelConfig:
     kind: str = "sage"              # 'sage' | 'gcn' | 'sum'
     dims: list = field(default_factory=lambda: [602, 64, 64, 41])
     lr: float = 0.1
+    # 'uniform': U(-.5,.5), the reference's make_layer_weights values; 'he': the same
+    # draws times 2 sqrt(6 / fan_in) (He-uniform), which keeps a 56-layer stack finite
+    # (U(-.5,.5) grows activations ~1.6x per layer and overflows by layer ~40)
+    init: str = "uniform"
 
     @property
     def layers(self) -> int:
@@ -75,9 +80,19 @@ def init_weights(cfg: ModelConfig, seed: int) -> list:
         t = torch.empty(o * i, dtype=torch.float64, device=d)
         call("gdx_init_uniform_f64", seed, WEIG_TAG, 0, first, o, i, -0.5, 0.5, t.data_ptr(), i,
              stream_handle())
-        ws.append(t.cpu().numpy().reshape(o, i))
+        w = t.cpu().numpy().reshape(o, i)
+        ws.append(w * init_scale(cfg.init, i))
         first += o * i
     return ws
+
+
+def init_scale(init: str, fan_in: int) -> float:
+    """Multiplier of the U(-.5,.5) weight draws (see ModelConfig.init)."""
+    if init == "uniform":
+        return 1.0
+    if init == "he":
+        return 2.0 * math.sqrt(6.0 / fan_in)
+    raise InputError(f"unknown weight init {init!r}")
 
 
 L2_RESIDENT_BYTES = 96 << 20  # gathered matrices up to this size stay in the 126 MB L2
@@ -183,8 +198,8 @@ class _Layer:
     def refresh_splits(self):
         self.Wsp.fill_from(self.W, self.fin_ld)
 
-    def get_weights(self):
-        W = self.W.double().cpu().numpy()
+    def get_weights(self, M=None):
+        W = (self.W if M is None else M).double().cpu().numpy()
         if self.kind == "sage":
             return [W[:self.fout, :self.fin].copy(), W[self.w:self.w + self.fout, :self.fin].copy()]
         return [W[:self.fout, :self.fin].copy()]
@@ -240,8 +255,8 @@ class _AggFirstLayer:
     def refresh_splits(self):
         self.Wsp.fill_from(self.W, self.fin_ld)
 
-    def get_weights(self):
-        W = self.W.double().cpu().numpy()
+    def get_weights(self, M=None):
+        W = (self.W if M is None else M).double().cpu().numpy()
         return [W[:self.fout, :self.fin].copy(), W[:self.fout, self.w:self.w + self.fin].copy()]
 
     def w_cols(self, half: int) -> Split:
@@ -404,8 +419,24 @@ class FullGraphTrainer:
         self.set_weights(weights)
         self.partial = dense(self.nloc, max(L.w for L in self.layers), d) if self.overlap else None
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=d)
+        if self.p2p is not None:
+            # the layers' shared buffers are torch views over memory P2PExchange owns:
+            # free it only when the trainer (and so every view) is gone
+            self._p2p_finalizer = weakref.finalize(self, _close_quietly, self.p2p)
         self.keep_activations = False
         self.activations = []
+
+    def close(self):
+        """Release the captured graph, every buffer view and the peer mappings
+        (call on all ranks; the trainer is unusable afterwards)."""
+        self.graph = None
+        self.layers = []
+        self.partial = None
+        torch.cuda.synchronize(self.d)
+        fin = getattr(self, "_p2p_finalizer", None)
+        if fin is not None:
+            fin()
+        self.p2p = None
 
     # ---- state ----
     def _refresh_input_splits(self):
@@ -420,6 +451,14 @@ class FullGraphTrainer:
         out = []
         for layer in self.layers:
             out.extend(layer.get_weights())
+        return out
+
+    def get_grads(self):
+        """The last step's weight gradients (reference order, like get_weights): the
+        reduced dW each layer's split-K pass (+ all-reduce) left in the flat buffer."""
+        out = []
+        for layer in self.layers:
+            out.extend(layer.get_weights(layer.dW))
         return out
 
     def load_features(self, x_host: torch.Tensor, labels_host: torch.Tensor | None = None):
@@ -538,7 +577,7 @@ class FullGraphTrainer:
                 gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s, m=m_in, peers=self._peers(L.z_peers, 0))
             else:
                 gemm_tn(A, L.Wsp, c0=own, m=m_in, peers=self._peers(L.z_peers, 0))
-            self._publish(own, L.z_peers)
+            self._publish(own, L.z_peers, stored=True)
             nxt = self.layers[l + 1] if l + 1 < cfg.layers else None
             if getattr(nxt, "agg_first", False):   # output rows feed an aggregate-first layer
                 out, out_split = nxt.Xin_full[self.lo:self.hi], _SplitView(nxt.C, 0)
@@ -572,11 +611,16 @@ class FullGraphTrainer:
             return None
         return (target, deltas)
 
-    def _publish(self, own: torch.Tensor, deltas):
-        """After the producer of an exchanged buffer: make our rows visible to peers."""
+    def _publish(self, own: torch.Tensor, deltas, stored: bool = False):
+        """After the producer of an exchanged buffer: make our rows visible to peers.
+        stored: the producer was launched with peers= (GDX_EXCHANGE=p2p-epilogue) and
+        already wrote the rows into every peer's copy, so only the arrival signal is
+        left.  Producers without peer stores (the aggregate kernel writing an
+        aggregate-first layer's input rows, the dA GEMM, gdx_grad_prepare) are pushed
+        by the SM push kernel in every mode."""
         if self.p2p is None:
             return
-        if self.p2p.mode == "epilogue":
+        if stored and self.p2p.mode == "epilogue":
             self.p2p.signal()
         else:
             self.p2p.push(own, deltas, rows=getattr(self, "send_rows", None))
@@ -621,7 +665,7 @@ class FullGraphTrainer:
                 gemm_tn(L.G, L.Wsp, c0=own, b_mn=True, mask=self._act(l - 1),
                         row_scale=scale, out_split=split, split_unscaled=True, m=self.rows_out[l - 1],
                         peers=self._peers(self.layers[l - 1].d_peers, 0))
-                self._publish(own, self.layers[l - 1].d_peers)
+                self._publish(own, self.layers[l - 1].d_peers, stored=True)
             # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
             # (K = the rows that fed layer l; rows past them carry no gradient)
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
@@ -823,6 +867,13 @@ class _RawCUDA:
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
+def _close_quietly(p2p: "P2PExchange"):
+    try:
+        p2p.close()
+    except Exception:  # interpreter teardown: the CUDA context may already be gone
+        pass
+
+
 class P2PExchange:
     """Row exchange over NVLink peer memory, no NCCL on the data path.
 
@@ -841,7 +892,10 @@ class P2PExchange:
     `wait()` (before the remote-source aggregation) spins until every peer's slot
     reached the round."""
 
-    TIMEOUT_NS = 20_000_000_000  # a wedged peer traps after 20 s instead of hanging
+    # A wedged peer makes gdx_peer_wait trap after this long instead of hanging forever
+    # (GDX_PEER_TIMEOUT_S, default 20 s).  A trap is a sticky device fault: it poisons
+    # this process's CUDA context, so the process must exit -- there is no recovery.
+    TIMEOUT_NS = int(float(os.environ.get("GDX_PEER_TIMEOUT_S", "20")) * 1e9)
 
     def __init__(self, rank: int, world: int, pg, device, mode: str = "ce"):
         """mode 'ce': the producer writes locally; copy engines push the owned rows to
@@ -1027,6 +1081,9 @@ class P2PExchange:
              stream_handle())
 
     def close(self):
+        """Unmap the peers' buffers and free ours.  Only valid once nothing views the
+        memory any more: FullGraphTrainer.close() drops its views first, and a
+        weakref finalizer runs this when the trainer is collected."""
         for p in self._opened:
             _lib.lib().gdx_ipc_close(p)
         self._opened = []

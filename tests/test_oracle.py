@@ -248,3 +248,19 @@ def test_labels_match_keyed_stream():
     lab = O.make_labels(300, 41, 5)
     ref = [(int(O.rng_draws(5, v, 0x6c61626c, 1)[0]) * 41) >> 64 for v in range(300)]
     assert np.array_equal(lab, ref)
+
+
+def test_stream_weights_continue_the_weight_stream():
+    """stream_weights (the bench / test initial weights) is make_layer_weights'
+    stream (reference_gnn.cpp:18-32) continued across matrices."""
+    ref = O.make_layer_weights(2, 5, 4, 77)
+    got = O.stream_weights([(4, 5), (4, 4)], 77, fp32=False)
+    assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+    r32 = O.stream_weights([(4, 5), (4, 4)], 77)
+    assert all(np.array_equal(a, b.astype(np.float32).astype(np.float64)) for a, b in zip(r32, ref))
+
+
+def test_feature_rows_are_rows_of_make_features():
+    full = O.make_features(300, 7, 9)
+    ids = np.array([0, 5, 299, 17, 17], np.uint32)
+    assert np.array_equal(O.feature_rows(ids, 7, 9), full[ids])

@@ -1,0 +1,195 @@
+"""Parity at the BASELINE.json configurations themselves (not toy sizes): the GPU
+trainer against the fp64 oracle on identical inputs -- fp32-rounded features
+(stream seed 1), labels (seed 2) and initial weights (weight stream seed 3).
+
+North_star contract: training loss within 1e-3 of the oracle every epoch over
+10 epochs; per-layer fp32 activations and gradients within relative 1e-4, read
+as |a - b| <= 1e-4 (|b| + rms(b)) (the doctest-style scaled check of SURVEY
+§8d, rms over the whole tensor so ReLU zeros do not divide by zero).
+
+Parity is UNPINNED against the reference itself: it has no training path
+(SPEC.md:9, :545); the oracle's forward reduces bit-exactly to the reference's
+forward_full (tests/test_oracle.py) and its backward is finite-difference checked.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+THREADS = os.cpu_count() or 1
+KIND = {"sage": O.SAGE, "gcn": O.GCN, "sum": O.SUM}
+
+
+def close(a, b, tol=1e-4, what=""):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    rms = float(np.sqrt(np.mean(b * b))) if b.size else 0.0
+    err = np.abs(a - b) - tol * (np.abs(b) + rms)
+    i = int(np.argmax(err))
+    assert err.flat[i] <= 0.0, (f"{what}: excess {err.flat[i]:.3e} at {i} "
+                                f"(gpu {a.flat[i]:.6e} oracle {b.flat[i]:.6e} rms {rms:.3e})")
+
+
+def _full_graph_pair(kind, n, deg, seed, dims, lr, epochs, init="uniform", sample_rows=4096):
+    """Train `epochs` epochs on the GPU and in the oracle from the same state; check
+    epoch-1 activations (sampled rows) and gradients, and every epoch's loss."""
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.train import FullGraphTrainer, ModelConfig
+
+    g = G.gen_random_graph(n, deg, seed)
+    cfg = ModelConfig(kind, list(dims), lr=lr, init=init)
+    model = O.Model(KIND[kind], dims)
+    w0 = O.stream_weights(model.weight_shapes(), 3, init=init)
+    tr = FullGraphTrainer(g, cfg, weights=w0)
+    c = O.CSR(n, g.row_offsets(), g.col_indices())
+    x = O.make_features(n, dims[0], 1).astype(np.float32).astype(np.float64)
+    labels = O.make_labels(n, dims[-1], 2)
+    w = np.concatenate([a.ravel() for a in w0])
+    rows = np.random.default_rng(0).choice(n, size=min(n, sample_rows), replace=False)
+    lg, lo = [], []
+    for e in range(epochs):
+        tr.keep_activations = e == 0
+        lg.append(tr.train_epoch())
+        if e == 0:
+            l_ref, grads, acts, _ = O.train_epoch(c, x, labels, model, w, lr, want_state=True,
+                                                  nthreads=THREADS)
+            for li, (a_gpu, a_ref) in enumerate(zip(tr.activations, acts)):
+                a = a_gpu.double().cpu().numpy()
+                rms_full = float(np.sqrt(np.mean(a_ref * a_ref)))
+                err = np.abs(a[rows] - a_ref[rows]) - 1e-4 * (np.abs(a_ref[rows]) + rms_full)
+                assert err.max() <= 0, f"layer {li} activations: excess {err.max():.3e}"
+            off = 0
+            for mi, gm in enumerate(tr.get_grads()):
+                ref = grads[off:off + gm.size].reshape(gm.shape)
+                off += gm.size
+                close(gm, ref, what=f"dW[{mi}]")
+            lo.append(l_ref)
+        else:
+            lo.append(O.train_epoch(c, x, labels, model, w, lr, nthreads=THREADS))
+    tr.close()
+    return np.array(lg), np.array(lo)
+
+
+def test_reddit_sage_configs1_ten_epochs(cuda):
+    """BASELINE configs[1] at full size: 232,965 vertices, 114.6 M entries, SAGE
+    602-64-64-41, lr 0.1 (the bench workload), 10 epochs."""
+    lg, lo = _full_graph_pair("sage", 232965, 491.99, 11, [602, 64, 64, 41], 0.1, 10)
+    assert np.all(np.isfinite(lg))
+    assert np.all(np.abs(lg - lo) <= 1e-3), np.c_[lg, lo]
+
+
+def test_products_gcn_configs3_epochs(cuda):
+    """BASELINE configs[3] at full size: 2,449,029 vertices, 61.9 M entries, GCN
+    100-64-64-47 (the HBM-regime gathers), 4 epochs."""
+    lg, lo = _full_graph_pair("gcn", 2449029, 25.26, 13, [100, 64, 64, 47], 0.1, 4)
+    assert np.all(np.abs(lg - lo) <= 1e-3), np.c_[lg, lo]
+
+
+def _local_graph(g, sub):
+    """The oracle's view of a DependencySubgraph: local ids in (hop, id) order and the
+    induced rows in global neighbour order (the engine's LocalSubgraph numbering)."""
+    n = g.num_vertices()
+    hop = sub.hop_array(n)
+    m = len(sub.inner_vertices) + len(sub.halo_vertices)
+    order = np.lexsort((np.arange(n), hop))[:m]
+    local = np.full(n, -1, np.int64)
+    local[order] = np.arange(m)
+    ro, ci = g.row_offsets().astype(np.int64), g.col_indices()
+    deg = np.diff(ro)[order]
+    starts = ro[order]
+    idx = np.repeat(starts - np.concatenate([[0], np.cumsum(deg)[:-1]]), deg) + np.arange(deg.sum())
+    nb = local[ci[idx]]
+    keep = nb >= 0
+    row_of = np.repeat(np.arange(m), deg)[keep]
+    counts = np.bincount(row_of, minlength=m)
+    lro = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    return O.CSR(m, lro, nb[keep].astype(np.uint32)), order, hop[order]
+
+
+@pytest.mark.parametrize("server", [0, 5])
+def test_gcn56_eas_configs2_reduced(cuda, server):
+    """BASELINE configs[2] semantics at reduced V: 56-layer normalised GCN (He-uniform
+    init, lr 1.0 as bench.py), EAS(m=1, k=15, seed 3) on an 8-server random partition
+    (N_s = 8 emulated servers), one server's preloaded subgraph on the GPU, loss on
+    its inner vertices, 10 epochs.  V and the degree are Reddit's / 10 (same edge
+    density p = deg / V); every layer's gradient is checked after epoch 1."""
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.train import FullGraphTrainer, ModelConfig
+
+    n, deg, dims, lr = 23297, 49.2, [602] + [64] * 55 + [41], 1.0
+    g = G.gen_random_graph(n, deg, 11)
+    part = G.partition_random(g, 8, 1)
+    sub = G.extract_sampled(g, part, server, G.SamplingConfig(1, 15, 3))
+    cfg = ModelConfig("gcn", dims, lr=lr, init="he")
+    model = O.Model(O.GCN, dims)
+    w0 = O.stream_weights(model.weight_shapes(), 3, init="he")
+    tr = FullGraphTrainer(g, cfg, weights=w0, subgraph=sub)
+    lc, order, hop_sorted = _local_graph(g, sub)
+    x = O.make_features(n, dims[0], 1).astype(np.float32).astype(np.float64)[order]
+    lab = O.make_labels(n, dims[-1], 2)[order]
+    L = len(dims) - 1
+    layer_rows = [int(np.sum(hop_sorted <= L - l - 1)) for l in range(L)]
+    x[hop_sorted > L] = 0.0
+    n_inner = len(sub.inner_vertices)
+    w = np.concatenate([a.ravel() for a in w0])
+    lg, lo = [], []
+    for e in range(10):
+        lg.append(tr.train_epoch())
+        loss, grads = O.train_epoch_masked(lc, x, lab, model, w, lr, n_inner, float(n_inner),
+                                           nthreads=THREADS, layer_rows=layer_rows)
+        lo.append(loss)
+        if e == 0:
+            off = 0
+            for mi, gm in enumerate(tr.get_grads()):
+                ref = grads[off:off + gm.size].reshape(gm.shape)
+                off += gm.size
+                close(gm, ref, what=f"dW[{mi}]")
+    tr.close()
+    lg, lo = np.array(lg), np.array(lo)
+    assert np.all(np.isfinite(lg))
+    assert np.all(np.abs(lg - lo) <= 1e-3), np.c_[lg, lo]
+
+
+def test_papers_cobatch_full_size_batch_step(cuda):
+    """BASELINE configs[4] at full size: the papers-shape graph (111 M vertices, 1.6 B
+    entries), one server, EAS(1, 15, 3), targets split into R = 256 groups
+    (split_targets_random); batch 0 (a full-size cooperative batch) gets one SGD step
+    on the GPU and in the oracle from the same weights."""
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.batch_plan import (BatchPlan, ModelSpec, make_batch,
+                                                  split_targets_random)
+    from paper_2311_06837_b200.cobatch import CobatchTrainer
+    from paper_2311_06837_b200.graph import Partition
+    from paper_2311_06837_b200.train import ModelConfig
+
+    dims, L = [128, 64, 64, 172], 3
+    g = G.gen_random_graph(111059956, 14.55, 17)
+    n = g.num_vertices()
+    sp = Partition(np.zeros(n, np.uint32), 1)
+    gp = Partition(np.zeros(n, np.uint32), 1)
+    scfg = G.SamplingConfig(1, 15, 3)
+    universe = np.ones(n, np.uint8)          # one server: every vertex is inner
+    targets = split_targets_random(np.arange(n, dtype=np.uint32), 256, scfg.seed)[0]
+    b0 = make_batch(g, universe, targets, L, scfg, ModelSpec(L, dims[1], dims[0]))
+    plan = BatchPlan(0, "fetch_then_split", L, [b0])
+    cfg = ModelConfig("sage", dims, lr=0.1)
+    model = O.Model(O.SAGE, dims)
+    w0 = O.stream_weights(model.weight_shapes(), 3)
+    tr = CobatchTrainer(g, cfg, plan, sp, gp, 0, weights=w0)
+    tr.train_batch(0)
+    loss_gpu = float(tr.loss_acc.item()) / len(b0.target_vertices)
+    geo = tr.geoms[0]
+    lp = geo.csr.row_ptr.cpu().numpy().astype(np.uint64)
+    lcol = geo.csr.col[:max(geo.nnz, 1)].cpu().numpy().view(np.uint32)[:geo.nnz]
+    csr = O.CSR(geo.nloc, lp, lcol)
+    l2g = geo.l2g.cpu().numpy().astype(np.int64)
+    x = O.feature_rows(l2g, dims[0], 1).astype(np.float32).astype(np.float64)
+    lab = O.make_labels(n, dims[-1], 2)[l2g]
+    w = np.concatenate([a.ravel() for a in w0])
+    loss, _ = O.train_epoch_masked(csr, x, lab, model, w, 0.1, geo.loss_rows, float(geo.loss_count),
+                                   nthreads=THREADS, layer_rows=list(geo.rows_out))
+    tr.close()
+    assert abs(loss_gpu - loss) <= 1e-3, (loss_gpu, loss)
