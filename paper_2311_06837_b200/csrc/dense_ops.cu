@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256) probe_kernel(const float4* __restrict__ b
 
 unsigned grid_for(uint64_t total, unsigned block = 256) {
     uint64_t b = (total + block - 1) / block;
-    const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 16;
+    const uint64_t cap = static_cast<uint64_t>(device_sms()) * 16;
     if (b > cap) b = cap;
     return static_cast<unsigned>(b ? b : 1);
 }
@@ -434,7 +434,7 @@ bool softmax_vec_launch(const float* logits, uint64_t ld, uint32_t rows, uint32_
     // grid-stride with a bounded grid: the loss is one fp64 atomic per warp, and
     // ~10^6 atomics on one address would serialise
     uint64_t blocks = (static_cast<uint64_t>(rows) + rpb - 1) / rpb;
-    if (blocks > static_cast<uint64_t>(kNumSMs) * 8) blocks = static_cast<uint64_t>(kNumSMs) * 8;
+    if (blocks > static_cast<uint64_t>(device_sms()) * 8) blocks = static_cast<uint64_t>(device_sms()) * 8;
     if (classes <= 64)
         softmax_xent_vec<16><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
             logits, ld, rows, classes, labels, inv_count, row_scale, gs, ld_gs, g_hi, g_lo, ld_g, cols, loss_sum);
@@ -524,7 +524,7 @@ extern "C" int gdx_probe_bandwidth(const float* buf, uint64_t bytes, uint32_t re
                                    float* sink, gdx_stream stream) {
     GDX_REQUIRE(buf && sink && bytes >= 4096 && (bytes % 4096) == 0, GDX_INPUT,
                 "gdx_probe_bandwidth: need a 4 KiB-multiple buffer");
-    probe_kernel<<<kNumSMs * 8, 256, 0, as_cuda(stream)>>>(reinterpret_cast<const float4*>(buf), bytes / 16,
+    probe_kernel<<<device_sms() * 8, 256, 0, as_cuda(stream)>>>(reinterpret_cast<const float4*>(buf), bytes / 16,
                                                            reps, mode, sink);
     note_launch();
     return check_launch("gdx_probe_bandwidth");

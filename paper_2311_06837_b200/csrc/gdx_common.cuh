@@ -33,7 +33,11 @@ int check_launch(const char* what);
                                                  cudaGetErrorString(_e));           \
     } while (0)
 
-constexpr int kNumSMs = 148;
+// SM count of the calling thread's current device (cached per device): grid caps
+// and persistent grids are sized from it, never from a hard-coded 148.
+int device_sms();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel).
+int ensure_smem_attr(const void* kernel, int bytes);
 
 inline cudaStream_t as_cuda(gdx_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 

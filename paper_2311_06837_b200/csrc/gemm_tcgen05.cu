@@ -580,8 +580,6 @@ int operand_maps(CUtensorMap* hi, CUtensorMap* lo, const uint16_t* phi, const ui
     return make_map(lo, plo, rows, k, ld, BK);
 }
 
-int g_num_sms = 0;
-
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EW>
 int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
@@ -590,18 +588,10 @@ int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     if ((rc = operand_maps(&mb_hi, &mb_lo, g->b_hi, g->b_lo, g->n, g->k, g->ldb, B_MN, BN))) return rc;
     auto kern = gemm_bf16x3<BN, STAGES, A_MN, B_MN, EW>;
     const int bytes = Smem<BN, STAGES, EW>::kBytes;
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-        GDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        configured = true;
-    }
-    if (!g_num_sms) {
-        int dev = 0;
-        GDX_CUDA(cudaGetDevice(&dev));
-        GDX_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
+    if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), bytes))) return rc;
+    const uint64_t sms = static_cast<uint64_t>(device_sms());
     const uint64_t tiles = static_cast<uint64_t>(ep.m_tiles) * ep.n_tiles * ep.split_k;
-    const unsigned grid = static_cast<unsigned>(tiles < static_cast<uint64_t>(g_num_sms) ? tiles : g_num_sms);
+    const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
     kern<<<grid, kThreadsFor(EW), bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, ep);
     note_launch();
     return check_launch("gdx_gemm_tn");

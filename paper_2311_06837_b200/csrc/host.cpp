@@ -14,8 +14,10 @@
 #include <cstdint>
 #include <cstring>
 #include <limits>
+#include <mutex>
 #include <numeric>
 #include <queue>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -91,6 +93,38 @@ int fail(int code, const std::string& msg) {
     g_last_error = msg;
     return code;
 }
+int device_sms() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+    if (dev >= 64) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v == 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;
+        cache[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+int ensure_smem_attr(const void* kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(GDX_INTERNAL, "cudaGetDevice failed");
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({dev, kernel})) return GDX_OK;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess)
+        return fail(GDX_INTERNAL, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    done.insert({dev, kernel});
+    return GDX_OK;
+}
+
 void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();

@@ -320,7 +320,7 @@ __global__ void tail_total(const uint64_t* counts, uint64_t* out, uint64_t n) {
 
 unsigned grid_for(uint64_t threads, unsigned block = 256) {
     uint64_t b = (threads + block - 1) / block;
-    const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 32;
+    const uint64_t cap = static_cast<uint64_t>(device_sms()) * 32;
     if (b > cap) b = cap;
     return static_cast<unsigned>(b ? b : 1);
 }

@@ -29,7 +29,7 @@ import oracle as O
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 THREADS = os.cpu_count() or 1
-WGRAD_TOL = 1e-2
+WGRAD_TOL = 2e-3   # measured at configs[1]: 2.4e-4 (tools/grad_precision.py, 19+30 ReLU flips)
 KIND = {"sage": O.SAGE, "gcn": O.GCN, "sum": O.SUM}
 
 
