@@ -273,6 +273,24 @@ int gdx_induced_count(const uint64_t* row_ptr, const uint32_t* col, uint32_t n,
 int gdx_peel_mfg(const uint64_t* row_ptr, const uint32_t* col, uint32_t n,
                  const uint8_t* in_batch, const uint32_t* targets, uint64_t nt, uint32_t layers,
                  uint32_t* work, uint64_t* counts, gdx_stream stream);
+/* Cooperative-batch evaluation of one target grouping on the device: for every
+ * group g (targets[group_off[g] .. group_off[g+1]), ascending ids, device; group_off
+ * is a HOST array of groups+1 offsets) the sampled closure of the group's targets
+ * inside universe[n] (candidates: universe minus the group's own targets; keyed
+ * shuffle as EAS) -- batch_closure, batch_plan.cpp:28-70 -- and its back-peeled MFG
+ * counts -- peel_mfg, :75-101 -- for all groups of a chunk in the same launches,
+ * with no host synchronisation until the end (the body of plan_cobatch's R scan,
+ * :155-180, and of plan_cobatch_fixed_r, :146-153).
+ * Outputs (HOST): sizes[groups] = |batch vertices|, mfg[groups*(layers+1)] (row g is
+ * the reference's mfg_vertices_per_layer).  If vertices (device) is non-NULL, batch
+ * g's ascending vertex list is written at vertices + vertex_off[g] (host offsets,
+ * from a previous call's sizes).  workspace_bytes bounds the per-call device
+ * workspace (20 bytes per vertex per group evaluated together; >= one group). */
+int gdx_cobatch_eval(const uint64_t* row_ptr, const uint32_t* col, uint32_t n,
+                     const uint8_t* universe, const uint32_t* targets, const uint64_t* group_off,
+                     uint32_t groups, uint32_t max_hop, uint32_t fanout, uint64_t seed,
+                     uint32_t layers, uint64_t workspace_bytes, uint64_t* sizes, uint64_t* mfg,
+                     uint32_t* vertices, const uint64_t* vertex_off, gdx_stream stream);
 /* split_batch (sim.cpp:81-102): share_of[i] for sorted batch_vertices[i]; inner
  * vertices to their home GPU, halo vertices (ascending) to the least-loaded GPU,
  * computed in closed form (greedy == (level, gpu)-ordered slot filling).

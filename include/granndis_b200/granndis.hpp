@@ -220,6 +220,51 @@ EquivalenceReport equivalence_check(const Graph& g, const Partition& server_part
                                     std::uint32_t layers, std::uint64_t seed,
                                     std::uint32_t feature_dim = 8, std::uint32_t hidden_dim = 8);
 
+// ---- model description (cost_model.hpp:24-29) ------------------------------------------
+struct ModelSpec {
+    std::uint32_t layers = 1;
+    std::uint32_t hidden_dim = 64;
+    std::uint32_t feature_dim = 64;
+    double expansion_factor = 1.5;  // per-layer dependency growth rate
+};
+
+// ---- cooperative batch planning (batch_plan.hpp:13-69) ----------------------------------
+// Device implementation: every group of one R is evaluated in batched launches
+// (gdx_cobatch_eval), the R scan reads one count array per R back; only the chosen
+// R's vertex lists are materialised.
+inline constexpr std::uint64_t kUnlimitedMemory = std::numeric_limits<std::uint64_t>::max();
+inline constexpr std::uint32_t kBytesPerScalar = 4;
+
+enum class BatchStrategy { FetchThenSplit, SplitThenFetch };
+
+struct Batch {
+    std::vector<VertexId> target_vertices;              // sorted
+    std::vector<VertexId> vertices;                     // sorted dependency universe
+    std::vector<std::uint64_t> mfg_vertices_per_layer;  // [0] inputs .. [L] targets
+    std::uint64_t est_memory_bytes = 0;
+};
+
+struct BatchPlan {
+    std::uint32_t worker_id = 0;
+    BatchStrategy strategy = BatchStrategy::FetchThenSplit;
+    std::uint32_t layers = 0;
+    std::vector<Batch> batches;
+    std::uint32_t batch_count() const noexcept { return static_cast<std::uint32_t>(batches.size()); }
+};
+
+std::uint64_t estimate_batch_memory(const Batch& b, const ModelSpec& model);
+BatchPlan plan_cobatch(const DependencySubgraph& sub, const Graph& g, std::uint32_t layers,
+                       const SamplingConfig& cfg, std::uint64_t mem_budget, const ModelSpec& model);
+BatchPlan plan_cobatch_fixed_r(const DependencySubgraph& sub, const Graph& g, std::uint32_t layers,
+                               const SamplingConfig& cfg, std::uint32_t r, const ModelSpec& model);
+// The paper's split-then-fetch comparison baseline (per-GPU chunks, layer-wise fanout);
+// host C++, not on the training path.
+BatchPlan plan_minibatch_baseline(const Graph& g, const Partition& gpu_partition, std::uint32_t gpu_id,
+                                  std::uint32_t layers, std::uint32_t fanout_per_layer,
+                                  std::uint64_t mem_budget, const ModelSpec& model, std::uint64_t seed);
+std::string plan_to_json(const BatchPlan& plan);
+void save_plan_json(const BatchPlan& plan, const std::string& path);
+
 // ---- cooperative split (sim.cpp:81-102, re-exported) ------------------------------------
 std::vector<std::vector<VertexId>> split_batch(const std::vector<VertexId>& batch_vertices,
                                                const Partition& server_partition,

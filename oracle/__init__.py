@@ -170,6 +170,10 @@ def ref() -> C.CDLL:
         L.grr_plan_cobatch_fixed_r.argtypes = [vp, _u32p, C.c_uint32, C.c_uint32, C.c_int,
                                                C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                                C.c_uint32, C.c_uint32, C.c_uint32]
+        L.grr_plan_cobatch.restype = vp
+        L.grr_plan_cobatch.argtypes = [vp, _u32p, C.c_uint32, C.c_uint32, C.c_int,
+                                       C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                       C.c_uint64, C.c_uint32, C.c_uint32]
         L.grr_plan_batches.restype = C.c_uint32
         L.grr_plan_batches.argtypes = [vp]
         L.grr_plan_batch_sizes.argtypes = [vp, C.c_uint32, C.POINTER(C.c_uint64),
@@ -446,6 +450,34 @@ def make_labels(n: int, classes: int, seed: int) -> np.ndarray:
     c = np.uint64(classes)
     # (x * c) >> 64 computed exactly with 32-bit halves
     return ((hi * c + ((lo * c) >> np.uint64(32))) >> np.uint64(32)).astype(np.int32)
+
+
+def ref_plan(g_handle, hop: np.ndarray, server: int, hop_limit: int, sampled: bool, layers: int,
+             max_hop: int, fanout: int, seed: int, hidden: int, feat: int, r: int = 0,
+             budget: int = 0):
+    """The compiled reference's plan_cobatch_fixed_r (r > 0) or plan_cobatch (budget):
+    a list of (targets, vertices, mfg, bytes) per batch, or the error string."""
+    R = ref()
+    hop = np.ascontiguousarray(hop, np.uint32)
+    if r:
+        p = R.grr_plan_cobatch_fixed_r(g_handle, hop, server, hop_limit, int(sampled), layers, max_hop,
+                                       fanout, seed, r, hidden, feat)
+    else:
+        p = R.grr_plan_cobatch(g_handle, hop, server, hop_limit, int(sampled), layers, max_hop,
+                               fanout, seed, budget, hidden, feat)
+    if not p:
+        return R.grr_last_error().decode()
+    out = []
+    for b in range(R.grr_plan_batches(p)):
+        nt, nv, by = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        R.grr_plan_batch_sizes(p, b, C.byref(nt), C.byref(nv), C.byref(by))
+        t = np.zeros(max(nt.value, 1), np.uint32)
+        v = np.zeros(max(nv.value, 1), np.uint32)
+        m = np.zeros(layers + 1, np.uint64)
+        R.grr_plan_batch_copy(p, b, t, v, m)
+        out.append((t[:nt.value], v[:nv.value], [int(x) for x in m], int(by.value)))
+    R.grr_plan_free(p)
+    return out
 
 
 def rng_draws(seed: int, k1: int, k2: int, count: int) -> np.ndarray:

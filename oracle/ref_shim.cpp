@@ -291,6 +291,21 @@ void* grr_plan_cobatch_fixed_r(void* g, const std::uint32_t* hop, std::uint32_t 
         return nullptr;
     return out;
 }
+// plan_cobatch (batch_plan.cpp:155-180): the budgeted R scan; nullptr + error on
+// failure (grr_last_error names the category, e.g. capacity).
+void* grr_plan_cobatch(void* g, const std::uint32_t* hop, std::uint32_t server, std::uint32_t hop_limit,
+                       int sampled, std::uint32_t layers, std::uint32_t max_hop, std::uint32_t fanout,
+                       std::uint64_t seed, std::uint64_t budget, std::uint32_t hidden, std::uint32_t feat) {
+    PlanOut* out = nullptr;
+    if (guarded([&] {
+            const Graph& gr = *static_cast<Graph*>(g);
+            DependencySubgraph sub = sub_from_hops(gr, hop, server, hop_limit, sampled);
+            ModelSpec m{layers, hidden, feat, 1.5};
+            out = new PlanOut{plan_cobatch(sub, gr, layers, SamplingConfig{max_hop, fanout, seed}, budget, m)};
+        }))
+        return nullptr;
+    return out;
+}
 std::uint32_t grr_plan_batches(void* p) { return static_cast<PlanOut*>(p)->plan.batch_count(); }
 void grr_plan_batch_sizes(void* p, std::uint32_t b, std::uint64_t* nt, std::uint64_t* nv,
                           std::uint64_t* bytes) {

@@ -86,6 +86,8 @@ _SIGS = {
     "gdx_induced_count": (C.c_int, [vp, vp, u32, vp, vp, C.POINTER(u64), vp]),
     "gdx_peel_mfg": (C.c_int, [vp, vp, u32, vp, vp, u64, u32, vp, vp, vp]),
     "gdx_split_batch": (C.c_int, [vp, u64, vp, vp, u32, u32, vp, vp, vp]),
+    "gdx_cobatch_eval": (C.c_int, [vp, vp, u32, vp, vp, vp, u32, u32, u32, u64, u32, u64, vp, vp, vp, vp,
+                                   vp]),
     "gdx_order_by_hop": (C.c_int, [vp, u32, u32, vp, vp, vp, C.POINTER(u32), vp]),
     "gdx_local_csr": (C.c_int, [vp, vp, vp, u32, vp, vp, vp, vp, vp]),
     "gdx_gather_rows": (C.c_int, [vp, u64, vp, u32, u32, vp, u64, vp]),

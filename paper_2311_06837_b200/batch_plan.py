@@ -128,21 +128,73 @@ def split_targets_random(targets: np.ndarray, r: int, seed: int) -> list:
     return [t[a == k] for k in range(r)]
 
 
+def _workspace_bytes(dev) -> int:
+    """Device workspace for one gdx_cobatch_eval call (groups evaluated together)."""
+    free, _ = torch.cuda.mem_get_info(dev)
+    return int(max(1 << 26, min(free // 4, 32 << 30)))
+
+
+def cobatch_eval(g: Graph, universe: torch.Tensor, groups: list, layers: int, cfg: SamplingConfig,
+                 emit: bool = False):
+    """Every group's batch closure + MFG counts in batched device launches
+    (gdx_cobatch_eval; batch_plan.cpp:28-112 for all groups of one R).  Returns
+    (sizes, mfg[groups][layers+1], vertex lists or None)."""
+    dg = g.device()
+    dev = dg.row_ptr.device
+    n = g.num_vertices()
+    G = len(groups)
+    off = np.zeros(G + 1, np.uint64)
+    off[1:] = np.cumsum([len(x) for x in groups])
+    flat = (np.concatenate([np.asarray(x, np.uint32) for x in groups]) if int(off[-1])
+            else np.zeros(1, np.uint32))
+    t = torch.from_numpy(flat.view(np.int32)).to(dev)
+    sizes = np.zeros(G, np.uint64)
+    mfg = np.zeros(G * (layers + 1), np.uint64)
+    ws = _workspace_bytes(dev)
+    args = (dg.row_ptr.data_ptr(), dg.col.data_ptr(), n, universe.data_ptr(), t.data_ptr(),
+            off.ctypes.data, G, cfg.max_hop, cfg.fanout & 0xFFFFFFFF, cfg.seed, layers, ws,
+            sizes.ctypes.data, mfg.ctypes.data)
+    call("gdx_cobatch_eval", *args, None, None, stream_handle())
+    verts = None
+    if emit:
+        voff = np.zeros(G + 1, np.uint64)
+        voff[1:] = np.cumsum(sizes)
+        out = torch.empty(max(int(voff[-1]), 1), dtype=torch.int32, device=dev)
+        call("gdx_cobatch_eval", *args, out.data_ptr(), voff.ctypes.data, stream_handle())
+        h = out.cpu().numpy().view(np.uint32)
+        verts = [h[int(voff[i]):int(voff[i + 1])].copy() for i in range(G)]
+    return sizes, mfg.reshape(G, layers + 1), verts
+
+
+def _target_groups(sub: DependencySubgraph, g: Graph, r: int, cfg: SamplingConfig,
+                   target_split: str) -> list:
+    if target_split == "random":
+        return split_targets_random(sub.inner_vertices, r, cfg.seed)
+    if target_split == "mincut":
+        return split_targets_mincut(g, sub.inner_vertices, r, cfg.seed)
+    raise InputError(f"plan_cobatch: unknown target split {target_split!r}")
+
+
+def _universe(sub: DependencySubgraph, g: Graph) -> torch.Tensor:
+    dev = g.device().row_ptr.device
+    m = _mask(g.num_vertices(), np.concatenate([sub.inner_vertices, sub.halo_vertices]), dev)
+    return m
+
+
+def _plan_from(sub, layers, groups, sizes, mfg, verts, model) -> BatchPlan:
+    plan = BatchPlan(sub.server_id, "fetch_then_split", layers)
+    for i, grp in enumerate(groups):
+        b = Batch(np.asarray(grp, np.uint32), verts[i], [int(c) for c in mfg[i]])
+        b.est_memory_bytes = estimate_batch_memory(b, model)
+        plan.batches.append(b)
+    return plan
+
+
 def _build_cobatch(sub: DependencySubgraph, g: Graph, layers: int, cfg: SamplingConfig, r: int,
                    model: ModelSpec, target_split: str = "mincut") -> BatchPlan:
-    universe = np.zeros(g.num_vertices(), np.uint8)
-    universe[sub.inner_vertices] = 1
-    universe[sub.halo_vertices] = 1
-    plan = BatchPlan(sub.server_id, "fetch_then_split", layers)
-    if target_split == "random":
-        groups = split_targets_random(sub.inner_vertices, r, cfg.seed)
-    elif target_split == "mincut":
-        groups = split_targets_mincut(g, sub.inner_vertices, r, cfg.seed)
-    else:
-        raise InputError(f"plan_cobatch: unknown target split {target_split!r}")
-    for group in groups:
-        plan.batches.append(make_batch(g, universe, group, layers, cfg, model))
-    return plan
+    groups = _target_groups(sub, g, r, cfg, target_split)
+    sizes, mfg, verts = cobatch_eval(g, _universe(sub, g), groups, layers, cfg, emit=True)
+    return _plan_from(sub, layers, groups, sizes, mfg, verts, model)
 
 
 def plan_cobatch_fixed_r(sub: DependencySubgraph, g: Graph, layers: int, cfg: SamplingConfig,
@@ -151,24 +203,37 @@ def plan_cobatch_fixed_r(sub: DependencySubgraph, g: Graph, layers: int, cfg: Sa
     split for split_targets_random (papers-scale plans)."""
     if r == 0:
         raise InputError("plan_cobatch: batch count must be >= 1")
+    require_cuda()
     capped = min(r, max(1, len(sub.inner_vertices)))
     return _build_cobatch(sub, g, layers, cfg, capped, model, target_split)
 
 
+def _est_bytes(mfg_row, model: ModelSpec) -> int:
+    return sum(int(c) * (model.feature_dim if l == 0 else model.hidden_dim) * kBytesPerScalar
+               for l, c in enumerate(mfg_row))
+
+
 def plan_cobatch(sub: DependencySubgraph, g: Graph, layers: int, cfg: SamplingConfig,
-                 mem_budget: int, model: ModelSpec) -> BatchPlan:
-    """batch_plan.cpp:155-180: smallest R whose batches all fit the budget (linear scan)."""
+                 mem_budget: int, model: ModelSpec, target_split: str = "mincut") -> BatchPlan:
+    """batch_plan.cpp:155-180: the smallest R whose batches all fit the budget, by the
+    reference's linear scan (max batch memory is not monotone in R, :162-163).  Each R
+    is one batched device evaluation of all its groups (no per-hop host syncs); only
+    the winning R's vertex lists are materialised."""
     if mem_budget == 0:
         raise InputError("plan_cobatch: mem_budget must be > 0")
+    require_cuda()
+    universe = _universe(sub, g)
     max_r = max(1, len(sub.inner_vertices))
-    plan = None
     for r in range(1, max_r + 1):
-        plan = _build_cobatch(sub, g, layers, cfg, r, model)
-        if max(b.est_memory_bytes for b in plan.batches) <= mem_budget:
-            return plan
-    worst = max(plan.batches, key=lambda b: b.est_memory_bytes)
-    first = int(worst.target_vertices[0]) if len(worst.target_vertices) else 0
-    raise CapacityError(f"single-target batch for vertex {first} needs {worst.est_memory_bytes} "
+        groups = _target_groups(sub, g, r, cfg, target_split)
+        sizes, mfg, _ = cobatch_eval(g, universe, groups, layers, cfg)
+        est = [_est_bytes(row, model) for row in mfg]
+        if max(est) <= mem_budget:
+            sizes, mfg, verts = cobatch_eval(g, universe, groups, layers, cfg, emit=True)
+            return _plan_from(sub, layers, groups, sizes, mfg, verts, model)
+    w = int(np.argmax(est))
+    first = int(groups[w][0]) if len(groups[w]) else 0
+    raise CapacityError(f"single-target batch for vertex {first} needs {est[w]} "
                         f"bytes, budget is {mem_budget}")
 
 

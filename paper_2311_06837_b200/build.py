@@ -26,7 +26,8 @@ CU_FLAGS = ARCH + COMMON + ["-Xcompiler", "-fPIC,-ffp-contract=off", "--expt-rel
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
              "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include"]
 
-SOURCES_CU = ["aggregate.cu", "gemm_tcgen05.cu", "dense_ops.cu", "sampling.cu", "exchange.cu"]
+SOURCES_CU = ["aggregate.cu", "gemm_tcgen05.cu", "dense_ops.cu", "sampling.cu", "exchange.cu",
+              "cobatch_plan.cu"]
 SOURCES_CXX = ["host.cpp"]
 
 
@@ -103,7 +104,7 @@ def build_ref_suite(verbose: bool = False, force: bool = False):
         return None
     build_cxx_api(verbose, force)
     srcs = [os.path.join(REF_TESTS, "test_reference_gnn.cpp"), os.path.join(REF_TESTS, "test_extract.cpp"),
-            os.path.join(ROOT, "tests", "cxx", "doctest_main.cpp")]
+            os.path.join(REF_TESTS, "test_batch_plan.cpp"), os.path.join(ROOT, "tests", "cxx", "doctest_main.cpp")]
     if force or _stale(SUITE_OUT, srcs + [API_OUT]):
         cmd = ["g++", "-O2", "-std=c++20", "-I" + os.path.join(ROOT, "tests", "cxx"),
                "-I" + os.path.join(ROOT, "include", "granndis_compat"), "-I" + os.path.join(ROOT, "include"),

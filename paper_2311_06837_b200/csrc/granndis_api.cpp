@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <set>
@@ -622,6 +623,249 @@ EquivalenceReport equivalence_check(const Graph& g, const Partition& p, std::uin
         rep.max_deviation = std::max(rep.max_deviation, dev);
     }
     return rep;
+}
+
+// ======================= cooperative batch planning ========================
+std::uint64_t estimate_batch_memory(const Batch& b, const ModelSpec& model) {
+    std::uint64_t bytes = 0;
+    for (std::size_t l = 0; l < b.mfg_vertices_per_layer.size(); ++l)
+        bytes += b.mfg_vertices_per_layer[l] * (l == 0 ? model.feature_dim : model.hidden_dim) * kBytesPerScalar;
+    return bytes;
+}
+
+namespace {
+
+// Target groups of one R (batch_plan.cpp:114-126): the inner vertices split by the
+// host min-cut of their induced subgraph (bit-identical to the reference's).
+std::vector<std::vector<VertexId>> target_groups(const Graph& g, const std::vector<VertexId>& targets,
+                                                 std::uint32_t r, std::uint64_t seed) {
+    if (r <= 1 || targets.size() <= 1) return {targets};
+    InducedSubgraph inner = induced_subgraph(g, targets);
+    Partition p = partition_mincut(inner.graph, r, seed);
+    std::vector<std::vector<VertexId>> groups(r);
+    for (VertexId i = 0; i < inner.global_ids.size(); ++i) groups[p.assignment[i]].push_back(inner.global_ids[i]);
+    for (auto& grp : groups) std::sort(grp.begin(), grp.end());
+    return groups;
+}
+
+// The planner's device context: graph + server universe resident for the whole R scan.
+struct PlanDevice {
+    DevCSR csr;
+    Dev<uint8_t> universe;
+    uint32_t n = 0;
+    PlanDevice(const Graph& g, const DependencySubgraph& sub) : csr(upload(g)), n(g.num_vertices()) {
+        std::vector<uint8_t> u(n, 0);
+        for (VertexId v : sub.inner_vertices) u[v] = 1;
+        for (VertexId v : sub.halo_vertices) u[v] = 1;
+        universe = Dev<uint8_t>(u.data(), n);
+    }
+};
+
+uint64_t workspace_budget() {
+    size_t free_b = 0, total = 0;
+    if (cudaMemGetInfo(&free_b, &total) != cudaSuccess) return 1ull << 28;
+    return std::max<uint64_t>(1ull << 26, std::min<uint64_t>(free_b / 4, 32ull << 30));
+}
+
+// One batched device evaluation of every group (gdx_cobatch_eval).  With plan: the
+// batches (vertex lists included) are written into it.
+std::vector<std::vector<std::uint64_t>> eval_groups(const PlanDevice& d,
+                                                    const std::vector<std::vector<VertexId>>& groups,
+                                                    std::uint32_t layers, const SamplingConfig& cfg,
+                                                    const ModelSpec& model, BatchPlan* plan) {
+    const uint32_t G = static_cast<uint32_t>(groups.size());
+    std::vector<uint64_t> off(G + 1, 0);
+    std::vector<uint32_t> flat;
+    for (uint32_t i = 0; i < G; ++i) {
+        flat.insert(flat.end(), groups[i].begin(), groups[i].end());
+        off[i + 1] = flat.size();
+    }
+    Dev<uint32_t> t(flat.data(), flat.size());
+    std::vector<uint64_t> sizes(G), mfg(size_t(G) * (layers + 1));
+    const uint64_t ws = workspace_budget();
+    check(gdx_cobatch_eval(d.csr.rp.p, d.csr.col.p, d.n, d.universe.p, t.p, off.data(), G, cfg.max_hop,
+                           cfg.fanout, cfg.seed, layers, ws, sizes.data(), mfg.data(), nullptr, nullptr,
+                           nullptr));
+    std::vector<std::vector<std::uint64_t>> counts(G);
+    for (uint32_t i = 0; i < G; ++i)
+        counts[i].assign(mfg.begin() + size_t(i) * (layers + 1), mfg.begin() + size_t(i + 1) * (layers + 1));
+    if (plan) {
+        std::vector<uint64_t> voff(G + 1, 0);
+        for (uint32_t i = 0; i < G; ++i) voff[i + 1] = voff[i] + sizes[i];
+        Dev<uint32_t> verts(std::max<uint64_t>(voff[G], 1), false);
+        check(gdx_cobatch_eval(d.csr.rp.p, d.csr.col.p, d.n, d.universe.p, t.p, off.data(), G, cfg.max_hop,
+                               cfg.fanout, cfg.seed, layers, ws, sizes.data(), mfg.data(), verts.p,
+                               voff.data(), nullptr));
+        std::vector<uint32_t> hv = verts.download();
+        for (uint32_t i = 0; i < G; ++i) {
+            Batch b;
+            b.target_vertices = groups[i];
+            b.vertices.assign(hv.begin() + voff[i], hv.begin() + voff[i + 1]);
+            b.mfg_vertices_per_layer = counts[i];
+            b.est_memory_bytes = estimate_batch_memory(b, model);
+            plan->batches.push_back(std::move(b));
+        }
+    }
+    return counts;
+}
+
+BatchPlan empty_plan(const DependencySubgraph& sub, std::uint32_t layers) {
+    BatchPlan plan;
+    plan.worker_id = sub.server_id;
+    plan.strategy = BatchStrategy::FetchThenSplit;
+    plan.layers = layers;
+    return plan;
+}
+
+[[noreturn]] void capacity_failure(const std::vector<VertexId>& worst_targets, std::uint64_t bytes,
+                                   std::uint64_t budget) {
+    throw CapacityError("single-target batch for vertex " +
+                        std::to_string(worst_targets.empty() ? 0 : worst_targets.front()) + " needs " +
+                        std::to_string(bytes) + " bytes, budget is " + std::to_string(budget));
+}
+
+}  // namespace
+
+BatchPlan plan_cobatch_fixed_r(const DependencySubgraph& sub, const Graph& g, std::uint32_t layers,
+                               const SamplingConfig& cfg, std::uint32_t r, const ModelSpec& model) {
+    if (r == 0) throw InputError("plan_cobatch: batch count must be >= 1");
+    const std::uint32_t capped =
+        std::min<std::uint32_t>(r, std::max<std::uint32_t>(1, static_cast<std::uint32_t>(sub.inner_vertices.size())));
+    PlanDevice d(g, sub);
+    BatchPlan plan = empty_plan(sub, layers);
+    eval_groups(d, target_groups(g, sub.inner_vertices, capped, cfg.seed), layers, cfg, model, &plan);
+    return plan;
+}
+
+// batch_plan.cpp:155-180: the reference's linear scan over R (the worst batch's bytes
+// are not monotone in R); each R is one batched device evaluation, only the first R
+// that fits is materialised.
+BatchPlan plan_cobatch(const DependencySubgraph& sub, const Graph& g, std::uint32_t layers,
+                       const SamplingConfig& cfg, std::uint64_t mem_budget, const ModelSpec& model) {
+    if (mem_budget == 0) throw InputError("plan_cobatch: mem_budget must be > 0");
+    const std::uint32_t max_r = std::max<std::uint32_t>(1, static_cast<std::uint32_t>(sub.inner_vertices.size()));
+    PlanDevice d(g, sub);
+    std::vector<std::vector<VertexId>> groups;
+    std::uint64_t worst = 0;
+    std::size_t worst_i = 0;
+    for (std::uint32_t r = 1; r <= max_r; ++r) {
+        groups = target_groups(g, sub.inner_vertices, r, cfg.seed);
+        auto counts = eval_groups(d, groups, layers, cfg, model, nullptr);
+        worst = 0;
+        worst_i = 0;
+        for (std::size_t i = 0; i < counts.size(); ++i) {
+            Batch b;
+            b.mfg_vertices_per_layer = counts[i];
+            const std::uint64_t bytes = estimate_batch_memory(b, model);
+            if (bytes > worst) {
+                worst = bytes;
+                worst_i = i;
+            }
+        }
+        if (worst <= mem_budget) {
+            BatchPlan plan = empty_plan(sub, layers);
+            eval_groups(d, groups, layers, cfg, model, &plan);
+            return plan;
+        }
+    }
+    capacity_failure(groups[worst_i], worst, mem_budget);
+}
+
+// The split-then-fetch baseline (the planner the paper compares against): each chunk
+// of the GPU's own vertices grows GraphSAGE-style layered dependency sets from the
+// whole graph -- at every step each vertex already in the set keeps at most
+// fanout_per_layer neighbours of its (seed, vertex, layer)-keyed permutation.  Host
+// code: a visited stamp per vertex (no O(V) clearing per batch), one scan per chunk.
+BatchPlan plan_minibatch_baseline(const Graph& g, const Partition& gpu_partition, std::uint32_t gpu_id,
+                                  std::uint32_t layers, std::uint32_t fanout_per_layer,
+                                  std::uint64_t mem_budget, const ModelSpec& model, std::uint64_t seed) {
+    if (mem_budget == 0) throw InputError("plan_minibatch_baseline: mem_budget must be > 0");
+    if (gpu_id >= gpu_partition.num_parts) throw InputError("plan_minibatch_baseline: gpu id out of range");
+    const std::vector<VertexId> own = gpu_partition.members(gpu_id);
+    std::vector<std::uint32_t> stamp(g.num_vertices(), 0);
+    std::uint32_t epoch = 0;
+    auto build = [&](std::vector<VertexId> targets) {
+        ++epoch;
+        Batch b;
+        b.target_vertices = std::move(targets);
+        std::vector<VertexId> set = b.target_vertices;
+        for (VertexId v : set) stamp[v] = epoch;
+        b.mfg_vertices_per_layer.assign(layers + 1, 0);
+        b.mfg_vertices_per_layer[layers] = set.size();
+        std::vector<VertexId> picks;
+        for (std::uint32_t step = 1; step <= layers; ++step) {
+            const std::uint32_t key = layers - step + 1;
+            const std::size_t before = set.size();
+            for (std::size_t i = 0; i < before; ++i) {
+                const auto nb = g.neighbors(set[i]);
+                picks.assign(nb.begin(), nb.end());
+                if (fanout_per_layer != kUnlimitedFanout && picks.size() > fanout_per_layer) {
+                    KeyedRng rng(seed, set[i], key);
+                    keyed_shuffle(picks, rng);
+                    picks.resize(fanout_per_layer);
+                }
+                for (VertexId u : picks)
+                    if (stamp[u] != epoch) {
+                        stamp[u] = epoch;
+                        set.push_back(u);
+                    }
+            }
+            b.mfg_vertices_per_layer[layers - step] = set.size();
+        }
+        std::sort(set.begin(), set.end());
+        b.vertices = std::move(set);
+        b.est_memory_bytes = estimate_batch_memory(b, model);
+        return b;
+    };
+    BatchPlan plan;
+    plan.worker_id = gpu_id;
+    plan.strategy = BatchStrategy::SplitThenFetch;
+    plan.layers = layers;
+    const std::uint32_t max_r = std::max<std::uint32_t>(1, static_cast<std::uint32_t>(own.size()));
+    for (std::uint32_t r = 1; r <= max_r; ++r) {
+        plan.batches.clear();
+        std::uint64_t worst = 0;
+        const std::size_t base = own.size() / r, rem = own.size() % r;
+        std::size_t pos = 0;
+        for (std::uint32_t i = 0; i < r; ++i) {
+            const std::size_t len = base + (i < rem ? 1 : 0);
+            plan.batches.push_back(build({own.begin() + pos, own.begin() + pos + len}));
+            pos += len;
+            worst = std::max(worst, plan.batches.back().est_memory_bytes);
+        }
+        if (worst <= mem_budget) return plan;
+    }
+    const Batch* w = &plan.batches.front();
+    for (const Batch& b : plan.batches)
+        if (b.est_memory_bytes > w->est_memory_bytes) w = &b;
+    capacity_failure(w->target_vertices, w->est_memory_bytes, mem_budget);
+}
+
+std::string plan_to_json(const BatchPlan& plan) {
+    std::string o = "{\n  \"worker_id\": " + std::to_string(plan.worker_id) + ",\n  \"strategy\": \"" +
+                    (plan.strategy == BatchStrategy::FetchThenSplit ? "fetch_then_split" : "split_then_fetch") +
+                    "\",\n  \"layers\": " + std::to_string(plan.layers) + ",\n  \"batch_count\": " +
+                    std::to_string(plan.batch_count()) + ",\n  \"batches\": [";
+    for (std::size_t i = 0; i < plan.batches.size(); ++i) {
+        const Batch& b = plan.batches[i];
+        o += (i ? ",\n    {" : "\n    {");
+        o += "\"targets\": " + std::to_string(b.target_vertices.size()) + ", \"vertices\": " +
+             std::to_string(b.vertices.size()) + ", \"mfg_vertices_per_layer\": [";
+        for (std::size_t l = 0; l < b.mfg_vertices_per_layer.size(); ++l)
+            o += (l ? ", " : "") + std::to_string(b.mfg_vertices_per_layer[l]);
+        o += "], \"est_memory_bytes\": " + std::to_string(b.est_memory_bytes) + "}";
+    }
+    o += plan.batches.empty() ? "]\n}" : "\n  ]\n}";
+    return o;
+}
+
+void save_plan_json(const BatchPlan& plan, const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw InputError("cannot open output file: " + path);
+    const std::string s = plan_to_json(plan);
+    std::fputs(s.c_str(), f);
+    std::fputs("\n", f);
+    std::fclose(f);
 }
 
 // ======================= cooperative split ================================
