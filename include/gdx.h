@@ -327,6 +327,76 @@ int gdx_gather_split_rows(const uint16_t* src_hi, const uint16_t* src_lo, uint64
                           const uint32_t* idx, uint32_t rows, uint32_t cols, uint16_t* out_hi,
                           uint16_t* out_lo, uint64_t ld_out, gdx_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Training epoch as a C-ABI object (the benchmarked step, driven from C/C++ with
+ * no Python): the reference's layer model (reference_gnn.cpp:64-147) plus the
+ * north_star's softmax cross-entropy, backward and SGD, on this library's
+ * kernels.  One trainer per GPU; world > 1 ranks exchange rows and weight
+ * gradients through one CUDA-IPC arena per rank (gdx_trainer_ipc_export on every
+ * rank, the 64-byte blobs gathered by the caller -- MPI, sockets, torch -- then
+ * gdx_trainer_connect on every rank).  No NCCL on the data path.
+ * ---------------------------------------------------------------------- */
+enum { GDX_MODEL_SUM = 0, GDX_MODEL_GCN = 1, GDX_MODEL_SAGE = 2 };
+typedef struct gdx_trainer gdx_trainer;
+typedef struct gdx_trainer_config {
+    int kind;                 /* GDX_MODEL_*: Sum (reference), normalised GCN, SAGE-mean */
+    uint32_t layers;          /* L */
+    const uint32_t* dims;     /* [L+1]: feature width, hidden widths, classes (<= 256) */
+    float lr;                 /* SGD step */
+    uint32_t rank, world;     /* world <= 8 (<= 7 peers) */
+    int device;               /* CUDA ordinal */
+    uint64_t feature_seed;    /* make_features stream seed of the inputs (reference_gnn.cpp:11-16) */
+    uint64_t label_seed;      /* labels: KeyedRng(seed, v, "labl").next_below(classes) */
+    int use_graph;            /* capture the epoch as a CUDA graph after two eager epochs */
+    int no_agg_first;         /* 1: widening SAGE output layers stay transform-first */
+    uint32_t push_ctas;       /* CTAs of the NVLink push kernel (0: 32) */
+    double peer_timeout_s;    /* peer wait traps after this (0: 20 s); a trap poisons the context */
+} gdx_trainer_config;
+typedef struct gdx_trainer_graph {
+    uint32_t num_vertices;          /* V of the whole graph */
+    uint64_t nnz;                   /* full graph: row_offsets[V] */
+    const uint64_t* row_offsets;    /* HOST. full graph: [V+1]; local subgraph: [local_rows+1] */
+    const uint32_t* cols;           /* HOST. full graph: global ids; local subgraph: local ids */
+    /* local subgraph (EAS / preload mode) when local_rows > 0: local ids ordered so that
+     * the rows layer l reads / writes are prefixes rows_in[l] / rows_out[l]
+     * (forward_server_local's hop mask, reference_gnn.cpp:119-137); the loss covers rows
+     * < loss_rows, normalised by loss_count (the loss rows of all ranks). */
+    uint64_t local_rows;
+    const uint32_t* rows_in;        /* HOST [layers], nullable (= local_rows) */
+    const uint32_t* rows_out;       /* HOST [layers] */
+    uint32_t loss_rows;
+    double loss_count;
+    const uint32_t* global_ids;     /* HOST [local_rows]: stream row of each local row */
+} gdx_trainer_graph;
+int gdx_trainer_create(const gdx_trainer_config* cfg, const gdx_trainer_graph* graph, gdx_trainer** out);
+int gdx_trainer_destroy(gdx_trainer* t);
+/* Weights in reference order: per layer W [out x in] (Sum, GCN) or W_self, W_neigh (SAGE),
+ * row-major fp64, all layers concatenated; count = gdx_trainer_weight_count. */
+uint64_t gdx_trainer_weight_count(const gdx_trainer* t);
+int gdx_trainer_init_weights(gdx_trainer* t, uint64_t seed, int he_init);  /* (seed, "weig") stream */
+int gdx_trainer_set_weights(gdx_trainer* t, const double* w, uint64_t count);
+int gdx_trainer_get_weights(gdx_trainer* t, double* w, uint64_t count);
+int gdx_trainer_get_grads(gdx_trainer* t, double* g, uint64_t count);   /* last epoch's dW (summed) */
+int gdx_trainer_ipc_export(gdx_trainer* t, void* blob64);
+int gdx_trainer_connect(gdx_trainer* t, const void* blobs);  /* world x 64 bytes, rank order */
+/* One epoch (forward, loss, backward, gradient all-reduce, SGD) on the trainer's stream.
+ * loss_out (nullable): the mean loss, read back (synchronising). */
+int gdx_trainer_epoch(gdx_trainer* t, double* loss_out);
+/* End-to-end inputs from HOST memory: stage_inputs enqueues one contiguous H2D of this
+ * rank's feature block [local rows x F] fp32 (pinned memory overlaps the running epoch)
+ * and labels (nullable) on a copy stream, double-buffered; step_staged consumes the
+ * oldest staged block (split into the GEMM operand) and runs one epoch. */
+int gdx_trainer_stage_inputs(gdx_trainer* t, const float* x_host, const int32_t* labels_host);
+int gdx_trainer_step_staged(gdx_trainer* t, int with_labels, double* loss_out);
+/* The trainer's stream (cudaStream_t) for event timing by the caller. */
+void* gdx_trainer_stream(gdx_trainer* t);
+/* out[0..]: local rows, local nnz, first row, gathered rows, loss rows, loss count,
+ * graph captured, aggregate-first output layer, local-source nnz. */
+int gdx_trainer_info(const gdx_trainer* t, uint64_t* out, uint32_t count);
+/* Per-aggregation CUDA events on eager epochs (on = 1); reading (non-null outputs)
+ * returns the total ms, launch count and algorithmic bytes since on. */
+int gdx_trainer_profile(gdx_trainer* t, int on, double* ms, uint64_t* launches, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
              "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include"]
 
 SOURCES_CU = ["aggregate.cu", "gemm_tcgen05.cu", "dense_ops.cu", "sampling.cu", "exchange.cu",
-              "cobatch_plan.cu"]
+              "cobatch_plan.cu", "trainer.cu"]
 SOURCES_CXX = ["host.cpp"]
 
 
@@ -116,7 +116,28 @@ def build_ref_suite(verbose: bool = False, force: bool = False):
     return SUITE_OUT
 
 
+CXX_TESTS = {"trainer_epoch": os.path.join(ROOT, "tests", "cxx", "trainer_epoch.cpp")}
+
+
+def build_cxx_tests(verbose: bool = False, force: bool = False) -> list:
+    """C/C++ host programs that drive the engine through include/gdx.h only
+    (no Python, no torch) -> build/<name>, linked against the in-tree libgdx.so."""
+    build(verbose, force)
+    out = []
+    for name, src in CXX_TESTS.items():
+        exe = os.path.join(ROOT, "build", name)
+        if force or _stale(exe, [src, OUT, os.path.join(ROOT, "include", "gdx.h")]):
+            cmd = ["g++", "-O2", "-std=c++17", "-I" + os.path.join(ROOT, "include"), src, "-L" + HERE, "-lgdx",
+                   "-Wl,-rpath,$ORIGIN/../paper_2311_06837_b200", "-o", exe]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True)
+        out.append(exe)
+    return out
+
+
 if __name__ == "__main__":
     build(verbose=True, force="--force" in sys.argv)
     build_cxx_api(verbose=True)
     build_ref_suite(verbose=True)
+    build_cxx_tests(verbose=True)
