@@ -37,6 +37,8 @@ MODES = {
     "nccl": {"GDX_EXCHANGE": "nccl"},                      # all_gather_into_tensor, overlapped
     "nccl-nooverlap": {"GDX_EXCHANGE": "nccl", "GDX_OVERLAP": "0"},
     "dw-overlap": {"GDX_DW_OVERLAP": "1"},                 # dW GEMMs on a side stream
+    "native": {"_NATIVE": "1"},                            # C-ABI trainer (csrc/trainer.cu): IPC arena
+    "native-eas": {"_NATIVE": "eas"},                      # C-ABI trainer, per-rank EAS subgraphs
 }
 FULL_CASES = (("sage", 5001, 24.0, [96, 64, 64, 41], 5),
               ("gcn", 3001, 10.0, [32, 32, 8], 4),
@@ -57,6 +59,40 @@ def weights_identical(tr, dev):
     dist.all_reduce(Wmax, op=dist.ReduceOp.MAX)
     dist.all_reduce(Wmin, op=dist.ReduceOp.MIN)
     return bool(torch.equal(Wmax, Wmin))
+
+
+def native_eas_cases(world, rank, dev):
+    """configs[2] semantics at N = world: rank r trains server r's preloaded EAS subgraph of
+    an 8-server partition; the dW all-reduce runs through the native trainer's IPC arena.
+    Checked against the torch-orchestrated trainer in the same mode (NCCL all-reduce) and
+    for bit-identical weights across ranks."""
+    import torch.distributed as dist
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.native import NativeTrainer
+    from paper_2311_06837_b200.train import FullGraphTrainer, ModelConfig
+
+    cases = []
+    for kind, dims, lr, init in (("gcn", [64] + [32] * 7 + [8], 0.5, "he"), ("sage", [48, 32, 32, 8], 0.5, "uniform")):
+        g = G.gen_random_graph(6000, 20.0, 13)
+        part = G.partition_random(g, 8, 1)
+        sub = G.extract_sampled(g, part, rank % 8, G.SamplingConfig(1, 15, 3))
+        cfg = ModelConfig(kind, dims, lr=lr, init=init)
+        a = NativeTrainer(g, cfg, rank=rank, world=world, subgraph=sub, pg=dist.group.WORLD)
+        b = FullGraphTrainer(g, cfg, rank=rank, world=world, subgraph=sub, pg=dist.group.WORLD)
+        la = [a.train_epoch() for _ in range(4)]
+        lb = [b.train_epoch() for _ in range(4)]
+        same = weights_identical(a, dev)
+        wa = np.concatenate([x.ravel() for x in a.get_weights()])
+        wb = np.concatenate([x.ravel() for x in b.get_weights()])
+        dist.barrier()
+        a.close()
+        b.close()
+        d = float(np.max(np.abs(np.array(la) - np.array(lb))))
+        wd = float(np.max(np.abs(wa - wb)))
+        cases.append({"kind": kind, "layers": len(dims) - 1, "losses_native": la, "losses_torch": lb,
+                      "max_abs_loss_diff": d, "max_abs_weight_diff": wd,
+                      "weights_identical_across_ranks": same, "ok": bool(same and d <= 1e-5 and wd <= 1e-5)})
+    return cases
 
 
 def main():
@@ -88,17 +124,32 @@ def main():
         if mode == "ring" and world <= 2:
             out["modes"][mode] = {"skipped": "ring order needs world > 2"}
             continue
-        set_mode(env)
+        set_mode({k: v for k, v in env.items() if not k.startswith("_")})
         res = {"env": env, "ok": True, "cases": []}
         t0 = time.time()
+        if env.get("_NATIVE") == "eas":
+            try:
+                res["cases"] = native_eas_cases(world, rank, dev)
+                res["ok"] = all(c["ok"] for c in res["cases"])
+            except Exception as e:  # noqa: BLE001
+                res["ok"], res["error"] = False, f"{type(e).__name__}: {e}"
+            res["seconds"] = round(time.time() - t0, 1)
+            out["modes"][mode] = res
+            out["ok"] &= res["ok"]
+            dist.barrier()
+            continue
+        Trainer = FullGraphTrainer
+        if env.get("_NATIVE"):
+            from paper_2311_06837_b200.native import NativeTrainer as Trainer
         try:
             for ci, (kind, n, deg, dims, epochs) in enumerate(FULL_CASES):
                 g = G.gen_random_graph(n, deg, 5)
                 cfg = ModelConfig(kind, dims, lr=0.5)
                 w0 = init_weights(cfg, 3)
-                tr = FullGraphTrainer(g, cfg, rank=rank, world=world, weights=w0, pg=dist.group.WORLD)
+                tr = Trainer(g, cfg, rank=rank, world=world, weights=w0, pg=dist.group.WORLD)
                 losses = [tr.train_epoch() for _ in range(epochs)]
                 same = weights_identical(tr, dev)
+                dist.barrier()   # no rank frees its IPC-shared buffers while a peer may touch them
                 tr.close()
                 case = {"kind": kind, "n": n, "dims": dims, "losses": losses,
                         "weights_identical_across_ranks": same}
@@ -116,6 +167,12 @@ def main():
                     case["ok"] = same and case["max_abs_loss_diff"] <= 1e-3
                     res["ok"] &= case["ok"]
                 res["cases"].append(case)
+            if env.get("_NATIVE"):
+                res["seconds"] = round(time.time() - t0, 1)
+                out["modes"][mode] = res
+                out["ok"] &= res["ok"]
+                dist.barrier()
+                continue
             # cooperative batching (config 5 semantics): one server, `world` GPUs share each batch
             dims = [48, 32, 32, 72]   # widening output layer: aggregate-first inside the batch
             g, hp, plan = _plan(4000, 10.0, 21, 1, world, 3, 3, G.SamplingConfig(1, 15, 3), dims)
