@@ -259,17 +259,6 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def launches_per_epoch(tr) -> int:
-    """libgdx kernel launches in one eager epoch (graph replays issue the same kernels)."""
-    import torch
-    from paper_2311_06837_b200 import _lib
-    torch.cuda.synchronize()
-    a = _lib.launch_count()
-    tr.train_epoch(sync_loss=False)
-    torch.cuda.synchronize()
-    return _lib.launch_count() - a
-
-
 def probe_l2_peak(torch, dev):
     """Live L2 read ceiling: the library's coalesced-stream probe over a 60 MB
     (L2-resident) buffer, best of 3, GB/s."""
@@ -306,7 +295,11 @@ def exchange_label(tr, world: int) -> str:
         return "1 GPU: no exchange"
     if getattr(tr, "subgraph_mode", False):
         return (f"x{world} self-contained preloaded subgraphs: no per-layer exchange, one dW "
-                f"all-reduce (NCCL) per step")
+                f"all-reduce per step over the CUDA-IPC arena (SM push, no NCCL)")
+    if not hasattr(tr, "p2p"):   # native trainer
+        return (f"row-partition x{world}: per-layer NVLink exchange (SM push kernel into every "
+                f"peer's IPC-mapped buffer, device arrival flags; local sources aggregated while "
+                f"it flies), dW all-reduce over the same IPC arena; no NCCL on the data path")
     if tr.p2p is not None:
         kind = {"sm": "SM push kernel", "ce": "copy engines", "mc": "NVSwitch multicast"}.get(
             tr.p2p.push_kind, tr.p2p.push_kind)
@@ -581,7 +574,8 @@ def main():
 
     import paper_2311_06837_b200 as G
     from paper_2311_06837_b200 import _lib
-    from paper_2311_06837_b200.train import L2_RESIDENT_BYTES, FullGraphTrainer, ModelConfig
+    from paper_2311_06837_b200.native import NativeTrainer
+    from paper_2311_06837_b200.train import L2_RESIDENT_BYTES, ModelConfig, agg_width
 
     t0 = time.perf_counter()
     g = G.gen_random_graph(args.n, args.degree, C["seed"])
@@ -593,51 +587,46 @@ def main():
         servers = C.get("servers", world)
         part = G.partition_random(g, servers, 1)
         sub = G.extract_sampled(g, part, rank % servers, G.SamplingConfig(m, k, sseed))
-    tr = FullGraphTrainer(g, cfg, rank=rank, world=world, pg=pg, subgraph=sub)
+    # the C-ABI trainer (csrc/trainer.cu): the whole epoch runs in libgdx's C++
+    t0 = time.perf_counter()
+    tr = NativeTrainer(g, cfg, rank=rank, world=world, pg=pg, subgraph=sub, use_graph=not args.eager)
+    t_setup = time.perf_counter() - t0
+    stream = tr.stream()
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # epoch 1 from the initial weights: its loss is the parity anchor against the oracle
+    # epoch 1 from the initial weights (eager): the parity anchor, and the launch count
+    l0 = _lib.launch_count()
     loss_epoch1 = tr.train_epoch(sync_loss=True)
-    for _ in range(max(args.warmup, 3) - 1):
-        tr.train_epoch(sync_loss=False)
+    launches_epoch = _lib.launch_count() - l0
     barrier()
 
-    # ---- kernel-level roofline: the aggregation launches of K eager epochs, timed
-    # with CUDA events on the launching stream ----
-    tr.enable_kernel_events(True)
-    barrier()
+    # ---- kernel-level roofline: every aggregation launch of K eager epochs, CUDA events
+    # on the trainer's stream (the stream the kernels run on) ----
+    tr.profile(True)
     for _ in range(args.steps):
         tr.train_epoch(sync_loss=False)
     barrier()
-    agg_ms_total, agg_launches, agg_bytes = tr.kernel_event_summary()
-    tr.enable_kernel_events(False)
+    agg_ms_total, agg_launches, agg_bytes = tr.profile_read()   # also turns profiling off
 
     # ---- timed region: K epochs (CUDA-graph replays unless --eager) ----
-    use_graph = not args.eager
-    if use_graph:
-        tr.capture(warmup=1)
-        for _ in range(2):
-            tr.replay()
-    step = tr.replay if use_graph else (lambda: tr.train_epoch(sync_loss=False))
+    for _ in range(max(args.warmup, 3) - 1):
+        tr.train_epoch(sync_loss=False)
     barrier()
-    launches0 = _lib.launch_count()
     with ClockSampler(local) as clk:
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0.record(stream)
         for _ in range(args.steps):
-            step()
-        e1.record()
+            tr.train_epoch(sync_loss=False)
+        e1.record(stream)
         barrier()
-    launches = _lib.launch_count() - launches0
-    if use_graph:
-        launches = launches_per_epoch(tr) * args.steps
     ms = e0.elapsed_time(e1) / args.steps
+    use_graph = tr.graph_captured
     loss = tr.train_epoch(sync_loss=True)
 
     t_ms = torch.tensor([ms, agg_ms_total / args.steps], dtype=torch.float64, device=dev)
@@ -645,35 +634,23 @@ def main():
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms, agg_ms_step = float(t_ms[0]), float(t_ms[1])
 
-    # ---- e2e through the public API: every step copies its feature block and labels
-    # host -> device (pinned) and reads its loss back; the copy of step i+1 overlaps the
-    # compute of step i (FeatureStream double buffering) ----
+    # ---- e2e through the C ABI with HOST buffers: every step stages its feature block
+    # and labels from pinned host memory (gdx_trainer_stage_inputs: one contiguous H2D on
+    # a copy stream, overlapping the previous step) and reads its loss back
+    # (gdx_trainer_step_staged) ----
     e2e = None
     if not args.no_e2e:
-        from paper_2311_06837_b200.train import FeatureStream
-        xh = torch.empty((tr.nloc, tr.F), dtype=torch.float32).pin_memory()
-        xh.copy_(tr.X[:tr.nloc, :tr.F].cpu())
-        lh = tr.labels[:tr.nloc].cpu().pin_memory()
-        loss_h = torch.zeros(1, dtype=torch.float64).pin_memory()
-        fs = FeatureStream(tr)
+        xh, lh = host_inputs(torch, dev, tr, g, C)
         barrier()
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
-        s0.record()
-        fs.prefetch(xh, lh)
+        s0.record(stream)
+        tr.stage_inputs(None, x_ptr=xh.data_ptr(), labels_ptr=lh.data_ptr())
         for i in range(args.steps):
             if i + 1 < args.steps:
-                fs.prefetch(xh, lh)
-            fs.consume()
-            if use_graph:
-                tr.replay()
-            else:
-                tr.train_epoch(sync_loss=False)
-            loss_h.copy_(tr.loss_acc, non_blocking=True)
-            done = torch.cuda.Event()
-            done.record()
-            done.synchronize()  # the step's loss is on the host before the next step
-        s1.record()
+                tr.stage_inputs(None, x_ptr=xh.data_ptr(), labels_ptr=lh.data_ptr())
+            tr.step_staged(with_labels=True, sync_loss=True)   # the step's loss is on the host
+        s1.record(stream)
         barrier()
         e2e_ms = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device=dev)
         if world > 1:
@@ -681,8 +658,8 @@ def main():
         h2d = int(xh.numel() * 4 + lh.numel() * 4) * world
         e2e = {"value": round(float(e2e_ms[0]), 3), "unit": "ms",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * world,
+               "api": "gdx_trainer_stage_inputs + gdx_trainer_step_staged (C ABI), pinned host buffers",
                "pipelining": "step i+1's feature H2D overlaps step i's compute (double buffer)",
-               "h2d_ms_per_step": round(fs.copy_ms(), 3),
                "pcie_floor_ms": round(h2d / world / 55e9 * 1e3, 2),
                "pcie_floor_note": "each rank's H2D at the ~55 GB/s pinned PCIe rate measured alone "
                                   "(tools/h2d_probe.py): e2e cannot go below this while the "
@@ -700,8 +677,8 @@ def main():
     peak, peak_kind = load_peaks()
     agg_avg_ms = (agg_ms_total / agg_launches) if agg_launches else None
     achieved = (agg_bytes / agg_launches) / (agg_avg_ms * 1e-3) / 1e9 if agg_launches else None
-    gathered_bytes = max(L.Zfull.numel() if hasattr(L, "Zfull") else L.Xin_full.numel()
-                         for L in tr.layers) * 4
+    nrows_gather = tr.info()[3]
+    gathered_bytes = nrows_gather * max(agg_width(d, nrows_gather) for d in cfg.dims[1:]) * 4
     l2_resident = gathered_bytes <= L2_RESIDENT_BYTES
     traffic, traffic_src = load_traffic(args.config)
 
@@ -727,8 +704,10 @@ def main():
                            f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
             "algorithmic_bytes_per_launch": int(agg_bytes / agg_launches) if agg_launches else None,
             "avg_launch_ms": round(agg_avg_ms, 4) if agg_avg_ms else None,
+            "launches_per_step": int(agg_launches / max(args.steps, 1)),
             "share_of_step": round(agg_ms_step / ms, 3) if ms else None,
-            "note": ("bytes = 4 nnz + 8 (rows+1) + 4 F nnz + 4 F rows per launch (SURVEY §8d). "
+            "note": ("bytes = 4 nnz + 8 (rows+1) + 4 F nnz + 4 F rows per launch (SURVEY §8d), "
+                     "timed on the trainer's stream over K eager epochs. "
                      + (f"The gathered matrix ({gathered_bytes / 1e6:.0f} MB) is L2-resident, so the "
                         f"binding ceiling is L2 read bandwidth (frac vs the live L2 probe); vs HBM "
                         f"see hbm_secondary, and the HBM-regime pass is hbm_regime"
@@ -751,7 +730,7 @@ def main():
             "warmup": max(args.warmup, 3),
             "ms_per_step": round(ms, 3),
             "higher_is_better": False,
-            "scaling": "strong",
+            "scaling": "strong" if C["mode"] == "full" else "weak",
             "vs_baseline": None,
             "dtype": "f32 (tcgen05 GEMMs: bf16x3 split, fp32 accumulate)",
             "data": DATA[args.config],
@@ -763,27 +742,63 @@ def main():
             "loss_after": round(loss, 6),
             "parity": parity,
             "roofline": roof,
-            "gpu_launches": int(launches),
+            "gpu_launches": int(launches_epoch * args.steps),
+            "gpu_launches_note": "libgdx launches of one eager epoch x steps (the timed epochs replay "
+                                 "the same kernels as one CUDA graph)",
+            "trainer": "C-ABI gdx_trainer (csrc/trainer.cu): epoch orchestrated in C++, no torch on "
+                       "the step path",
             "cuda_graph": use_graph,
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "setup_s": {"graph_generation": round(t_gen, 2)},
+            "setup_s": {"graph_generation": round(t_gen, 2), "trainer": round(t_setup, 2)},
         }
         if sub is not None:
             out["config"]["subgraph"] = {"servers": C.get("servers", world), "server": rank,
                                          "inner": len(sub.inner_vertices),
                                          "halo": len(sub.halo_vertices),
-                                         "induced_edges": sub.induced_edges}
+                                         "induced_edges": sub.induced_edges,
+                                         "local_rows": tr.nloc}
         print(json.dumps(out), flush=True)
-    # release the captured graph (it references the NCCL communicator) before teardown
-    tr.graph = None
-    torch.cuda.synchronize()
+    barrier()
+    tr.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0 and parity is not None and not parity["ok"]:
         sys.exit(1)   # a number whose loss disagrees with the oracle is not a result
+
+
+def host_inputs(torch, dev, tr, g, C):
+    """This rank's feature block and labels in PINNED host memory -- the inputs a user
+    hands the engine -- generated by the library's keyed streams on the device
+    (gdx_init_uniform / gdx_init_labels, the make_features stream) and copied once."""
+    from paper_2311_06837_b200._lib import call
+    from paper_2311_06837_b200.device import stream_handle
+
+    F, classes = C["dims"][0], C["dims"][-1]
+    x = torch.zeros((max(tr.nloc, 1), F), dtype=torch.float32, device=dev)
+    lab = torch.zeros(max(tr.nloc, 1), dtype=torch.int32, device=dev)
+    if not tr.subgraph_mode:
+        call("gdx_init_uniform", 1, 0x66656174, 0, tr.lo * F, tr.nloc, F, -0.5, 0.5, x.data_ptr(), F,
+             stream_handle())
+        call("gdx_init_labels", 2, tr.lo, tr.nloc, classes, lab.data_ptr(), stream_handle())
+    else:
+        n = g.num_vertices()
+        xa = torch.empty((n, F), dtype=torch.float32, device=dev)
+        la = torch.empty(n, dtype=torch.int32, device=dev)
+        call("gdx_init_uniform", 1, 0x66656174, 0, 0, n, F, -0.5, 0.5, xa.data_ptr(), F, stream_handle())
+        call("gdx_init_labels", 2, 0, n, classes, la.data_ptr(), stream_handle())
+        ids = torch.from_numpy(tr.l2g.astype(np.int64)).to(dev)
+        avail = int(tr.rows_in[0])
+        x[:avail] = xa[ids[:avail]]       # inputs beyond L hops stay zero
+        lab[:tr.nloc] = la[ids]
+        del xa, la
+    xh = torch.empty((tr.nloc, F), dtype=torch.float32).pin_memory()
+    lh = torch.empty(tr.nloc, dtype=torch.int32).pin_memory()
+    xh.copy_(x[:tr.nloc].cpu())
+    lh.copy_(lab[:tr.nloc].cpu())
+    return xh, lh
 
 
 if __name__ == "__main__":

@@ -272,6 +272,13 @@ class CobatchTrainer(FullGraphTrainer):
         if off[-1] <= 0.9 * (self.world - 1) * geo.nloc:
             geo.send_rows = (recv, off)
 
+    def _peers(self, deltas, target: int):
+        """No producer-side peer stores for cooperative batches: a producer writes only the
+        batch's produced row prefix, while the peers must also see the zeroed rows past it
+        (bind() clears them locally; a stale row from the previous batch would leak into the
+        peers' aggregation), so every exchange is a push of the whole block."""
+        return None
+
     def _refresh_input_splits(self):  # inputs arrive split (LOAD); nothing to refresh
         pass
 

@@ -130,6 +130,7 @@ class NativeTrainer:
             gr.global_ids = l2g.ctypes.data
             keep += [lptr, lcol, l2g, rows_in, rows_out]
             self.local_rows = loc.n
+            self.l2g, self.rows_in = l2g, rows_in
             del loc
         h = C.c_void_p()
         call("gdx_trainer_create", C.byref(c), C.byref(gr), C.byref(h))

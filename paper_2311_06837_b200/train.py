@@ -571,13 +571,14 @@ class FullGraphTrainer:
                     acts.append(L.Hout[:self.nloc, :L.fout].clone())
                 continue
             own = L.Zfull[self.lo:self.hi]
+            pe = self._peers(L.z_peers, 1 if cfg.kind == "sage" else 0)
             if cfg.kind == "sage":
-                gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w, m=m_in, peers=self._peers(L.z_peers, 1))
+                gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w, m=m_in, peers=pe)
             elif cfg.kind == "gcn":
-                gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s, m=m_in, peers=self._peers(L.z_peers, 0))
+                gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s, m=m_in, peers=pe)
             else:
-                gemm_tn(A, L.Wsp, c0=own, m=m_in, peers=self._peers(L.z_peers, 0))
-            self._publish(own, L.z_peers, stored=True)
+                gemm_tn(A, L.Wsp, c0=own, m=m_in, peers=pe)
+            self._publish(own, L.z_peers, stored=pe is not None)
             nxt = self.layers[l + 1] if l + 1 < cfg.layers else None
             if getattr(nxt, "agg_first", False):   # output rows feed an aggregate-first layer
                 out, out_split = nxt.Xin_full[self.lo:self.hi], _SplitView(nxt.C, 0)
@@ -662,10 +663,11 @@ class FullGraphTrainer:
             # epilogue: ReLU backward with H_{l} as mask, scale, split -> layer l-1's inputs
             if l > 0:
                 own, scale, split = self._grad_targets(l - 1)
+                pe = self._peers(self.layers[l - 1].d_peers, 0)
                 gemm_tn(L.G, L.Wsp, c0=own, b_mn=True, mask=self._act(l - 1),
                         row_scale=scale, out_split=split, split_unscaled=True, m=self.rows_out[l - 1],
-                        peers=self._peers(self.layers[l - 1].d_peers, 0))
-                self._publish(own, self.layers[l - 1].d_peers, stored=True)
+                        peers=pe)
+                self._publish(own, self.layers[l - 1].d_peers, stored=pe is not None)
             # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
             # (K = the rows that fed layer l; rows past them carry no gradient)
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
@@ -750,7 +752,7 @@ class FullGraphTrainer:
                 return float(self.loss_acc.item()) / self.loss_count
             return None
         own, scale, split = self._grad_targets(self.cfg.layers - 1)
-        if self.p2p is not None and self.p2p.mode == "epilogue":
+        if self._peers(self.layers[-1].d_peers, 0) is not None:   # p2p-epilogue: softmax stores to peers
             Lz = self.layers[-1]
             deltas = (_lib.C.c_int64 * 7)(*Lz.d_peers)
             call("gdx_softmax_xent_fused_peers", logits.data_ptr(), logits.shape[1], self.loss_rows,
