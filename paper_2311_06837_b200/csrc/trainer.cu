@@ -969,11 +969,13 @@ extern "C" int gdx_trainer_stage_inputs(gdx_trainer* t, const float* x_host, con
     GDX_REQUIRE(t && x_host, GDX_INPUT, "gdx_trainer_stage_inputs: null pointer");
     GDX_CUDA(cudaSetDevice(t->dev));
     const int i = static_cast<int>(t->issued % 2);
-    if (!t->stage[i]) {
-        GDX_CUDA(cudaMalloc(&t->stage[i], std::max<uint64_t>(t->nloc, 1) * t->F * 4));
-        GDX_CUDA(cudaMalloc(&t->stage_labels[i], std::max<uint64_t>(t->nloc, 1) * 4));
-        GDX_CUDA(cudaEventCreateWithFlags(&t->ready[i], cudaEventDisableTiming));
-        GDX_CUDA(cudaEventCreateWithFlags(&t->freed[i], cudaEventDisableTiming));
+    if (!t->stage[0]) {  // both halves of the double buffer at once, before any copy is queued
+        for (int j = 0; j < 2; ++j) {
+            GDX_CUDA(cudaMalloc(&t->stage[j], std::max<uint64_t>(t->nloc, 1) * t->F * 4));
+            GDX_CUDA(cudaMalloc(&t->stage_labels[j], std::max<uint64_t>(t->nloc, 1) * 4));
+            GDX_CUDA(cudaEventCreateWithFlags(&t->ready[j], cudaEventDisableTiming));
+            GDX_CUDA(cudaEventCreateWithFlags(&t->freed[j], cudaEventDisableTiming));
+        }
     }
     if (t->issued >= 2) GDX_CUDA(cudaStreamWaitEvent(t->copy, t->freed[i], 0));
     // ONE contiguous DMA of the host block [nloc, F] (the PCIe rate from pinned memory)
