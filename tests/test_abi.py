@@ -124,3 +124,40 @@ def test_golden_mincut_partition():
     f = np.load(os.path.join(gold, "forward_full_config1.npz"))
     g = G.Graph(int(z["n"]), z["row_offsets"], z["cols"])
     assert np.array_equal(partition_mincut(g, 2, 1).assignment, f["mincut2"])
+
+
+def test_every_push_path_takes_seven_peers():
+    """One box of 8 GPUs = 7 peers per rank: every peer-store entry point accepts 7 and
+    rejects 8 (checked before any device work, so this runs on CPU)."""
+    import ctypes as C
+
+    from paper_2311_06837_b200 import _lib
+    from paper_2311_06837_b200.errors import InputError
+    L = _lib.lib()
+    d7 = (C.c_int64 * 8)(*([256] * 8))
+    for npeers, ok in ((7, True), (8, False)):
+        rc = L.gdx_push_peers(None, 16, d7, npeers, None, None, 1, None)
+        msg = L.gdx_last_error().decode()
+        assert rc == 1 and (("at most 7" in msg) != ok), (npeers, msg)
+        rc = L.gdx_push_rows(None, 16, None, None, d7, npeers, None, None, 1, None)
+        msg = L.gdx_last_error().decode()
+        assert rc == 1 and (("at most 7" in msg) != ok), (npeers, msg)
+        rc = L.gdx_softmax_xent_fused_peers(None, 0, 0, 1, None, 1.0, None, None, 0, None, None, 0, None,
+                                            npeers, d7, None)
+        msg = L.gdx_last_error().decode()
+        assert rc == 1, msg
+    # the trainer: world <= 8 is accepted by the argument checks, 9 is not
+    from paper_2311_06837_b200 import native
+    native._bind()
+    dims = (C.c_uint32 * 3)(8, 8, 4)
+    ro = (C.c_uint64 * 3)(0, 1, 2)
+    ci = (C.c_uint32 * 2)(1, 0)
+    gr = native.TrainerGraph(2, 2, C.cast(ro, C.c_void_p), C.cast(ci, C.c_void_p))
+    for world, ok in ((8, True), (9, False)):
+        cfg = native.TrainerConfig(2, 2, dims, 0.1, 0, world, 0, 1, 2, 1, 0, 0, 0.0)
+        h = C.c_void_p()
+        rc = L.gdx_trainer_create(C.byref(cfg), C.byref(gr), C.byref(h))
+        msg = L.gdx_last_error().decode()
+        assert ("world must be 1..8" in msg) != ok, (world, rc, msg)
+        if rc == 0:
+            L.gdx_trainer_destroy(h)

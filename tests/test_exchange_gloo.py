@@ -1,5 +1,6 @@
 """The multi-rank exchange (row all-gather + gradient all-reduce) of the
-full-graph trainer, driven with the gloo backend on CPU at world_size 2 and 3."""
+full-graph trainer, driven with the gloo backend on CPU at world sizes 2, 3, 4
+and 8 (one box of 8 B200s: 7 peers per rank)."""
 import os
 import socket
 
@@ -36,7 +37,13 @@ def _worker(rank, world, port, offsets, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("offsets", [[0, 4, 8], [0, 5, 9], [0, 3, 6, 7]])
+def _ceil_blocks(n, world):
+    B = -(-n // world)
+    return [int(x) for x in np.minimum(np.arange(world + 1) * B, n)]
+
+
+@pytest.mark.parametrize("offsets", [[0, 4, 8], [0, 5, 9], [0, 3, 6, 7], _ceil_blocks(30, 4),
+                                     _ceil_blocks(61, 8), list(range(0, 9 * 5, 5))])
 def test_row_exchange_gloo(offsets):
     world = len(offsets) - 1
     ctx = mp.get_context("spawn")
@@ -45,9 +52,9 @@ def test_row_exchange_gloo(offsets):
     procs = [ctx.Process(target=_worker, args=(r, world, port, offsets, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=90) for _ in range(world)]
+    res = [q.get(timeout=240) for _ in range(world)]
     for p in procs:
-        p.join(timeout=60)
+        p.join(timeout=120)
         assert p.exitcode == 0
     n = offsets[-1]
     want = np.arange(n, dtype=np.float32)[:, None] * 10 + np.arange(5)
@@ -56,12 +63,21 @@ def test_row_exchange_gloo(offsets):
         assert np.all(g == sum(range(1, world + 1)))
 
 
-def test_trainer_block_layout():
-    """Ceil-sized blocks: every gather block has the same size, the last may be short."""
-    n, world = 232965, 8
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("n", [232965, 2449029, 111059956, 9])
+def test_trainer_block_layout(n, world):
+    """Ceil-sized blocks (FullGraphTrainer and csrc/trainer.cu): every gather block has the
+    same size B, rank r's rows sit at [r B, r B + nloc) in every GPU's gathered buffer, the
+    last block may be short, and the blocks tile [0, n) exactly."""
     B = -(-n // world)
     offs = np.minimum(np.arange(world + 1) * B, n)
-    assert offs[-1] == n and np.all(np.diff(offs)[:-1] == B) and 0 < offs[-1] - offs[-2] <= B
+    assert offs[0] == 0 and offs[-1] == n
+    nloc = np.diff(offs)
+    assert np.array_equal(nloc, np.clip(n - np.arange(world) * B, 0, B)) and nloc.sum() == n
+    if n >= world * (world - 1):       # the BASELINE shapes: only the last block is short
+        assert np.all(nloc[:-1] == B) and 0 < nloc[-1] <= B
+    # the gathered buffer (world * B rows) holds every rank's block at the same offset
+    assert world * B >= n and world * B - n < world
 
 
 def _needs_worker(rank, world, port, q):
@@ -87,7 +103,7 @@ def _needs_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_sparse_push_row_lists_gloo(world):
     """The cooperative-batch sparse push's row lists (all_to_all of per-source needs)."""
     ctx = mp.get_context("spawn")
@@ -96,9 +112,9 @@ def test_sparse_push_row_lists_gloo(world):
     ps = [ctx.Process(target=_needs_worker, args=(r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
+    res = [q.get(timeout=240) for _ in range(world)]
     for p in ps:
-        p.join(timeout=60)
+        p.join(timeout=120)
     assert all(ok for _, ok, _ in res), res
 
 
