@@ -1,0 +1,78 @@
+"""Same box, same workload: the C-ABI trainer (csrc/trainer.cu) vs the torch-
+orchestrated FullGraphTrainer, CUDA-graph epochs, CUDA-event time, max over ranks.
+
+    torchrun --nproc-per-node N tools/trainer_compare.py [--config products-gcn]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="reddit-sage")
+    ap.add_argument("--steps", type=int, default=20)
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.native import NativeTrainer
+    from paper_2311_06837_b200.train import FullGraphTrainer, ModelConfig
+
+    world, rank, local = bench.dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = True
+        dist.init_process_group("nccl", device_id=dev, pg_options=opts)
+        pg = dist.group.WORLD
+    C = bench.CONFIGS[args.config]
+    g = G.gen_random_graph(C["n"], C["degree"], C["seed"])
+    cfg = ModelConfig(C["kind"], list(C["dims"]), lr=C["lr"])
+
+    def timeit(step, stream):
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    out = {"config": args.config, "world": world}
+    nt = NativeTrainer(g, cfg, rank=rank, world=world, pg=pg)
+    out["native_ms"] = timeit(lambda: nt.train_epoch(sync_loss=False), nt.stream())
+    ft = FullGraphTrainer(g, cfg, rank=rank, world=world, pg=pg)
+    ft.capture(warmup=2)
+    out["torch_ms"] = timeit(ft.replay, torch.cuda.current_stream())
+    out["native_ms_again"] = timeit(lambda: nt.train_epoch(sync_loss=False), nt.stream())
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    ft.graph = None
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    nt.close()
+    ft.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
