@@ -332,8 +332,8 @@ int gdx_gather_split_rows(const uint16_t* src_hi, const uint16_t* src_lo, uint64
  * no Python): the reference's layer model (reference_gnn.cpp:64-147) plus the
  * north_star's softmax cross-entropy, backward and SGD, on this library's
  * kernels.  One trainer per GPU; world > 1 ranks exchange rows and weight
- * gradients through one CUDA-IPC arena per rank (gdx_trainer_ipc_export on every
- * rank, the 64-byte blobs gathered by the caller -- MPI, sockets, torch -- then
+ * gradients through CUDA-IPC-shared buffers (gdx_trainer_ipc_export on every rank,
+ * the blobs gathered by the caller -- MPI, sockets, torch -- then
  * gdx_trainer_connect on every rank).  No NCCL on the data path.
  * ---------------------------------------------------------------------- */
 enum { GDX_MODEL_SUM = 0, GDX_MODEL_GCN = 1, GDX_MODEL_SAGE = 2 };
@@ -377,8 +377,10 @@ int gdx_trainer_init_weights(gdx_trainer* t, uint64_t seed, int he_init);  /* (s
 int gdx_trainer_set_weights(gdx_trainer* t, const double* w, uint64_t count);
 int gdx_trainer_get_weights(gdx_trainer* t, double* w, uint64_t count);
 int gdx_trainer_get_grads(gdx_trainer* t, double* g, uint64_t count);   /* last epoch's dW (summed) */
-int gdx_trainer_ipc_export(gdx_trainer* t, void* blob64);
-int gdx_trainer_connect(gdx_trainer* t, const void* blobs);  /* world x 64 bytes, rank order */
+/* Each rank's shared buffers travel as a blob of CUDA IPC handles (same size on every rank). */
+uint64_t gdx_trainer_ipc_blob_bytes(const gdx_trainer* t);
+int gdx_trainer_ipc_export(gdx_trainer* t, void* blob);
+int gdx_trainer_connect(gdx_trainer* t, const void* blobs);  /* world blobs, rank order */
 /* One epoch (forward, loss, backward, gradient all-reduce, SGD) on the trainer's stream.
  * loss_out (nullable): the mean loss, read back (synchronising). */
 int gdx_trainer_epoch(gdx_trainer* t, double* loss_out);

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -113,8 +114,12 @@ struct gdx_trainer {
     Mat partial;
     double* loss_acc = nullptr;
     std::vector<Layer> layers;
-    // shared arena (IPC): [grad slots: world x gstride floats][arrival slots][exchange buffers]
-    char* arena = nullptr;
+    // IPC-shared regions, each its own cudaMalloc: region 0 = [grad slots: world x gstride
+    // floats][arrival slots]; regions 1.. = the gathered buffers (full-graph mode, world > 1)
+    std::vector<char*> regions;
+    std::vector<uint64_t> region_bytes;
+    std::vector<std::vector<int64_t>> region_delta;  // [region][peer]: peer base - our base
+    char* arena = nullptr;                             // == regions[0]
     uint64_t arena_bytes = 0, gstride = 0;
     float* grad_slots = nullptr;
     unsigned long long* slots = nullptr;
@@ -122,7 +127,6 @@ struct gdx_trainer {
     unsigned int* push_done = nullptr;
     unsigned long long** peer_slots_dev = nullptr;
     std::vector<void*> opened;
-    int64_t deltas[7] = {0};
     bool connected = false;
     // streams, graph, staging
     cudaStream_t stream = nullptr, side = nullptr, copy = nullptr;
@@ -277,11 +281,22 @@ int aggregate(gdx_trainer* t, const Mat& src, uint32_t width, uint32_t rows, con
 // Make this rank's rows [lo, lo+nloc) of a gathered buffer visible to the peers:
 // SM push (16-byte NVLink stores into every peer's copy) on the side stream, forked
 // from the producer and joined before the next wait.
+const int64_t* deltas_for(gdx_trainer* t, const void* p) {
+    for (size_t k = 0; k < t->regions.size(); ++k) {
+        const char* b = t->regions[k];
+        if (static_cast<const char*>(p) >= b && static_cast<const char*>(p) < b + t->region_bytes[k])
+            return t->region_delta[k].data();
+    }
+    return nullptr;
+}
+
 int publish(gdx_trainer* t, const float* own, uint64_t bytes) {
     if (t->world == 1 || t->subgraph) return GDX_OK;
+    const int64_t* deltas = deltas_for(t, own);
+    if (!deltas) return err(GDX_INTERNAL, "publish: buffer outside the shared regions");
     TR_CUDA(cudaEventRecord(t->ev_fork, t->stream));
     TR_CUDA(cudaStreamWaitEvent(t->side, t->ev_fork, 0));
-    TR_OK(gdx_push_peers(own, bytes, t->deltas, t->world - 1, t->peer_slots_dev, t->push_done,
+    TR_OK(gdx_push_peers(own, bytes, deltas, t->world - 1, t->peer_slots_dev, t->push_done,
                          t->cfg.push_ctas ? t->cfg.push_ctas : 32, reinterpret_cast<gdx_stream>(t->side)));
     TR_CUDA(cudaEventRecord(t->ev_join, t->side));
     return GDX_OK;
@@ -469,7 +484,8 @@ int backward_and_step(gdx_trainer* t) {
         note_launch();
         TR_CUDA(cudaEventRecord(t->ev_fork, t->stream));
         TR_CUDA(cudaStreamWaitEvent(t->side, t->ev_fork, 0));
-        TR_OK(gdx_push_peers(mine, t->gstride * 4, t->deltas, t->world - 1, t->peer_slots_dev, t->push_done, 8,
+        TR_OK(gdx_push_peers(mine, t->gstride * 4, t->region_delta[0].data(), t->world - 1, t->peer_slots_dev,
+                             t->push_done, 8,
                              reinterpret_cast<gdx_stream>(t->side)));
         TR_CUDA(cudaEventRecord(t->ev_join, t->side));
         TR_OK(wait_peers(t));
@@ -557,9 +573,21 @@ int setup_model(gdx_trainer* t) {
             off += (bytes + 255) / 256 * 256;
         }
     }
-    t->arena_bytes = off;
-    TR_CUDA(cudaMalloc(&t->arena, t->arena_bytes));
-    TR_CUDA(cudaMemset(t->arena, 0, t->arena_bytes));
+    // region 0: grad slots + arrival slots; one region per gathered buffer
+    t->arena_bytes = slots_off + 256 + pad64(8 * t->world);
+    std::vector<uint64_t> sizes{t->arena_bytes};
+    for (size_t j = 0; j < xoff.size(); ++j) {
+        const uint64_t end = j + 1 < xoff.size() ? xoff[j + 1] : off;
+        sizes.push_back(end - xoff[j]);
+    }
+    for (uint64_t b : sizes) {
+        char* r = nullptr;
+        TR_CUDA(cudaMalloc(&r, b));
+        TR_CUDA(cudaMemset(r, 0, b));
+        t->regions.push_back(r);
+        t->region_bytes.push_back(b);
+    }
+    t->arena = t->regions[0];
     t->grad_slots = reinterpret_cast<float*>(t->arena);
     t->slots = reinterpret_cast<unsigned long long*>(t->arena + slots_off + 256);
     TR_OK(dalloc(t, &t->expected, 1));
@@ -575,7 +603,7 @@ int setup_model(gdx_trainer* t) {
         auto shared = [&](Mat* m, uint32_t width, int which) -> int {
             if (xoff.empty()) return dmat(t, m, t->nfull, width);
             m->ld = pad4(width);
-            m->p = reinterpret_cast<float*>(t->arena + xoff[2 * l + which]);
+            m->p = reinterpret_cast<float*>(t->regions[1 + 2 * l + which]);
             return GDX_OK;
         };
         if (Ly.agg_first) {
@@ -698,7 +726,7 @@ gdx_trainer::~gdx_trainer() {
         if (freed[i]) cudaEventDestroy(freed[i]);
     }
     if (loss_host) cudaFreeHost(loss_host);
-    if (arena) cudaFree(arena);
+    for (char* r : regions) cudaFree(r);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
@@ -731,7 +759,13 @@ extern "C" int gdx_trainer_create(const gdx_trainer_config* cfg, const gdx_train
     t->classes = t->dims[t->L];
     GDX_CUDA(cudaSetDevice(t->dev));
     GDX_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
-    GDX_CUDA(cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking));
+    {   // the NVLink push stream; GDX_TR_PUSH_PRIO=high gives it the highest priority
+        int least = 0, greatest = 0;
+        GDX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        const char* pr = std::getenv("GDX_TR_PUSH_PRIO");
+        const int prio = (pr && std::string(pr) == "high") ? greatest : least;
+        GDX_CUDA(cudaStreamCreateWithPriority(&t->side, cudaStreamNonBlocking, prio));
+    }
     GDX_CUDA(cudaStreamCreateWithFlags(&t->copy, cudaStreamNonBlocking));
     GDX_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
     GDX_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
@@ -921,10 +955,16 @@ extern "C" uint64_t gdx_trainer_weight_count(const gdx_trainer* t) {
     return need;
 }
 
-extern "C" int gdx_trainer_ipc_export(gdx_trainer* t, void* blob64) {
-    GDX_REQUIRE(t && blob64, GDX_INPUT, "gdx_trainer_ipc_export: null pointer");
+extern "C" uint64_t gdx_trainer_ipc_blob_bytes(const gdx_trainer* t) {
+    return t ? 64ull * t->regions.size() : 0;
+}
+
+extern "C" int gdx_trainer_ipc_export(gdx_trainer* t, void* blob) {
+    GDX_REQUIRE(t && blob, GDX_INPUT, "gdx_trainer_ipc_export: null pointer");
     GDX_CUDA(cudaSetDevice(t->dev));
-    return gdx_ipc_get_handle(t->arena, blob64);
+    for (size_t k = 0; k < t->regions.size(); ++k)
+        TR_OK(gdx_ipc_get_handle(t->regions[k], static_cast<char*>(blob) + 64 * k));
+    return GDX_OK;
 }
 
 extern "C" int gdx_trainer_connect(gdx_trainer* t, const void* blobs) {
@@ -936,16 +976,20 @@ extern "C" int gdx_trainer_connect(gdx_trainer* t, const void* blobs) {
         return GDX_OK;
     }
     std::vector<unsigned long long*> peer_slot(t->world - 1);
-    uint32_t i = 0;
     const uint64_t slot_off = reinterpret_cast<char*>(t->slots) - t->arena;
+    const uint64_t blob = 64ull * t->regions.size();
+    t->region_delta.assign(t->regions.size(), std::vector<int64_t>(7, 0));
+    uint32_t i = 0;
     for (uint32_t r = 0; r < t->world; ++r) {
         if (r == t->rank) continue;
-        void* base = nullptr;
-        TR_OK(gdx_ipc_open(static_cast<const char*>(blobs) + 64 * r, &base));
-        t->opened.push_back(base);
-        t->deltas[i] = static_cast<char*>(base) - t->arena;
-        // our arrival slot inside peer r's array
-        peer_slot[i] = reinterpret_cast<unsigned long long*>(static_cast<char*>(base) + slot_off) + t->rank;
+        for (size_t k = 0; k < t->regions.size(); ++k) {
+            void* base = nullptr;
+            TR_OK(gdx_ipc_open(static_cast<const char*>(blobs) + blob * r + 64 * k, &base));
+            t->opened.push_back(base);
+            t->region_delta[k][i] = static_cast<char*>(base) - t->regions[k];
+            // our arrival slot inside peer r's array
+            if (k == 0) peer_slot[i] = reinterpret_cast<unsigned long long*>(static_cast<char*>(base) + slot_off) + t->rank;
+        }
         ++i;
     }
     GDX_CUDA(cudaMemcpy(t->peer_slots_dev, peer_slot.data(), peer_slot.size() * sizeof(void*), cudaMemcpyHostToDevice));

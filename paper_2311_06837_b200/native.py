@@ -45,6 +45,7 @@ _SIGS = {
     "gdx_trainer_set_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "gdx_trainer_get_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "gdx_trainer_get_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "gdx_trainer_ipc_blob_bytes": (C.c_uint64, [C.c_void_p]),
     "gdx_trainer_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gdx_trainer_connect": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gdx_trainer_epoch": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
@@ -147,11 +148,12 @@ class NativeTrainer:
     # ---- plumbing ----
     def _connect(self):
         import torch.distributed as dist
-        blob = C.create_string_buffer(64)
+        nb = int(_lib.lib().gdx_trainer_ipc_blob_bytes(self._h))
+        blob = C.create_string_buffer(nb)
         call("gdx_trainer_ipc_export", self._h, blob)
         out = [None] * self.world
         dist.all_gather_object(out, blob.raw, group=self.pg)
-        allb = C.create_string_buffer(b"".join(out), 64 * self.world)
+        allb = C.create_string_buffer(b"".join(out), nb * self.world)
         call("gdx_trainer_connect", self._h, allb)
         dist.barrier(group=self.pg)
 

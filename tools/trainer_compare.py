@@ -61,6 +61,27 @@ def main():
     ft.capture(warmup=2)
     out["torch_ms"] = timeit(ft.replay, torch.cuda.current_stream())
     out["native_ms_again"] = timeit(lambda: nt.train_epoch(sync_loss=False), nt.stream())
+    # aggregation launches of eager epochs (CUDA events on each trainer's stream)
+    nt2 = NativeTrainer(g, cfg, rank=rank, world=world, pg=pg, use_graph=False)
+    nt2.profile(True)
+    for _ in range(3):
+        nt2.train_epoch(sync_loss=False)
+    ms, n, by = nt2.profile_read()
+    out["native_agg_ms_per_epoch"] = ms / 3
+    out["native_eager_ms"] = timeit(lambda: nt2.train_epoch(sync_loss=False), nt2.stream())
+    ft.graph = None
+    ft.enable_kernel_events(True)
+    for _ in range(3):
+        ft.train_epoch(sync_loss=False)
+    ms2, n2, by2 = ft.kernel_event_summary()
+    ft.enable_kernel_events(False)
+    out["torch_agg_ms_per_epoch"] = ms2 / 3
+    out["torch_eager_ms"] = timeit(lambda: ft.train_epoch(sync_loss=False), torch.cuda.current_stream())
+    out["agg_launches"] = [n / 3, n2 / 3]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    nt2.close()
     if rank == 0:
         print(json.dumps(out), flush=True)
     ft.graph = None
