@@ -461,25 +461,31 @@ def run_cobatch(args, C, world, rank, local, dev, pg):
     # batch 0's first step from the initial weights: the parity anchor (one more warm-up step)
     tr.train_batch(0)
     loss_b0 = float(tr.loss_acc.item()) / max(1, len(plan.batches[0].target_vertices))
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(args.warmup, 3) - 1):
         tr.train_epoch(sync_loss=False)
     barrier()
     tr.enable_kernel_events(True)
+    launches0 = _lib.launch_count()
     tr.train_epoch(sync_loss=False)
     barrier()
+    launches = (_lib.launch_count() - launches0) * args.steps   # graph replays run the same kernels
     agg_ms_epoch, agg_launches, agg_bytes = tr.kernel_event_summary()
     tr.enable_kernel_events(False)
-    launches0 = _lib.launch_count()
+    use_graph = not args.eager
+    if use_graph:   # one CUDA graph per batch
+        tr.capture(warmup=0)
+    step = tr.replay_epoch if use_graph else (lambda: tr.train_epoch(sync_loss=False))
+    step()
+    barrier()
     with ClockSampler(local) as clk:
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            tr.train_epoch(sync_loss=False)
+            step()
         e1.record()
         barrier()
-    launches = _lib.launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps
     loss = tr.train_epoch(sync_loss=True)
     t_ms = torch.tensor([ms, agg_ms_epoch], dtype=torch.float64, device=dev)
@@ -529,8 +535,8 @@ def run_cobatch(args, C, world, rank, local, dev, pg):
                 "algorithmic_bytes_per_launch": int(agg_bytes / agg_launches) if agg_launches else None,
                 "avg_launch_ms": round(agg_avg_ms, 4) if agg_avg_ms else None,
                 "share_of_step": round(agg_ms / ms, 3) if ms else None},
-            "gpu_launches": int(launches / max(args.steps, 1)),
-            "cuda_graph": False,
+            "gpu_launches": int(launches),
+            "cuda_graph": use_graph,
             "clocks": clk.summary(),
             "e2e": None,
             "e2e_note": "not measured for this config: host-side features would be 57 GB",

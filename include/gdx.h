@@ -101,7 +101,21 @@ typedef struct gdx_aggregate_args {
     uint16_t* out_hi;         /* nullable split-bf16 copy [rows x ld_split] */
     uint16_t* out_lo;
     uint64_t ld_split;
+    /* Packed-24 rows (fp32 rounded to 24 bits: 15 mantissa bits, relative error <= 2^-16,
+     * the split-bf16 GEMM operands' precision) in two planes of the same pitch: u16 high
+     * bits + u8 next bits -- 6 of a 64-wide row's 8 sectors.  src_lo8 non-null: src is
+     * the u16 high plane (pitch ld_src elements) of the gathered matrix, self term
+     * included; out24_*: packed-24 copy of the output.  Width a multiple of 8. */
+    const uint8_t* src_lo8;
+    uint16_t* out24_hi;
+    uint8_t* out24_lo;
+    uint64_t ld_out24;
 } gdx_aggregate_args;
+/* fp32 <-> packed-24 conversion (round to nearest even at bit 8). */
+int gdx_pack24(const float* src, uint64_t ld_src, uint32_t rows, uint32_t cols, uint16_t* hi, uint8_t* lo,
+               uint64_t ld_dst, gdx_stream stream);
+int gdx_unpack24(const uint16_t* hi, const uint8_t* lo, uint64_t ld_src, uint32_t rows, uint32_t cols, float* dst,
+                 uint64_t ld_dst, gdx_stream stream);
 int gdx_aggregate(const gdx_aggregate_args* a, gdx_stream stream);
 /* seg_lo[v], seg_hi[v] = sub-range of row v's (sorted) column ids inside [lo, hi). */
 int gdx_row_split(const uint64_t* row_ptr, const uint32_t* col, uint32_t rows, uint32_t lo,
@@ -193,6 +207,9 @@ int gdx_push_multicast(const void* src, uint64_t bytes, void* mc_dst, uint32_t n
                        gdx_stream stream);
 /* One copy-engine push (cudaMemcpyAsync D2D; dst may be an IPC-mapped peer address). */
 int gdx_memcpy_async(void* dst, const void* src, uint64_t bytes, gdx_stream stream);
+/* rows x width_bytes of a pitched buffer set to `value` (stream-ordered, graph-capturable). */
+int gdx_memset2d_async(void* dst, uint64_t pitch_bytes, int value, uint64_t width_bytes, uint64_t rows,
+                       gdx_stream stream);
 /* After the producing kernel: release its peer stores and increment this rank's slot
  * in every peer's arrival array (peer_slots_dev: device array of npeers IPC-mapped
  * u64 slot pointers). */

@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <limits>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -106,6 +107,10 @@ private:
     std::vector<VertexId> cols_;
     bool undirected_ = true;
     std::uint32_t feature_dim_ = 0;
+    // The engine's device copy of this (immutable) CSR: uploaded on first use and kept,
+    // shared by copies of the graph, so repeated calls do not re-upload it.
+    mutable std::shared_ptr<void> device_;
+    friend struct GraphDevice;
 };
 
 Graph gen_random_graph(VertexId n, double avg_degree, std::uint64_t seed);

@@ -27,6 +27,7 @@ class AggregateArgs(C.Structure):
         ("src", vp), ("ld_src", u64), ("self_coef", C.c_float), ("self_base", u64),
         ("post_scale", vp), ("add", vp), ("ld_add", u64), ("relu", C.c_int),
         ("out", vp), ("ld_out", u64), ("out_hi", vp), ("out_lo", vp), ("ld_split", u64),
+        ("src_lo8", vp), ("out24_hi", vp), ("out24_lo", vp), ("ld_out24", u64),
     ]
 
 
@@ -54,6 +55,8 @@ _SIGS = {
     "gdx_init_uniform_f64": (C.c_int, [u64, u64, u64, u64, u32, u32, C.c_double, C.c_double, vp, u64, vp]),
     "gdx_init_labels": (C.c_int, [u64, u64, u32, u32, vp, vp]),
     "gdx_aggregate": (C.c_int, [C.POINTER(AggregateArgs), vp]),
+    "gdx_pack24": (C.c_int, [vp, u64, u32, u32, vp, vp, u64, vp]),
+    "gdx_unpack24": (C.c_int, [vp, vp, u64, u32, u32, vp, u64, vp]),
     "gdx_aggregate_variant": (C.c_int, [C.POINTER(AggregateArgs), C.c_int, vp]),
     "gdx_row_split": (C.c_int, [vp, vp, u32, u32, u32, vp, vp, vp]),
     "gdx_gemm_tn": (C.c_int, [C.POINTER(GemmArgs), vp]),
@@ -72,6 +75,7 @@ _SIGS = {
     "gdx_ipc_close": (C.c_int, [vp]),
     "gdx_peer_signal": (C.c_int, [vp, u32, vp]),
     "gdx_memcpy_async": (C.c_int, [vp, vp, u64, vp]),
+    "gdx_memset2d_async": (C.c_int, [vp, u64, C.c_int, u64, u64, vp]),
     "gdx_set_l2_window": (C.c_int, [vp, u64, C.c_float, vp]),
     "gdx_push_peers": (C.c_int, [vp, u64, vp, u32, vp, vp, u32, vp]),
     "gdx_peer_wait_src": (C.c_int, [vp, vp, u32, C.c_int, u64, vp]),

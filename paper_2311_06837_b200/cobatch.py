@@ -303,25 +303,31 @@ class CobatchTrainer(FullGraphTrainer):
         call("gdx_gather_split_rows", self.Xall.hi.data_ptr(), self.Xall.lo.data_ptr(), self.Xall.ld,
              geo.l2g.data_ptr(), geo.nloc, self.F, self.Xsp.hi.data_ptr(), self.Xsp.lo.data_ptr(),
              self.Xsp.ld, stream_handle())
-        if geo.nloc:
-            torch.index_select(self.labels_all, 0, geo.l2g.long(), out=self.labels[:geo.nloc])
+        if geo.nloc:   # labels of the batch rows: 4-byte rows moved bit for bit
+            call("gdx_gather_rows", self.labels_all.data_ptr(), 1, geo.l2g.data_ptr(), geo.nloc, 1,
+                 self.labels.data_ptr(), 1, stream_handle())
         # rows this batch does not produce must hold no gradient (buffers are reused
         # across batches): own gradient rows past each layer's produced prefix and, for
         # SAGE, the dP half of G on rows read but not produced (the dW GEMM's K covers
         # rows_in; the aggregation rewrites the other half there every step)
+        s = stream_handle()
+
+        def clear(t2d, r0, r1, cols=None):
+            if r1 > r0:
+                pitch = t2d.stride(0) * t2d.element_size()
+                width = (t2d.shape[1] if cols is None else cols) * t2d.element_size()
+                call("gdx_memset2d_async", t2d.data_ptr() + r0 * pitch, pitch, 0, width, r1 - r0, s)
+
         for l, L in enumerate(self.layers):
             r_out, r_in = geo.rows_out[l], geo.rows_in[l]
             if getattr(L, "agg_first", False):   # dA rows past the produced ones, dH_self
-                if r_out < geo.nloc:
-                    L.dAfull[self.lo + r_out:self.hi].zero_()
-                if r_out < r_in:
-                    L.dself[r_out:r_in].zero_()
+                clear(L.dAfull, self.lo + r_out, self.hi)
+                clear(L.dself, r_out, r_in)
                 continue
-            if r_out < geo.nloc:
-                L.dfull[self.lo + r_out:self.hi].zero_()
-            if self.cfg.kind == "sage" and r_out < r_in:
-                L.G.hi.view(-1, L.G.ld)[r_out:r_in, :L.w].zero_()
-                L.G.lo.view(-1, L.G.ld)[r_out:r_in, :L.w].zero_()
+            clear(L.dfull, self.lo + r_out, self.hi)
+            if self.cfg.kind == "sage":
+                clear(L.G.hi.view(-1, L.G.ld), r_out, r_in, L.w)
+                clear(L.G.lo.view(-1, L.G.ld), r_out, r_in, L.w)
 
     def train_batch(self, i: int):
         self.bind(i)
@@ -338,5 +344,27 @@ class CobatchTrainer(FullGraphTrainer):
             return float(self.epoch_loss.item()) / max(self.total_targets, 1)
         return None
 
-    def capture(self, warmup: int = 2):
-        raise NotImplementedError("cobatch epochs run eagerly (per-batch geometry)")
+    def capture(self, warmup: int = 1):
+        """One CUDA graph per batch (LOAD, clears, forward, loss, backward, exchanges, SGD:
+        every step of the batch is a library kernel or a stream-ordered copy/memset with
+        the batch's geometry baked in), sharing one memory pool."""
+        for _ in range(warmup):
+            self.train_epoch(sync_loss=False)
+        torch.cuda.synchronize(self.d)
+        self.graphs, pool = [], None
+        for i in range(len(self.geoms)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=pool):
+                self.train_batch(i)
+            pool = g.pool()
+            self.graphs.append(g)
+        torch.cuda.synchronize(self.d)
+
+    def replay_epoch(self, sync_loss: bool = False):
+        """One epoch as R graph replays (capture() first)."""
+        self.epoch_loss.zero_()
+        for g in self.graphs:
+            g.replay()
+        if sync_loss:
+            return float(self.epoch_loss.item()) / max(self.total_targets, 1)
+        return None

@@ -13,6 +13,8 @@
 //  * partial sums of the lane groups are combined with xor-shuffles and the
 //    whole epilogue (self term, destination scale, SAGE self path, ReLU,
 //    fp32 and split-bf16 stores) is fused, so the output is written once.
+#include <cstdlib>
+
 #include "gdx_common.cuh"
 
 // Occupancy: 8 resident 256-thread blocks (64 warps, <= 32 registers; the few spills
@@ -94,6 +96,10 @@ struct AggParams {
     uint16_t* out_hi;
     uint16_t* out_lo;
     uint64_t ld_split;
+    const uint8_t* src_lo8;   // packed-24 source: src is the u16 high plane, this the u8 low plane
+    uint16_t* out24_hi;       // optional packed-24 copy of the output
+    uint8_t* out24_lo;
+    uint64_t ld_out24;
 };
 
 constexpr int pow2_floor(int x) { return x >= 32 ? 32 : x >= 16 ? 16 : x >= 8 ? 8 : x >= 4 ? 4 : x >= 2 ? 2 : 1; }
@@ -371,6 +377,311 @@ __global__ void __launch_bounds__(256) aggregate_scalar(const AggParams p, uint3
     }
 }
 
+// ---- packed-24 rows ----------------------------------------------------------------
+// A gathered matrix may be stored as fp32 rounded to 24 bits (sign, exponent, 15
+// mantissa bits; relative error <= 2^-16, the precision of the split-bf16 GEMM
+// operands that produce and consume it) in two planes: the high 16 bits (u16) and
+// the next 8 bits (u8).  A 64-wide row is then 128 + 64 bytes (6 sectors) instead
+// of 256 (8 sectors): the L2-bound gather moves 25% fewer bytes.  Decoding is three
+// byte permutes per two values; accumulation stays fp32.
+__device__ __forceinline__ void pack24(float x, uint16_t& hi, uint8_t& lo) {
+    uint32_t u = __float_as_uint(x);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x7fu + ((u >> 8) & 1u)) & 0xffffff00u;  // RNE at bit 8
+    hi = static_cast<uint16_t>(u >> 16);
+    lo = static_cast<uint8_t>(u >> 8);
+}
+__device__ __forceinline__ float unpack24(uint16_t hi, uint8_t lo) {
+    return __uint_as_float((static_cast<uint32_t>(hi) << 16) | (static_cast<uint32_t>(lo) << 8));
+}
+
+// 8 values from one 16-byte high-plane vector and one 8-byte low-plane vector
+__device__ __forceinline__ void decode8(const uint4 h, const uint2 l, float4& a, float4& b) {
+    // t = [l1 0 l0 0] style spreads of the low bytes, then [h.hi h.lo l 0] per value
+    const uint32_t t0 = __byte_perm(l.x, 0u, 0x1404), t1 = __byte_perm(l.x, 0u, 0x3424);
+    const uint32_t t2 = __byte_perm(l.y, 0u, 0x1404), t3 = __byte_perm(l.y, 0u, 0x3424);
+    a.x = __uint_as_float(__byte_perm(h.x, t0, 0x1054));
+    a.y = __uint_as_float(__byte_perm(h.x, t0, 0x3276));
+    a.z = __uint_as_float(__byte_perm(h.y, t1, 0x1054));
+    a.w = __uint_as_float(__byte_perm(h.y, t1, 0x3276));
+    b.x = __uint_as_float(__byte_perm(h.z, t2, 0x1054));
+    b.y = __uint_as_float(__byte_perm(h.z, t2, 0x3276));
+    b.z = __uint_as_float(__byte_perm(h.w, t3, 0x1054));
+    b.w = __uint_as_float(__byte_perm(h.w, t3, 0x3276));
+}
+
+__device__ __forceinline__ uint2 ld_row8b(const void* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_row16b(const void* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+// Epilogue of 8 columns [8 ch, 8 ch + 8) of one destination row (shared by the
+// packed-24 kernels): partial, self term, scale, SAGE add, ReLU, fp32 / split /
+// packed-24 stores.
+__device__ __forceinline__ void epilogue8(const AggParams& p, uint32_t row, uint32_t ch, float4 r0, float4 r1) {
+    const float scale = p.post_scale ? p.post_scale[row] : 1.f;
+    float v[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    const uint32_t c0 = 8 * ch;
+    if (p.partial) {
+        const float4 a = ld_plain4(p.partial + row * p.ld_partial + c0);
+        const float4 b = ld_plain4(p.partial + row * p.ld_partial + c0 + 4);
+        v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+        v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+    }
+    if (p.self_coef != 0.f) {
+        const uint64_t o = (p.self_base + row) * p.ld_src + c0;
+        const uint4 h = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.src) + o));
+        const uint2 l = __ldg(reinterpret_cast<const uint2*>(p.src_lo8 + o));
+        float4 a, b;
+        decode8(h, l, a, b);
+        v[0] += p.self_coef * a.x; v[1] += p.self_coef * a.y; v[2] += p.self_coef * a.z; v[3] += p.self_coef * a.w;
+        v[4] += p.self_coef * b.x; v[5] += p.self_coef * b.y; v[6] += p.self_coef * b.z; v[7] += p.self_coef * b.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] *= scale;
+    if (p.add) {
+        const float4 a = ld_plain4(p.add + row * p.ld_add + c0);
+        const float4 b = ld_plain4(p.add + row * p.ld_add + c0 + 4);
+        v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+        v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+    }
+    if (p.relu) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+    }
+    if (p.out) {
+        *reinterpret_cast<float4*>(p.out + row * p.ld_out + c0) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(p.out + row * p.ld_out + c0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    if (p.out_hi) {
+        ushort4 h0, l0, h1, l1;
+        split_bf16(v[0], h0.x, l0.x); split_bf16(v[1], h0.y, l0.y);
+        split_bf16(v[2], h0.z, l0.z); split_bf16(v[3], h0.w, l0.w);
+        split_bf16(v[4], h1.x, l1.x); split_bf16(v[5], h1.y, l1.y);
+        split_bf16(v[6], h1.z, l1.z); split_bf16(v[7], h1.w, l1.w);
+        *reinterpret_cast<ushort4*>(p.out_hi + row * p.ld_split + c0) = h0;
+        *reinterpret_cast<ushort4*>(p.out_hi + row * p.ld_split + c0 + 4) = h1;
+        *reinterpret_cast<ushort4*>(p.out_lo + row * p.ld_split + c0) = l0;
+        *reinterpret_cast<ushort4*>(p.out_lo + row * p.ld_split + c0 + 4) = l1;
+    }
+    if (p.out24_hi) {
+        uint16_t h[8];
+        uint8_t l[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pack24(v[i], h[i], l[i]);
+        *reinterpret_cast<uint4*>(p.out24_hi + row * p.ld_out24 + c0) = *reinterpret_cast<uint4*>(h);
+        *reinterpret_cast<uint2*>(p.out24_lo + row * p.ld_out24 + c0) = *reinterpret_cast<uint2*>(l);
+    }
+}
+
+// Warp per destination row over packed-24 sources: LPE lanes x 8 values cover a row,
+// EPW rows in flight per warp step, UNROLL steps unrolled.
+template <int LPE, int UNROLL, int MINB>
+__global__ void __launch_bounds__(256, MINB) aggregate_p24(const AggParams p) {
+    constexpr int EPW = pow2_floor(32 / LPE);
+    constexpr int STEP = EPW * UNROLL;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / LPE;
+    const int lin = lane - sub * LPE;
+    const bool lane_on = sub < EPW;
+    uint64_t pol_keep, pol_stream;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const uint64_t hbase = reinterpret_cast<uint64_t>(p.src) + 16 * lin;
+    const uint64_t lbase = reinterpret_cast<uint64_t>(p.src_lo8) + 8 * lin;
+    const uint32_t ldh = static_cast<uint32_t>(p.ld_src * 2), ldl = static_cast<uint32_t>(p.ld_src);
+    const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < p.rows; row += warps_total) {
+        const uint64_t beg = p.row_ptr[row];
+        const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
+        float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+        const int nseg = p.skip_lo ? 2 : 1;
+        for (int seg = 0; seg < nseg; ++seg) {
+            uint64_t sbeg = beg, send = end;
+            if (p.skip_lo) {
+                if (seg == 0) send = p.skip_lo[row];
+                else sbeg = p.skip_hi[row];
+            }
+            uint32_t my = (sbeg + lane < send) ? ld_stream_u32(p.col + sbeg + lane, pol_stream) : 0u;
+            for (uint64_t e0 = sbeg; e0 < send; e0 += 32) {
+                const uint32_t cnt = static_cast<uint32_t>((send - e0) < 32 ? (send - e0) : 32);
+                const uint64_t e1 = e0 + 32;
+                const uint32_t nxt = (e1 + lane < send) ? ld_stream_u32(p.col + e1 + lane, pol_stream) : 0u;
+                uint32_t j = 0;
+                for (; j + STEP <= cnt; j += STEP) {
+                    uint4 h[UNROLL];
+                    uint2 l[UNROLL];
+#pragma unroll
+                    for (int u = 0; u < UNROLL; ++u) {
+                        const uint32_t nb = __shfl_sync(0xffffffffu, my, (j + u * EPW + sub) & 31);
+                        if (lane_on) {
+                            h[u] = ld_row16b(row_addr(hbase, nb, ldh), pol_keep);
+                            l[u] = ld_row8b(row_addr(lbase, nb, ldl), pol_keep);
+                        } else {
+                            h[u] = make_uint4(0, 0, 0, 0);
+                            l[u] = make_uint2(0, 0);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < UNROLL; ++u) {
+                        float4 x0, x1;
+                        decode8(h[u], l[u], x0, x1);
+                        add4(a0, x0);
+                        add4(a1, x1);
+                    }
+                }
+                for (; j < cnt; j += EPW) {
+                    const uint32_t slot = j + sub;
+                    const uint32_t nb = __shfl_sync(0xffffffffu, my, slot & 31);
+                    if (lane_on && slot < cnt) {
+                        float4 x0, x1;
+                        decode8(ld_row16b(row_addr(hbase, nb, ldh), pol_keep), ld_row8b(row_addr(lbase, nb, ldl), pol_keep),
+                                x0, x1);
+                        add4(a0, x0);
+                        add4(a1, x1);
+                    }
+                }
+                my = nxt;
+            }
+        }
+#pragma unroll
+        for (int k = EPW / 2; k >= 1; k >>= 1) {
+            a0.x += __shfl_down_sync(0xffffffffu, a0.x, k * LPE);
+            a0.y += __shfl_down_sync(0xffffffffu, a0.y, k * LPE);
+            a0.z += __shfl_down_sync(0xffffffffu, a0.z, k * LPE);
+            a0.w += __shfl_down_sync(0xffffffffu, a0.w, k * LPE);
+            a1.x += __shfl_down_sync(0xffffffffu, a1.x, k * LPE);
+            a1.y += __shfl_down_sync(0xffffffffu, a1.y, k * LPE);
+            a1.z += __shfl_down_sync(0xffffffffu, a1.z, k * LPE);
+            a1.w += __shfl_down_sync(0xffffffffu, a1.w, k * LPE);
+        }
+        if (sub == 0) epilogue8(p, row, lin, a0, a1);
+    }
+}
+
+// Lane group per destination row (low-degree rows) over packed-24 sources.
+template <int LPE, int UNROLL, int MINB>
+__global__ void __launch_bounds__(256, MINB) aggregate_rows_p24(const AggParams p) {
+    constexpr int EPW = pow2_floor(32 / LPE);
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / LPE;
+    const int lin = lane - sub * LPE;
+    if (sub >= EPW) return;
+    uint64_t pol_keep, pol_stream;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const uint64_t hbase = reinterpret_cast<uint64_t>(p.src) + 16 * lin;
+    const uint64_t lbase = reinterpret_cast<uint64_t>(p.src_lo8) + 8 * lin;
+    const uint32_t ldh = static_cast<uint32_t>(p.ld_src * 2), ldl = static_cast<uint32_t>(p.ld_src);
+    const uint64_t groups = static_cast<uint64_t>((gridDim.x * blockDim.x) >> 5) * EPW;
+    for (uint64_t r = static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * EPW + sub; r < p.rows;
+         r += groups) {
+        const uint32_t row = static_cast<uint32_t>(r);
+        const uint64_t beg = p.row_ptr[row];
+        const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
+        float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+        const int nseg = p.skip_lo ? 2 : 1;
+        for (int seg = 0; seg < nseg; ++seg) {
+            uint64_t e = beg, send = end;
+            if (p.skip_lo) {
+                if (seg == 0) send = p.skip_lo[row];
+                else e = p.skip_hi[row];
+            }
+            for (; e + UNROLL <= send; e += UNROLL) {
+                uint32_t nb[UNROLL];
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) nb[u] = ld_stream_u32(p.col + e + u, pol_stream);
+                uint4 h[UNROLL];
+                uint2 l[UNROLL];
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    h[u] = ld_row16b(row_addr(hbase, nb[u], ldh), pol_keep);
+                    l[u] = ld_row8b(row_addr(lbase, nb[u], ldl), pol_keep);
+                }
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    float4 x0, x1;
+                    decode8(h[u], l[u], x0, x1);
+                    add4(a0, x0);
+                    add4(a1, x1);
+                }
+            }
+            for (; e < send; ++e) {
+                const uint32_t nb = ld_stream_u32(p.col + e, pol_stream);
+                float4 x0, x1;
+                decode8(ld_row16b(row_addr(hbase, nb, ldh), pol_keep), ld_row8b(row_addr(lbase, nb, ldl), pol_keep), x0,
+                        x1);
+                add4(a0, x0);
+                add4(a1, x1);
+            }
+        }
+        epilogue8(p, row, lin, a0, a1);
+    }
+}
+
+__global__ void pack24_kernel(const float* src, uint64_t ld_src, uint32_t rows, uint32_t cols, uint16_t* hi,
+                              uint8_t* lo, uint64_t ld_dst) {
+    const uint64_t total = static_cast<uint64_t>(rows) * cols;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / cols, c = i % cols;
+        pack24(src[r * ld_src + c], hi[r * ld_dst + c], lo[r * ld_dst + c]);
+    }
+}
+
+__global__ void unpack24_kernel(const uint16_t* hi, const uint8_t* lo, uint64_t ld_src, uint32_t rows, uint32_t cols,
+                                float* dst, uint64_t ld_dst) {
+    const uint64_t total = static_cast<uint64_t>(rows) * cols;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / cols, c = i % cols;
+        dst[r * ld_dst + c] = unpack24(hi[r * ld_src + c], lo[r * ld_src + c]);
+    }
+}
+
+int launch_p24(const AggParams& p, int variant, cudaStream_t s) {
+    const uint32_t c8 = p.c4 / 2;
+    auto vec = [&](auto kern, int epw) {
+        uint64_t blocks = (static_cast<uint64_t>(p.rows) + 7) / 8;
+        if (variant == GDX_AGG_ROWS) blocks = (static_cast<uint64_t>(p.rows) + 8 * epw - 1) / (8 * epw);
+        if (blocks > 65535ull * 64) blocks = 65535ull * 64;
+        kern<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
+    };
+    const bool rows = variant == GDX_AGG_ROWS;
+    // resident blocks per SM (registers): GDX_P24_MINB tuning knob, default 6 (40 registers)
+    static const int minb = [] {
+        const char* e = std::getenv("GDX_P24_MINB");
+        return e ? std::atoi(e) : 6;
+    }();
+#define GDX_P24_CASE(C8, LPE, UN, EPW)                                                          \
+    case C8:                                                                                    \
+        if (minb >= 8) rows ? vec(aggregate_rows_p24<LPE, UN, 8>, EPW) : vec(aggregate_p24<LPE, UN, 8>, EPW); \
+        else if (minb >= 6) rows ? vec(aggregate_rows_p24<LPE, UN, 6>, EPW) : vec(aggregate_p24<LPE, UN, 6>, EPW); \
+        else rows ? vec(aggregate_rows_p24<LPE, UN, 4>, EPW) : vec(aggregate_p24<LPE, UN, 4>, EPW); \
+        return 0;
+    switch (c8) {
+        GDX_P24_CASE(1, 1, 4, 32)
+        GDX_P24_CASE(2, 2, 4, 16)
+        GDX_P24_CASE(4, 4, 4, 8)
+        GDX_P24_CASE(6, 6, 4, 4)
+        GDX_P24_CASE(8, 8, 4, 4)
+        GDX_P24_CASE(12, 12, 4, 2)
+        GDX_P24_CASE(16, 16, 4, 2)
+        GDX_P24_CASE(32, 32, 2, 1)
+        default: return -1;
+    }
+#undef GDX_P24_CASE
+}
+
 // Per-row sub-range of column ids in [lo, hi): rows are sorted, so it is contiguous.
 __global__ void row_split_kernel(const uint64_t* row_ptr, const uint32_t* col, uint32_t rows,
                                  uint32_t lo, uint32_t hi, uint64_t* seg_lo, uint64_t* seg_hi) {
@@ -495,7 +806,27 @@ int aggregate_impl(const gdx_aggregate_args* a, int variant, gdx_stream stream) 
     AggParams p{a->row_ptr, a->row_end, a->skip_lo, a->skip_hi, a->partial, a->ld_partial, a->col,
                 a->rows, a->width / 4, a->src, a->ld_src,
                 static_cast<uint32_t>(a->ld_src * 4), a->self_coef, a->self_base, a->post_scale,
-                a->add, a->ld_add, a->relu, a->out, a->ld_out, a->out_hi, a->out_lo, a->ld_split};
+                a->add, a->ld_add, a->relu, a->out, a->ld_out, a->out_hi, a->out_lo, a->ld_split,
+                a->src_lo8, a->out24_hi, a->out24_lo, a->ld_out24};
+    if (a->src_lo8 || a->out24_hi) {
+        // packed-24 rows: widths in whole 8-value groups (8..256, 48 included), 16-byte rows
+        GDX_REQUIRE(!a->out24_hi == !a->out24_lo, GDX_INPUT, "gdx_aggregate: out24_hi/out24_lo must pair");
+        GDX_REQUIRE(a->width % 8 == 0 && a->ld_src % 8 == 0 && aligned16(a->src) &&
+                        (!a->src_lo8 || (reinterpret_cast<uintptr_t>(a->src_lo8) & 7) == 0),
+                    GDX_INPUT, "gdx_aggregate: packed-24 rows need width and pitch multiples of 8");
+        GDX_REQUIRE(a->src_lo8, GDX_INPUT, "gdx_aggregate: a packed-24 output needs a packed-24 source");
+        GDX_REQUIRE(!a->out24_hi || (a->ld_out24 % 8 == 0 && aligned16(a->out24_hi) &&
+                                     (reinterpret_cast<uintptr_t>(a->out24_lo) & 7) == 0),
+                    GDX_INPUT, "gdx_aggregate: packed-24 output pitch must be a multiple of 8");
+        GDX_REQUIRE((!a->add || (a->ld_add % 4 == 0 && aligned16(a->add))) &&
+                        (!a->partial || (a->ld_partial % 4 == 0 && aligned16(a->partial))) &&
+                        (!a->out || (a->ld_out % 4 == 0 && aligned16(a->out))),
+                    GDX_INPUT, "gdx_aggregate: packed-24 epilogue operands must be 16-byte rows");
+        GDX_REQUIRE(launch_p24(p, variant, as_cuda(stream)) == 0, GDX_INPUT,
+                    "gdx_aggregate: packed-24 width must be 8, 16, 32, 48, 64, 96, 128 or 256");
+        note_launch();
+        return check_launch("gdx_aggregate");
+    }
     const bool vec = a->width % 4 == 0 && a->ld_src % 4 == 0 && aligned16(a->src) && a->width <= 4096 &&
                      a->ld_src * 4 < (1ull << 32) &&
                      (!a->add || (a->ld_add % 4 == 0 && aligned16(a->add))) &&
@@ -536,4 +867,28 @@ extern "C" int gdx_row_split(const uint64_t* row_ptr, const uint32_t* col, uint3
     gdx::row_split_kernel<<<blocks, 256, 0, gdx::as_cuda(stream)>>>(row_ptr, col, rows, lo, hi, seg_lo, seg_hi);
     gdx::note_launch();
     return gdx::check_launch("gdx_row_split");
+}
+
+extern "C" int gdx_pack24(const float* src, uint64_t ld_src, uint32_t rows, uint32_t cols, uint16_t* hi,
+                          uint8_t* lo, uint64_t ld_dst, gdx_stream stream) {
+    GDX_REQUIRE(src && hi && lo, GDX_INPUT, "gdx_pack24: null pointer");
+    if (!rows || !cols) return GDX_OK;
+    uint64_t blocks = (static_cast<uint64_t>(rows) * cols + 255) / 256;
+    if (blocks > static_cast<uint64_t>(gdx::device_sms()) * 16) blocks = static_cast<uint64_t>(gdx::device_sms()) * 16;
+    gdx::pack24_kernel<<<static_cast<unsigned>(blocks), 256, 0, gdx::as_cuda(stream)>>>(src, ld_src, rows, cols, hi,
+                                                                                        lo, ld_dst);
+    gdx::note_launch();
+    return gdx::check_launch("gdx_pack24");
+}
+
+extern "C" int gdx_unpack24(const uint16_t* hi, const uint8_t* lo, uint64_t ld_src, uint32_t rows, uint32_t cols,
+                            float* dst, uint64_t ld_dst, gdx_stream stream) {
+    GDX_REQUIRE(hi && lo && dst, GDX_INPUT, "gdx_unpack24: null pointer");
+    if (!rows || !cols) return GDX_OK;
+    uint64_t blocks = (static_cast<uint64_t>(rows) * cols + 255) / 256;
+    if (blocks > static_cast<uint64_t>(gdx::device_sms()) * 16) blocks = static_cast<uint64_t>(gdx::device_sms()) * 16;
+    gdx::unpack24_kernel<<<static_cast<unsigned>(blocks), 256, 0, gdx::as_cuda(stream)>>>(hi, lo, ld_src, rows, cols,
+                                                                                          dst, ld_dst);
+    gdx::note_launch();
+    return gdx::check_launch("gdx_unpack24");
 }

@@ -277,6 +277,18 @@ extern "C" int gdx_memcpy_async(void* dst, const void* src, uint64_t bytes, gdx_
     return GDX_OK;
 }
 
+extern "C" int gdx_memset2d_async(void* dst, uint64_t pitch_bytes, int value, uint64_t width_bytes, uint64_t rows,
+                                  gdx_stream stream) {
+    GDX_REQUIRE(dst || rows == 0 || width_bytes == 0, GDX_INPUT, "gdx_memset2d_async: null pointer");
+    GDX_REQUIRE(rows <= 1 || pitch_bytes >= width_bytes, GDX_INPUT, "gdx_memset2d_async: pitch < width");
+    if (!rows || !width_bytes) return GDX_OK;
+    if (rows == 1 || pitch_bytes == width_bytes)
+        GDX_CUDA(cudaMemsetAsync(dst, value, width_bytes * rows, as_cuda(stream)));
+    else
+        GDX_CUDA(cudaMemset2DAsync(dst, pitch_bytes, value, width_bytes, rows, as_cuda(stream)));
+    return GDX_OK;
+}
+
 // SM-driven push + signal (see push_peers_kernel); `done` is a zeroed device counter.
 extern "C" int gdx_push_peers(const void* src, uint64_t bytes, const int64_t* peer_delta, uint32_t npeers,
                               unsigned long long* const* peer_slots_dev, unsigned int* done, uint32_t ctas,

@@ -77,14 +77,26 @@ struct DevCSR {
     uint32_t rows = 0;
 };
 
-DevCSR upload(const Graph& g) {
-    DevCSR d;
-    d.rp = Dev<uint64_t>(g.row_offsets().data(), g.row_offsets().size());
-    d.col = g.col_indices().empty() ? Dev<uint32_t>(1)
-                                    : Dev<uint32_t>(g.col_indices().data(), g.col_indices().size());
-    d.rows = g.num_vertices();
-    return d;
-}
+}  // namespace
+
+// The device copy of a Graph's CSR, uploaded once per graph (Graph::device_).
+struct GraphDevice {
+    static const DevCSR& get(const Graph& g) {
+        if (!g.device_) {
+            auto d = std::make_shared<DevCSR>();
+            d->rp = Dev<uint64_t>(g.row_offsets().data(), g.row_offsets().size());
+            d->col = g.col_indices().empty() ? Dev<uint32_t>(1)
+                                             : Dev<uint32_t>(g.col_indices().data(), g.col_indices().size());
+            d->rows = g.num_vertices();
+            g.device_ = d;
+        }
+        return *static_cast<const DevCSR*>(g.device_.get());
+    }
+};
+
+namespace {
+
+const DevCSR& upload(const Graph& g) { return GraphDevice::get(g); }
 
 // split-bf16 copy of an fp32 device matrix (rows x cols, pitch ld) with pitch pad8(cols)
 struct Split {
@@ -206,7 +218,7 @@ Partition finish(std::vector<std::uint32_t> a, std::uint32_t parts) {
 DependencySubgraph grow(const Graph& g, const Partition& p, std::uint32_t server, std::uint32_t max_hop,
                         std::uint32_t fanout, std::uint64_t seed, bool sampled) {
     const uint32_t n = g.num_vertices();
-    DevCSR csr = upload(g);
+    const DevCSR& csr = upload(g);
     std::vector<uint8_t> inner(n);
     std::vector<uint32_t> mark(n);
     for (uint32_t v = 0; v < n; ++v) {
@@ -537,7 +549,7 @@ DenseFeatures forward_full(const Graph& g, const DenseFeatures& x, const LayerWe
     if (x.rows != g.num_vertices()) throw InputError("forward_full: feature rows do not match vertex count");
     check_shapes(x, w, layers);
     if (layers == 0) return x;
-    DevCSR csr = upload(g);
+    const DevCSR& csr = upload(g);
     const uint32_t n = g.num_vertices();
     uint32_t width = 0;
     Dev<float> out = run_layers(csr, n, upload_features(x), x.cols, w, layers,
@@ -569,7 +581,7 @@ DenseFeatures forward_server_local(const DependencySubgraph& sub, const Graph& g
         hop[sub.halo_vertices[i]] = sub.halo_hops[i];
         max_hop = std::max(max_hop, sub.halo_hops[i]);
     }
-    DevCSR gcsr = upload(g);
+    const DevCSR& gcsr = upload(g);
     Dev<uint32_t> dhop(hop.data(), n);
     Dev<uint32_t> l2g(n), local_of(n);
     std::vector<uint64_t> hop_start(max_hop + 2, 0);
@@ -650,7 +662,7 @@ std::vector<std::vector<VertexId>> target_groups(const Graph& g, const std::vect
 
 // The planner's device context: graph + server universe resident for the whole R scan.
 struct PlanDevice {
-    DevCSR csr;
+    const DevCSR& csr;
     Dev<uint8_t> universe;
     uint32_t n = 0;
     PlanDevice(const Graph& g, const DependencySubgraph& sub) : csr(upload(g)), n(g.num_vertices()) {
