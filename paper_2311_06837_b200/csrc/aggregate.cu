@@ -657,10 +657,11 @@ int launch_p24(const AggParams& p, int variant, cudaStream_t s) {
         kern<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
     };
     const bool rows = variant == GDX_AGG_ROWS;
-    // resident blocks per SM (registers): GDX_P24_MINB tuning knob, default 6 (40 registers)
+    // resident blocks per SM: GDX_P24_MINB tuning knob, default 4 (60 registers, no spills;
+    // measured: Reddit 64-wide 1.22 ms at 4, 1.69 at 6, 2.61 at 8 -- tools/agg24_bench.py)
     static const int minb = [] {
         const char* e = std::getenv("GDX_P24_MINB");
-        return e ? std::atoi(e) : 6;
+        return e ? std::atoi(e) : 4;
     }();
 #define GDX_P24_CASE(C8, LPE, UN, EPW)                                                          \
     case C8:                                                                                    \
