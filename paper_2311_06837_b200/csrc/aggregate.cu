@@ -768,8 +768,21 @@ int launch_rows_any(const AggParams& p, cudaStream_t s) {
 
 // variant: 4 / 8 = unroll depth of the exact 12/16-lane warp-per-row kernels
 // (tuning); GDX_AGG_ROWS = the lane-group-per-row kernel for low-degree rows.
+// GDX_AGG_ROWS2: lane groups of half the width, two 16-byte chunks per lane, so twice
+// the destination rows (independent row_ptr -> col -> row chains) per warp.
+int launch_rows_wide(const AggParams& p, cudaStream_t s) {
+    switch (p.c4) {
+        case 16: launch_rows<8, 2, true>(p, s); return 0;
+        case 12: launch_rows<6, 2, true>(p, s); return 0;
+        case 32: launch_rows<16, 2, true>(p, s); return 0;
+        case 8: launch_rows<4, 2, true>(p, s); return 0;
+        default: return launch_rows_any(p, s);
+    }
+}
+
 int launch_variant(const AggParams& p, int variant, cudaStream_t s) {
     if (variant == GDX_AGG_ROWS) return launch_rows_any(p, s);
+    if (variant == 2) return launch_rows_wide(p, s);
     const bool u8 = variant == 8;
     if (p.c4 == 16) {
         if (u8) launch_vec<16, 1, true, 8>(p, s);
