@@ -111,6 +111,31 @@ typedef struct gdx_aggregate_args {
     uint8_t* out24_lo;
     uint64_t ld_out24;
 } gdx_aggregate_args;
+/* Degree-binned load balancing for skewed graphs (replaces the reference's uniform
+ * per-vertex loop, reference_gnn.cpp:76-83, for hub-heavy inputs): rows with more
+ * than heavy_degree edges are cut into chunks of chunk_edges edges; one warp per chunk
+ * gathers an fp32 partial row, one warp per heavy row sums its chunks in order
+ * (deterministic) and applies the epilogue; the other rows run the normal kernels
+ * through a row list.  Built once per CSR from its HOST row offsets. */
+typedef struct gdx_row_bins {
+    uint32_t rows, n_light, n_heavy, n_chunks, chunk_edges;
+    uint32_t* light_rows;       /* device, ascending */
+    uint32_t* heavy_rows;       /* device, ascending */
+    uint32_t* chunk_row;        /* device [n_chunks]: position in heavy_rows */
+    uint64_t* chunk_beg;        /* device [n_chunks]: first edge of the chunk */
+    uint64_t* chunk_off;        /* device [n_heavy+1]: chunks of each heavy row */
+    float* partial;             /* device workspace [n_chunks x ld_partial] */
+    uint64_t ld_partial;
+    uint32_t* light_host;       /* host copies (prefix sizes per call) */
+    uint32_t* heavy_host;
+    uint64_t* chunk_off_host;
+} gdx_row_bins;
+int gdx_row_bins_build(const uint64_t* row_ptr_host, uint32_t rows, uint32_t heavy_degree, uint32_t chunk_edges,
+                       uint32_t max_width, gdx_row_bins** out);
+int gdx_row_bins_free(gdx_row_bins* bins);
+/* gdx_aggregate_variant over the bins (bins NULL or no heavy row: the plain call).
+ * Rows >= a->rows are skipped (hop prefixes).  fp32 rows only. */
+int gdx_aggregate_balanced(const gdx_aggregate_args* a, int variant, const gdx_row_bins* bins, gdx_stream stream);
 /* fp32 <-> packed-24 conversion (round to nearest even at bit 8). */
 int gdx_pack24(const float* src, uint64_t ld_src, uint32_t rows, uint32_t cols, uint16_t* hi, uint8_t* lo,
                uint64_t ld_dst, gdx_stream stream);
@@ -368,6 +393,8 @@ typedef struct gdx_trainer_config {
     int no_agg_first;         /* 1: widening SAGE output layers stay transform-first */
     uint32_t push_ctas;       /* CTAs of the NVLink push kernel (0: 32) */
     double peer_timeout_s;    /* peer wait traps after this (0: 20 s); a trap poisons the context */
+    uint32_t heavy_degree;    /* rows above this degree run chunked (gdx_row_bins); 0: auto
+                               * (max(4096, 32 x mean degree)), 0xFFFFFFFF: never */
 } gdx_trainer_config;
 typedef struct gdx_trainer_graph {
     uint32_t num_vertices;          /* V of the whole graph */
@@ -410,7 +437,7 @@ int gdx_trainer_step_staged(gdx_trainer* t, int with_labels, double* loss_out);
 /* The trainer's stream (cudaStream_t) for event timing by the caller. */
 void* gdx_trainer_stream(gdx_trainer* t);
 /* out[0..]: local rows, local nnz, first row, gathered rows, loss rows, loss count,
- * graph captured, aggregate-first output layer, local-source nnz. */
+ * graph captured, aggregate-first output layer, local-source nnz, heavy (chunked) rows. */
 int gdx_trainer_info(const gdx_trainer* t, uint64_t* out, uint32_t count);
 /* Per-aggregation CUDA events on eager epochs (on = 1); reading (non-null outputs)
  * returns the total ms, launch count and algorithmic bytes since on. */

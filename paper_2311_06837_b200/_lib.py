@@ -31,6 +31,13 @@ class AggregateArgs(C.Structure):
     ]
 
 
+class RowBins(C.Structure):
+    _fields_ = [("rows", u32), ("n_light", u32), ("n_heavy", u32), ("n_chunks", u32), ("chunk_edges", u32),
+                ("light_rows", vp), ("heavy_rows", vp), ("chunk_row", vp), ("chunk_beg", vp), ("chunk_off", vp),
+                ("partial", vp), ("ld_partial", u64), ("light_host", vp), ("heavy_host", vp),
+                ("chunk_off_host", vp)]
+
+
 class GemmArgs(C.Structure):
     _fields_ = [
         ("a_hi", vp), ("a_lo", vp), ("lda", u64), ("b_hi", vp), ("b_lo", vp), ("ldb", u64),
@@ -56,6 +63,9 @@ _SIGS = {
     "gdx_init_labels": (C.c_int, [u64, u64, u32, u32, vp, vp]),
     "gdx_aggregate": (C.c_int, [C.POINTER(AggregateArgs), vp]),
     "gdx_pack24": (C.c_int, [vp, u64, u32, u32, vp, vp, u64, vp]),
+    "gdx_row_bins_build": (C.c_int, [vp, u32, u32, u32, u32, C.POINTER(C.POINTER(RowBins))]),
+    "gdx_row_bins_free": (C.c_int, [C.POINTER(RowBins)]),
+    "gdx_aggregate_balanced": (C.c_int, [C.POINTER(AggregateArgs), C.c_int, C.POINTER(RowBins), vp]),
     "gdx_unpack24": (C.c_int, [vp, vp, u64, u32, u32, vp, u64, vp]),
     "gdx_aggregate_variant": (C.c_int, [C.POINTER(AggregateArgs), C.c_int, vp]),
     "gdx_row_split": (C.c_int, [vp, vp, u32, u32, u32, vp, vp, vp]),

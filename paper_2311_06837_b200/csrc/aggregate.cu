@@ -13,7 +13,10 @@
 //  * partial sums of the lane groups are combined with xor-shuffles and the
 //    whole epilogue (self term, destination scale, SAGE self path, ReLU,
 //    fp32 and split-bf16 stores) is fused, so the output is written once.
+#include <algorithm>
 #include <cstdlib>
+#include <type_traits>
+#include <vector>
 
 #include "gdx_common.cuh"
 
@@ -96,6 +99,7 @@ struct AggParams {
     uint16_t* out_hi;
     uint16_t* out_lo;
     uint64_t ld_split;
+    const uint32_t* row_list; // optional: the rows to compute (list position -> destination row)
     const uint8_t* src_lo8;   // packed-24 source: src is the u16 high plane, this the u8 low plane
     uint16_t* out24_hi;       // optional packed-24 copy of the output
     uint8_t* out24_lo;
@@ -124,8 +128,9 @@ __global__ void __launch_bounds__(256, agg_min_blocks(LPE, NCH)) aggregate_vec4(
     for (int c = 0; c < NCH; ++c) chan_on[c] = EXACT || (lin + c * LPE) < p.c4;
 
     const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < p.rows;
-         row += warps_total) {
+    for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < p.rows;
+         it += warps_total) {
+        const uint32_t row = p.row_list ? p.row_list[it] : it;
         const uint64_t beg = p.row_ptr[row];
         const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
         float4 acc[NCH];
@@ -263,7 +268,7 @@ __global__ void __launch_bounds__(256, agg_min_blocks(LPE == 12 ? 16 : LPE, NCH)
     const uint64_t groups = static_cast<uint64_t>((gridDim.x * blockDim.x) >> 5) * EPW;
     for (uint64_t r = static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * EPW + sub;
          r < p.rows; r += groups) {
-        const uint32_t row = static_cast<uint32_t>(r);
+        const uint32_t row = p.row_list ? p.row_list[r] : static_cast<uint32_t>(r);
         const uint64_t beg = p.row_ptr[row];
         const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
         float4 acc[NCH];
@@ -356,8 +361,9 @@ __global__ void __launch_bounds__(256, agg_min_blocks(LPE == 12 ? 16 : LPE, NCH)
 __global__ void __launch_bounds__(256) aggregate_scalar(const AggParams p, uint32_t width) {
     const int lane = threadIdx.x & 31;
     const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < p.rows;
-         row += warps_total) {
+    for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < p.rows;
+         it += warps_total) {
+        const uint32_t row = p.row_list ? p.row_list[it] : it;
         const uint64_t beg = p.row_ptr[row];
         const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
         const uint64_t s0 = p.skip_lo ? p.skip_lo[row] : end, s1 = p.skip_hi ? p.skip_hi[row] : end;
@@ -500,7 +506,8 @@ __global__ void __launch_bounds__(256, MINB) aggregate_p24(const AggParams p) {
     const uint64_t lbase = reinterpret_cast<uint64_t>(p.src_lo8) + 8 * lin;
     const uint32_t ldh = static_cast<uint32_t>(p.ld_src * 2), ldl = static_cast<uint32_t>(p.ld_src);
     const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < p.rows; row += warps_total) {
+    for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < p.rows; it += warps_total) {
+        const uint32_t row = p.row_list ? p.row_list[it] : it;
         const uint64_t beg = p.row_ptr[row];
         const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
         float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
@@ -585,7 +592,7 @@ __global__ void __launch_bounds__(256, MINB) aggregate_rows_p24(const AggParams 
     const uint64_t groups = static_cast<uint64_t>((gridDim.x * blockDim.x) >> 5) * EPW;
     for (uint64_t r = static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * EPW + sub; r < p.rows;
          r += groups) {
-        const uint32_t row = static_cast<uint32_t>(r);
+        const uint32_t row = p.row_list ? p.row_list[r] : static_cast<uint32_t>(r);
         const uint64_t beg = p.row_ptr[row];
         const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
         float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
@@ -681,6 +688,142 @@ int launch_p24(const AggParams& p, int variant, cudaStream_t s) {
         default: return -1;
     }
 #undef GDX_P24_CASE
+}
+
+// ---- heavy rows (degree-binned load balancing) ----------------------------------
+// On skewed graphs a hub row (10^4..10^6 edges) would keep one warp busy long after
+// the rest of the pass finished.  Rows above a degree threshold are cut into chunks of
+// a fixed number of edges; one warp per chunk gathers it (the aggregate_vec4 inner
+// loop, same MLP) into an fp32 partial row, then one warp per heavy row sums its
+// chunks in chunk order (deterministic) and applies the epilogue.  Light rows run the
+// normal kernels through a row list.
+
+// Epilogue of one float4 column chunk (the fp32 kernels' epilogue, shared form).
+__device__ __forceinline__ void epi4(const AggParams& p, uint32_t row, uint32_t ch, float4 r) {
+    const float scale = p.post_scale ? p.post_scale[row] : 1.f;
+    if (p.partial) {
+        const float4 q = ld_plain4(p.partial + row * p.ld_partial + 4 * ch);
+        r.x += q.x; r.y += q.y; r.z += q.z; r.w += q.w;
+    }
+    if (p.self_coef != 0.f) {
+        const float4 q = ld_plain4(p.src + (p.self_base + row) * p.ld_src + 4 * ch);
+        r.x += p.self_coef * q.x; r.y += p.self_coef * q.y; r.z += p.self_coef * q.z; r.w += p.self_coef * q.w;
+    }
+    r.x *= scale; r.y *= scale; r.z *= scale; r.w *= scale;
+    if (p.add) {
+        const float4 q = ld_plain4(p.add + row * p.ld_add + 4 * ch);
+        r.x += q.x; r.y += q.y; r.z += q.z; r.w += q.w;
+    }
+    if (p.relu) {
+        r.x = fmaxf(r.x, 0.f); r.y = fmaxf(r.y, 0.f); r.z = fmaxf(r.z, 0.f); r.w = fmaxf(r.w, 0.f);
+    }
+    if (p.out) *reinterpret_cast<float4*>(p.out + row * p.ld_out + 4 * ch) = r;
+    if (p.out_hi) {
+        ushort4 h, l;
+        split_bf16(r.x, h.x, l.x); split_bf16(r.y, h.y, l.y); split_bf16(r.z, h.z, l.z); split_bf16(r.w, h.w, l.w);
+        *reinterpret_cast<ushort4*>(p.out_hi + row * p.ld_split + 4 * ch) = h;
+        *reinterpret_cast<ushort4*>(p.out_lo + row * p.ld_split + 4 * ch) = l;
+    }
+}
+
+// One warp per chunk: edges [chunk_beg, chunk_beg + chunk_edges) of row heavy[chunk_row],
+// clipped to the row's effective range (row_ptr / row_end) minus the skip range.
+template <int LPE, int NCH>
+__global__ void __launch_bounds__(256) heavy_chunks(const AggParams p, const uint32_t* heavy, const uint32_t* chunk_row,
+                                                   const uint64_t* chunk_beg, uint32_t nchunks, uint32_t chunk_edges,
+                                                   float* part, uint64_t ld_part) {
+    constexpr int EPW = pow2_floor(32 / LPE);
+    constexpr int UNROLL = 4;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / LPE;
+    const int lin = lane - sub * LPE;
+    const bool lane_on = sub < EPW;
+    uint64_t pol_keep, pol_stream;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const uint64_t base = reinterpret_cast<uint64_t>(p.src) + 16 * lin;
+    bool chan_on[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) chan_on[c] = (lin + c * LPE) < p.c4;
+    const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t ci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ci < nchunks; ci += warps_total) {
+        const uint32_t row = heavy[chunk_row[ci]];
+        const uint64_t rb = p.row_ptr[row];
+        const uint64_t re = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
+        const uint64_t cb = chunk_beg[ci], ce = cb + chunk_edges;
+        float4 acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int nseg = p.skip_lo ? 2 : 1;
+        for (int seg = 0; seg < nseg; ++seg) {
+            uint64_t a = rb, b = re;
+            if (p.skip_lo) {
+                if (seg == 0) b = p.skip_lo[row];
+                else a = p.skip_hi[row];
+            }
+            a = a > cb ? a : cb;
+            b = b < ce ? b : ce;
+            for (uint64_t e0 = a; e0 < b; e0 += 32) {
+                const uint32_t cnt = static_cast<uint32_t>((b - e0) < 32 ? (b - e0) : 32);
+                const uint32_t my = lane < cnt ? ld_stream_u32(p.col + e0 + lane, pol_stream) : 0u;
+                for (uint32_t j = 0; j < cnt; j += EPW * UNROLL) {
+                    float4 v[UNROLL][NCH];
+#pragma unroll
+                    for (int u = 0; u < UNROLL; ++u) {
+                        const uint32_t slot = j + u * EPW + sub;
+                        const uint32_t nb = __shfl_sync(0xffffffffu, my, slot & 31);
+                        const char* rp = row_addr(base, nb, p.ld_bytes);
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c)
+                            v[u][c] = (lane_on && chan_on[c] && slot < cnt) ? ld_row4(rp + 16 * LPE * c, pol_keep)
+                                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) add4(acc[c], v[u][c]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = EPW / 2; k >= 1; k >>= 1)
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                acc[c].x += __shfl_down_sync(0xffffffffu, acc[c].x, k * LPE);
+                acc[c].y += __shfl_down_sync(0xffffffffu, acc[c].y, k * LPE);
+                acc[c].z += __shfl_down_sync(0xffffffffu, acc[c].z, k * LPE);
+                acc[c].w += __shfl_down_sync(0xffffffffu, acc[c].w, k * LPE);
+            }
+        if (sub == 0) {
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+                if (chan_on[c]) *reinterpret_cast<float4*>(part + ci * ld_part + 4 * (lin + c * LPE)) = acc[c];
+        }
+    }
+}
+
+// One warp per heavy row: its chunk partials summed in chunk order, then the epilogue.
+__global__ void __launch_bounds__(256) heavy_combine(const AggParams p, const uint32_t* heavy, uint32_t nheavy,
+                                                     const uint64_t* chunk_off, const float* part, uint64_t ld_part) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < nheavy; h += warps_total) {
+        const uint32_t row = heavy[h];
+        for (uint32_t ch = lane; ch < p.c4; ch += 32) {
+            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (uint64_t c = chunk_off[h]; c < chunk_off[h + 1]; ++c) add4(r, ld_plain4(part + c * ld_part + 4 * ch));
+            epi4(p, row, ch, r);
+        }
+    }
+}
+
+template <int LPE, int NCH>
+void launch_heavy(const AggParams& p, const gdx_row_bins* b, uint32_t nchunks, cudaStream_t s) {
+    uint64_t blocks = (static_cast<uint64_t>(nchunks) + 7) / 8;
+    if (blocks > 65535ull * 64) blocks = 65535ull * 64;
+    heavy_chunks<LPE, NCH><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, b->heavy_rows, b->chunk_row, b->chunk_beg,
+                                                                         nchunks, b->chunk_edges, b->partial,
+                                                                         b->ld_partial);
 }
 
 // Per-row sub-range of column ids in [lo, hi): rows are sorted, so it is contiguous.
@@ -821,7 +964,7 @@ int aggregate_impl(const gdx_aggregate_args* a, int variant, gdx_stream stream) 
                 a->rows, a->width / 4, a->src, a->ld_src,
                 static_cast<uint32_t>(a->ld_src * 4), a->self_coef, a->self_base, a->post_scale,
                 a->add, a->ld_add, a->relu, a->out, a->ld_out, a->out_hi, a->out_lo, a->ld_split,
-                a->src_lo8, a->out24_hi, a->out24_lo, a->ld_out24};
+                nullptr, a->src_lo8, a->out24_hi, a->out24_lo, a->ld_out24};
     if (a->src_lo8 || a->out24_hi) {
         // packed-24 rows: widths in whole 8-value groups (8..256, 48 included), 16-byte rows
         GDX_REQUIRE(!a->out24_hi == !a->out24_lo, GDX_INPUT, "gdx_aggregate: out24_hi/out24_lo must pair");
@@ -905,4 +1048,128 @@ extern "C" int gdx_unpack24(const uint16_t* hi, const uint8_t* lo, uint64_t ld_s
                                                                                           dst, ld_dst);
     gdx::note_launch();
     return gdx::check_launch("gdx_unpack24");
+}
+
+// ---- degree bins ------------------------------------------------------------------
+extern "C" int gdx_row_bins_build(const uint64_t* row_ptr_host, uint32_t rows, uint32_t heavy_degree,
+                                  uint32_t chunk_edges, uint32_t max_width, gdx_row_bins** out) {
+    GDX_REQUIRE(row_ptr_host && out, GDX_INPUT, "gdx_row_bins_build: null pointer");
+    GDX_REQUIRE(heavy_degree >= 1 && chunk_edges >= 32 && max_width >= 1, GDX_INPUT,
+                "gdx_row_bins_build: heavy_degree >= 1, chunk_edges >= 32, max_width >= 1");
+    *out = nullptr;
+    std::vector<uint32_t> light, heavy, crow;
+    std::vector<uint64_t> cbeg, coff{0};
+    for (uint32_t v = 0; v < rows; ++v) {
+        const uint64_t d = row_ptr_host[v + 1] - row_ptr_host[v];
+        if (d <= heavy_degree) {
+            light.push_back(v);
+            continue;
+        }
+        for (uint64_t e = row_ptr_host[v]; e < row_ptr_host[v + 1]; e += chunk_edges) {
+            crow.push_back(static_cast<uint32_t>(heavy.size()));
+            cbeg.push_back(e);
+        }
+        heavy.push_back(v);
+        coff.push_back(cbeg.size());
+    }
+    auto* b = new gdx_row_bins{};
+    b->rows = rows;
+    b->n_light = static_cast<uint32_t>(light.size());
+    b->n_heavy = static_cast<uint32_t>(heavy.size());
+    b->n_chunks = static_cast<uint32_t>(cbeg.size());
+    b->chunk_edges = chunk_edges;
+    b->ld_partial = (static_cast<uint64_t>(max_width) + 3) / 4 * 4;
+    auto up = [](auto** dst, const auto& v) -> cudaError_t {
+        using T = typename std::remove_reference<decltype(v)>::type::value_type;
+        cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), std::max<size_t>(v.size(), 1) * sizeof(T));
+        if (e == cudaSuccess && !v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+        return e;
+    };
+    cudaError_t e = up(&b->light_rows, light);
+    if (e == cudaSuccess) e = up(&b->heavy_rows, heavy);
+    if (e == cudaSuccess) e = up(&b->chunk_row, crow);
+    if (e == cudaSuccess) e = up(&b->chunk_beg, cbeg);
+    if (e == cudaSuccess) e = up(&b->chunk_off, coff);
+    if (e == cudaSuccess)
+        e = cudaMalloc(reinterpret_cast<void**>(&b->partial), std::max<uint64_t>(b->n_chunks, 1) * b->ld_partial * 4);
+    b->light_host = new uint32_t[std::max<size_t>(light.size(), 1)];
+    b->heavy_host = new uint32_t[std::max<size_t>(heavy.size(), 1)];
+    b->chunk_off_host = new uint64_t[coff.size()];
+    std::copy(light.begin(), light.end(), b->light_host);
+    std::copy(heavy.begin(), heavy.end(), b->heavy_host);
+    std::copy(coff.begin(), coff.end(), b->chunk_off_host);
+    if (e != cudaSuccess) {
+        gdx_row_bins_free(b);
+        return gdx::fail(GDX_INTERNAL, std::string("gdx_row_bins_build: ") + cudaGetErrorString(e));
+    }
+    *out = b;
+    return GDX_OK;
+}
+
+extern "C" int gdx_row_bins_free(gdx_row_bins* b) {
+    if (!b) return GDX_OK;
+    cudaFree(b->light_rows);
+    cudaFree(b->heavy_rows);
+    cudaFree(b->chunk_row);
+    cudaFree(b->chunk_beg);
+    cudaFree(b->chunk_off);
+    cudaFree(b->partial);
+    delete[] b->light_host;
+    delete[] b->heavy_host;
+    delete[] b->chunk_off_host;
+    delete b;
+    return GDX_OK;
+}
+
+extern "C" int gdx_aggregate_balanced(const gdx_aggregate_args* a, int variant, const gdx_row_bins* b,
+                                      gdx_stream stream) {
+    using namespace gdx;
+    if (!b || b->n_heavy == 0) return aggregate_impl(a, variant, stream);
+    GDX_REQUIRE(a != nullptr, GDX_INPUT, "gdx_aggregate_balanced: null args");
+    GDX_REQUIRE(a->rows <= b->rows, GDX_INPUT, "gdx_aggregate_balanced: more rows than the bins");
+    GDX_REQUIRE(!a->src_lo8 && !a->out24_hi, GDX_INPUT, "gdx_aggregate_balanced: fp32 rows only");
+    GDX_REQUIRE(a->width % 4 == 0 && a->ld_src % 4 == 0 && (reinterpret_cast<uintptr_t>(a->src) & 15) == 0 &&
+                    a->width <= b->ld_partial,
+                GDX_INPUT, "gdx_aggregate_balanced: 16-byte rows, width <= the bins' max width");
+    if (a->rows == 0) return GDX_OK;
+    // rows < a->rows only (a hop prefix): lists are ascending, so prefixes of them
+    const uint32_t nl = static_cast<uint32_t>(std::lower_bound(b->light_host, b->light_host + b->n_light, a->rows) -
+                                              b->light_host);
+    const uint32_t nh = static_cast<uint32_t>(std::lower_bound(b->heavy_host, b->heavy_host + b->n_heavy, a->rows) -
+                                              b->heavy_host);
+    const uint32_t nc = static_cast<uint32_t>(b->chunk_off_host[nh]);
+    cudaStream_t s = as_cuda(stream);
+    if (nl) {
+        gdx_aggregate_args la = *a;
+        la.rows = nl;
+        // the light pass reuses aggregate_impl with the row list
+        AggParams p{la.row_ptr, la.row_end, la.skip_lo, la.skip_hi, la.partial, la.ld_partial, la.col, nl,
+                    la.width / 4, la.src, la.ld_src, static_cast<uint32_t>(la.ld_src * 4), la.self_coef, la.self_base,
+                    la.post_scale, la.add, la.ld_add, la.relu, la.out, la.ld_out, la.out_hi, la.out_lo, la.ld_split,
+                    b->light_rows, nullptr, nullptr, nullptr, 0};
+        if (variant) launch_variant(p, variant, s);
+        else pick_and_launch(p, s);
+        note_launch();
+        if (int rc = check_launch("gdx_aggregate_balanced")) return rc;
+    }
+    if (nh) {
+        AggParams p{a->row_ptr, a->row_end, a->skip_lo, a->skip_hi, a->partial, a->ld_partial, a->col, nh,
+                    a->width / 4, a->src, a->ld_src, static_cast<uint32_t>(a->ld_src * 4), a->self_coef, a->self_base,
+                    a->post_scale, a->add, a->ld_add, a->relu, a->out, a->ld_out, a->out_hi, a->out_lo, a->ld_split,
+                    nullptr, nullptr, nullptr, nullptr, 0};
+        const uint32_t c4 = p.c4;
+        if (c4 <= 8) launch_heavy<8, 1>(p, b, nc, s);
+        else if (c4 <= 16) launch_heavy<16, 1>(p, b, nc, s);
+        else if (c4 <= 32) launch_heavy<32, 1>(p, b, nc, s);
+        else if (c4 <= 64) launch_heavy<32, 2>(p, b, nc, s);
+        else launch_heavy<32, 8>(p, b, nc, s);
+        note_launch();
+        if (int rc = check_launch("gdx_aggregate_balanced")) return rc;
+        uint64_t blocks = (static_cast<uint64_t>(nh) + 7) / 8;
+        heavy_combine<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, b->heavy_rows, nh, b->chunk_off, b->partial,
+                                                                    b->ld_partial);
+        note_launch();
+        return check_launch("gdx_aggregate_balanced");
+    }
+    return GDX_OK;
 }

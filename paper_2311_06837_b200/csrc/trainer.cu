@@ -139,6 +139,7 @@ struct gdx_trainer {
     cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
     uint64_t issued = 0, consumed = 0;
     double* loss_host = nullptr;  // pinned
+    gdx_row_bins* bins = nullptr;  // degree bins (skewed graphs), else null
     // kernel profiling (eager epochs)
     bool profile = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -268,7 +269,8 @@ int aggregate(gdx_trainer* t, const Mat& src, uint32_t width, uint32_t rows, con
         TR_CUDA(cudaEventCreate(&e1));
         TR_CUDA(cudaEventRecord(e0, t->stream));
     }
-    TR_OK(gdx_aggregate_variant(&a, agg_variant(width, t->nnz, t->nloc), reinterpret_cast<gdx_stream>(t->stream)));
+    TR_OK(gdx_aggregate_balanced(&a, agg_variant(width, t->nnz, t->nloc), t->bins,
+                                 reinterpret_cast<gdx_stream>(t->stream)));
     if (t->profile) {
         TR_CUDA(cudaEventRecord(e1, t->stream));
         t->prof_events.push_back({e0, e1});
@@ -711,6 +713,7 @@ int run_epoch(gdx_trainer* t) {
 
 gdx_trainer::~gdx_trainer() {
     if (stream) cudaStreamSynchronize(stream);
+    if (bins) gdx_row_bins_free(bins);
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     for (auto& e : prof_events) {
@@ -816,6 +819,21 @@ extern "C" int gdx_trainer_create(const gdx_trainer_config* cfg, const gdx_train
         if (int rc = dalloc(t.get(), &t->col, std::max<uint64_t>(t->nnz, 1))) return rc;
         GDX_CUDA(cudaMemcpy(t->row_ptr, lro.data(), (t->nloc + 1) * 8, cudaMemcpyHostToDevice));
         if (t->nnz) GDX_CUDA(cudaMemcpy(t->col, gr->cols + ro[0], t->nnz * 4, cudaMemcpyHostToDevice));
+    }
+    // degree bins for skewed graphs: hub rows are chunked across warps
+    {
+        uint64_t maxd = 0;
+        for (uint64_t i = 0; i < t->nloc; ++i) maxd = std::max<uint64_t>(maxd, lro[i + 1] - lro[i]);
+        const double mean = t->nloc ? static_cast<double>(t->nnz) / static_cast<double>(t->nloc) : 0.0;
+        const uint64_t thr = cfg->heavy_degree ? cfg->heavy_degree
+                                               : std::max<uint64_t>(4096, static_cast<uint64_t>(32.0 * mean));
+        if (cfg->heavy_degree != 0xFFFFFFFFu && maxd > thr) {
+            uint32_t wmax = 8;
+            for (uint32_t l = 1; l <= t->L; ++l) wmax = std::max<uint32_t>(wmax, static_cast<uint32_t>(pad8(t->dims[l])));
+            if (int rc = gdx_row_bins_build(lro.data(), static_cast<uint32_t>(t->nloc), static_cast<uint32_t>(thr), 1024,
+                                            (wmax + 31) / 32 * 32, &t->bins))
+                return rc;
+        }
     }
     // degree scales, fp64 then rounded (train.py: 1/deg, (deg+1)^-1/2)
     std::vector<float> inv(std::max<uint64_t>(t->nloc, 1), 0.f), gs(std::max<uint64_t>(t->nloc, 1), 0.f);
@@ -1053,7 +1071,7 @@ extern "C" int gdx_trainer_info(const gdx_trainer* t, uint64_t* out, uint32_t co
     GDX_REQUIRE(t && out, GDX_INPUT, "gdx_trainer_info: null pointer");
     const uint64_t v[] = {t->nloc, t->nnz, t->lo, t->nfull, t->loss_rows, static_cast<uint64_t>(t->loss_count),
                           t->exec ? 1ull : 0ull, (!t->layers.empty() && t->layers.back().agg_first) ? 1ull : 0ull,
-                          t->nnz_src};
+                          t->nnz_src, t->bins ? t->bins->n_heavy : 0ull};
     for (uint32_t i = 0; i < count && i < sizeof(v) / sizeof(v[0]); ++i) out[i] = v[i];
     return GDX_OK;
 }

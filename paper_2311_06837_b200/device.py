@@ -102,7 +102,8 @@ def dense(rows: int, cols: int, device, zero: bool = True) -> torch.Tensor:
 
 def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_split: Split | None = None,
               self_coef: float = 0.0, self_base: int = 0, post_scale=None, add=None, relu=False,
-              row_end=None, row_begin=None, skip=None, partial=None, stream=None, variant: int = 0):
+              row_end=None, row_begin=None, skip=None, partial=None, stream=None, variant: int = 0,
+              bins: "RowBins | None" = None):
     """K1/K3 (see include/gdx.h gdx_aggregate).  row_begin/row_end override the CSR
     row bounds; skip = (seg_lo, seg_hi) excludes a per-row sub-range; partial adds
     precomputed partial sums before the epilogue."""
@@ -129,10 +130,33 @@ def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_spli
     a.ld_out = out.stride(0) if out is not None else 0
     if out_split is not None:
         a.out_hi, a.out_lo, a.ld_split = out_split.hi.data_ptr(), out_split.lo.data_ptr(), out_split.ld
-    if variant:
+    if bins is not None:
+        call("gdx_aggregate_balanced", _lib.C.byref(a), variant, bins._p, stream_handle(stream))
+    elif variant:
         call("gdx_aggregate_variant", _lib.C.byref(a), variant, stream_handle(stream))
     else:
         call("gdx_aggregate", _lib.C.byref(a), stream_handle(stream))
+
+
+class RowBins:
+    """Degree bins of a CSR (gdx_row_bins_build): rows above heavy_degree are split into
+    chunk_edges-edge chunks; pass as aggregate(..., bins=) for skewed graphs."""
+
+    def __init__(self, row_ptr_host: np.ndarray, heavy_degree: int, chunk_edges: int = 1024,
+                 max_width: int = 256):
+        rp = np.ascontiguousarray(row_ptr_host, np.uint64)
+        self._p = _lib.C.POINTER(_lib.RowBins)()
+        call("gdx_row_bins_build", rp.ctypes.data, len(rp) - 1, heavy_degree, chunk_edges, max_width,
+             _lib.C.byref(self._p))
+        b = self._p.contents
+        self.n_light, self.n_heavy, self.n_chunks = b.n_light, b.n_heavy, b.n_chunks
+
+    def __del__(self):
+        try:
+            if self._p:
+                _lib.lib().gdx_row_bins_free(self._p)
+        except Exception:
+            pass
 
 
 def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None, relu=False,

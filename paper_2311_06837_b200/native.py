@@ -27,7 +27,8 @@ class TrainerConfig(C.Structure):
     _fields_ = [("kind", C.c_int), ("layers", C.c_uint32), ("dims", C.POINTER(C.c_uint32)),
                 ("lr", C.c_float), ("rank", C.c_uint32), ("world", C.c_uint32), ("device", C.c_int),
                 ("feature_seed", C.c_uint64), ("label_seed", C.c_uint64), ("use_graph", C.c_int),
-                ("no_agg_first", C.c_int), ("push_ctas", C.c_uint32), ("peer_timeout_s", C.c_double)]
+                ("no_agg_first", C.c_int), ("push_ctas", C.c_uint32), ("peer_timeout_s", C.c_double),
+                ("heavy_degree", C.c_uint32)]
 
 
 class TrainerGraph(C.Structure):
@@ -86,7 +87,7 @@ class NativeTrainer:
     def __init__(self, g: Graph, cfg, *, rank: int = 0, world: int = 1, device: int | None = None,
                  weights=None, weight_seed: int = 3, subgraph=None, pg=None, use_graph: bool = True,
                  feature_seed: int = FEATURE_SEED, label_seed: int = LABEL_SEED, push_ctas: int = 0,
-                 no_agg_first: bool = False):
+                 no_agg_first: bool = False, heavy_degree: int = 0):
         import torch
         L = _bind()
         if cfg.kind not in KIND:
@@ -96,7 +97,8 @@ class NativeTrainer:
         self.dims = list(cfg.dims)
         self._dims_c = (C.c_uint32 * len(self.dims))(*self.dims)
         c = TrainerConfig(KIND[cfg.kind], len(self.dims) - 1, self._dims_c, cfg.lr, rank, world, self.device,
-                          feature_seed, label_seed, int(use_graph), int(no_agg_first), push_ctas, 0.0)
+                          feature_seed, label_seed, int(use_graph), int(no_agg_first), push_ctas, 0.0,
+                          heavy_degree)
         gr = TrainerGraph()
         gr.num_vertices = g.num_vertices()
         self.subgraph_mode = subgraph is not None
@@ -158,8 +160,8 @@ class NativeTrainer:
         dist.barrier(group=self.pg)
 
     def info(self) -> list:
-        out = np.zeros(9, np.uint64)
-        call("gdx_trainer_info", self._h, out.ctypes.data, 9)
+        out = np.zeros(10, np.uint64)
+        call("gdx_trainer_info", self._h, out.ctypes.data, 10)
         return [int(x) for x in out]
 
     @property
