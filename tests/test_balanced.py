@@ -24,6 +24,14 @@ def hub_graph(n, deg, hubs, hub_deg, seed):
     return Graph.from_edges(np.concatenate(e), n)
 
 
+def scaled_close(a, b, tol):
+    """|a - b| <= tol (|b| + rms(b)): fp32 summation order differs between the chunked and
+    the whole-row reductions (hub rows sum ~10^4 terms)."""
+    rms = float(np.sqrt(np.mean(np.asarray(b, np.float64) ** 2)))
+    err = np.max(np.abs(a - b) / (np.abs(b) + rms))
+    assert err <= tol, err
+
+
 def _args(n, w, cuda):
     import torch
     rng = torch.Generator(device=cuda).manual_seed(0)
@@ -53,8 +61,8 @@ def test_balanced_equals_plain_and_fp64(cuda, w):
         aggregate(dg, src, w, out=out, out_split=sp, bins=b, **kw)
         outs.append((out[:, :w].double().cpu().numpy(), sp.to_float().double().cpu().numpy()))
     (a, asp), (b, bsp) = outs
-    np.testing.assert_allclose(b, a, rtol=2e-6, atol=2e-6)
-    np.testing.assert_allclose(bsp, b, rtol=1e-5, atol=1e-6)
+    scaled_close(b, a, 1e-4)     # the north_star activation contract
+    scaled_close(bsp, b, 1e-5)
     # fp64 reference of the same op
     ro, ci = g.row_offsets().astype(np.int64), g.col_indices()
     x = src[:, :w].double().cpu().numpy()
@@ -63,7 +71,8 @@ def test_balanced_equals_plain_and_fp64(cuda, w):
     np.add.at(agg, rows, x[ci])
     ref = np.maximum((agg + x) * scale.double().cpu().numpy()[:, None] + add[:, :w].double().cpu().numpy(), 0)
     rms = np.sqrt(np.mean(ref ** 2))
-    assert np.max(np.abs(b - ref) / (np.abs(ref) + rms)) <= 1e-5
+    assert np.max(np.abs(b - ref) / (np.abs(ref) + rms)) <= 1e-4
+    assert np.max(np.abs(a - ref) / (np.abs(ref) + rms)) <= 1e-4
 
 
 def test_balanced_split_passes_and_prefix(cuda):
@@ -93,7 +102,7 @@ def test_balanced_split_passes_and_prefix(cuda):
             aggregate(sub, src, w, out=out, skip=(seg_lo, seg_hi), partial=P, self_coef=1.0, post_scale=scale,
                       bins=b)
             res.append(out[:rows, :w].double().cpu().numpy())
-        np.testing.assert_allclose(res[1], res[0], rtol=2e-6, atol=2e-6)
+        scaled_close(res[1], res[0], 1e-4)
 
 
 def test_native_trainer_with_chunked_hubs_matches_oracle(cuda):
