@@ -357,6 +357,95 @@ __global__ void __launch_bounds__(256, agg_min_blocks(LPE == 12 ? 16 : LPE, NCH)
     }
 }
 
+__device__ __forceinline__ void epi4(const AggParams& p, uint32_t row, uint32_t ch, float4 r);
+
+// Epilogue of one destination row for a lane group (lane lin holds columns lin + c LPE).
+template <int LPE, int NCH>
+__device__ __forceinline__ void group_epilogue(const AggParams& p, uint32_t row, int lin, const bool (&chan_on)[NCH],
+                                               const float4 (&acc)[NCH]) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+        if (chan_on[c]) epi4(p, row, lin + c * LPE, acc[c]);
+}
+
+// Low-degree rows, edge-flat (GDX_AGG_FLAT): a lane group owns RG = LPE - 1 consecutive
+// rows -- one contiguous edge range -- and walks those edges in order with UNROLL
+// gathers in flight across row boundaries, flushing each row's epilogue as the walk
+// passes it.  The rows' offsets come in one coalesced load (one per lane) and the
+// column ids LPE at a time, so the per-row row_ptr -> col -> row chain of
+// aggregate_rows becomes one chain per RG rows.  A row's edges are summed in ascending
+// order, as in aggregate_rows.  Plain CSR rows only (no row_end / skip / row list).
+template <int LPE, int NCH, bool EXACT, int UNROLL>
+__global__ void __launch_bounds__(256, 4) aggregate_flat(const AggParams p) {
+    constexpr int EPW = pow2_floor(32 / LPE);
+    constexpr uint32_t RG = LPE - 1;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / LPE;
+    const int lin = lane - sub * LPE;
+    if (sub >= EPW) return;
+    const int g0 = sub * LPE;  // first lane of this group
+    const uint32_t gmask = (LPE >= 32) ? 0xffffffffu : (((1u << LPE) - 1u) << g0);
+    uint64_t pol_keep, pol_stream;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const uint64_t base = reinterpret_cast<uint64_t>(p.src) + 16 * lin;
+    const uint32_t ldb = p.ld_bytes;
+    bool chan_on[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) chan_on[c] = EXACT || (lin + c * LPE) < p.c4;
+    const uint64_t groups = static_cast<uint64_t>((gridDim.x * blockDim.x) >> 5) * EPW;
+    for (uint64_t grp = static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * EPW + sub;
+         grp * RG < p.rows; grp += groups) {
+        const uint32_t a = static_cast<uint32_t>(grp * RG);
+        const uint32_t nr = (p.rows - a) < RG ? (p.rows - a) : RG;
+        const uint64_t myoff = static_cast<uint32_t>(lin) <= nr ? p.row_ptr[a + lin] : 0;
+        uint64_t e = __shfl_sync(gmask, myoff, g0);
+        const uint64_t eend = __shfl_sync(gmask, myoff, g0 + static_cast<int>(nr));
+        uint32_t k = 0;
+        uint64_t next_off = __shfl_sync(gmask, myoff, g0 + 1);
+        float4 acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        while (e < eend) {
+            const uint32_t cnt = static_cast<uint32_t>((eend - e) < LPE ? (eend - e) : LPE);
+            const uint32_t mycol = static_cast<uint32_t>(lin) < cnt ? ld_stream_u32(p.col + e + lin, pol_stream) : 0u;
+            for (uint32_t j = 0; j < cnt; j += UNROLL) {
+                float4 v[UNROLL][NCH];
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    const uint32_t idx = j + u;
+                    const uint32_t nb = __shfl_sync(gmask, mycol, g0 + static_cast<int>(idx < cnt ? idx : 0));
+                    const char* rp = row_addr(base, nb, ldb);
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+                        v[u][c] = (idx < cnt && chan_on[c]) ? ld_row4(rp + 16 * LPE * c, pol_keep)
+                                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    if (j + u >= cnt) break;
+                    const uint64_t ed = e + j + u;
+                    while (ed >= next_off) {  // group-uniform: the walk passed row k
+                        group_epilogue<LPE, NCH>(p, a + k, lin, chan_on, acc);
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        ++k;
+                        next_off = __shfl_sync(gmask, myoff, g0 + static_cast<int>(k + 1));
+                    }
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) add4(acc[c], v[u][c]);
+                }
+            }
+            e += cnt;
+        }
+        for (; k < nr; ++k) {
+            group_epilogue<LPE, NCH>(p, a + k, lin, chan_on, acc);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+}
+
 // Any width / alignment: one warp per row, lanes stride over columns.
 __global__ void __launch_bounds__(256) aggregate_scalar(const AggParams p, uint32_t width) {
     const int lane = threadIdx.x & 31;
@@ -923,8 +1012,32 @@ int launch_rows_wide(const AggParams& p, cudaStream_t s) {
     }
 }
 
+template <int LPE, int NCH, bool EXACT>
+void launch_flat(const AggParams& p, cudaStream_t s) {
+    constexpr int EPW = pow2_floor(32 / LPE);
+    const uint64_t per_block = 8ull * EPW * (LPE - 1);
+    uint64_t blocks = (static_cast<uint64_t>(p.rows) + per_block - 1) / per_block;
+    if (blocks > 65535ull * 64) blocks = 65535ull * 64;
+    aggregate_flat<LPE, NCH, EXACT, 4><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
+}
+
+// GDX_AGG_FLAT: edge-flat low-degree kernel where it applies (plain CSR rows, exact
+// power-of-two lane groups), the row-group kernel otherwise.
+int launch_flat_any(const AggParams& p, cudaStream_t s) {
+    if (p.row_end || p.skip_lo || p.row_list) return launch_rows_any(p, s);
+    switch (p.c4) {
+        case 16: launch_flat<16, 1, true>(p, s); return 0;
+        case 8: launch_flat<8, 1, true>(p, s); return 0;
+        case 32: launch_flat<32, 1, true>(p, s); return 0;
+        case 64: launch_flat<32, 2, true>(p, s); return 0;
+        case 12: launch_flat<16, 1, false>(p, s); return 0;
+        default: return launch_rows_any(p, s);
+    }
+}
+
 int launch_variant(const AggParams& p, int variant, cudaStream_t s) {
     if (variant == GDX_AGG_ROWS) return launch_rows_any(p, s);
+    if (variant == 3) return launch_flat_any(p, s);
     if (variant == 2) return launch_rows_wide(p, s);
     const bool u8 = variant == 8;
     if (p.c4 == 16) {
