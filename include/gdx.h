@@ -151,6 +151,12 @@ int gdx_row_split(const uint64_t* row_ptr, const uint32_t* col, uint32_t rows, u
  * bound by the per-row row_ptr -> col -> row latency chain.  4 / 8: unroll depth
  * of the warp-per-row kernel (tuning).  0 = gdx_aggregate. */
 #define GDX_AGG_ROWS 1
+/* GDX_AGG_ROWS2: lane groups of half the row (two 16-byte chunks per lane), twice the rows
+ * per warp (degree ~8-20).  GDX_AGG_FLAT: a lane group walks the edges of LPE-1
+ * consecutive rows in order with gathers in flight across row boundaries (degree < 6);
+ * plain CSR rows only (falls back to GDX_AGG_ROWS with row_end / skip / row lists). */
+#define GDX_AGG_ROWS2 2
+#define GDX_AGG_FLAT 3
 int gdx_aggregate_variant(const gdx_aggregate_args* a, int variant, gdx_stream stream);
 
 /* ------------------------------------------------------------------------

@@ -1012,13 +1012,13 @@ int launch_rows_wide(const AggParams& p, cudaStream_t s) {
     }
 }
 
-template <int LPE, int NCH, bool EXACT>
+template <int LPE, int NCH, bool EXACT, int UNROLL = 4>
 void launch_flat(const AggParams& p, cudaStream_t s) {
     constexpr int EPW = pow2_floor(32 / LPE);
     const uint64_t per_block = 8ull * EPW * (LPE - 1);
     uint64_t blocks = (static_cast<uint64_t>(p.rows) + per_block - 1) / per_block;
     if (blocks > 65535ull * 64) blocks = 65535ull * 64;
-    aggregate_flat<LPE, NCH, EXACT, 4><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
+    aggregate_flat<LPE, NCH, EXACT, UNROLL><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
 }
 
 // GDX_AGG_FLAT: edge-flat low-degree kernel where it applies (plain CSR rows, exact
@@ -1038,6 +1038,14 @@ int launch_flat_any(const AggParams& p, cudaStream_t s) {
 int launch_variant(const AggParams& p, int variant, cudaStream_t s) {
     if (variant == GDX_AGG_ROWS) return launch_rows_any(p, s);
     if (variant == 3) return launch_flat_any(p, s);
+    if (variant == 5 && !p.row_end && !p.skip_lo && !p.row_list && p.c4 == 16) {  // tuning: 8 gathers in flight
+        launch_flat<16, 1, true, 8>(p, s);
+        return 0;
+    }
+    if (variant == 6 && !p.row_end && !p.skip_lo && !p.row_list && p.c4 == 16) {  // tuning: 8-lane groups x 2 chunks
+        launch_flat<8, 2, true, 4>(p, s);
+        return 0;
+    }
     if (variant == 2) return launch_rows_wide(p, s);
     const bool u8 = variant == 8;
     if (p.c4 == 16) {

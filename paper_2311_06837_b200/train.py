@@ -134,12 +134,20 @@ def source_bounds(row_ptr: torch.Tensor, col: torch.Tensor, rows: int, block: in
     return b
 
 
+AGG_ROWS2 = 2   # half-width lane groups, two chunks per lane (degree ~8-20)
+AGG_FLAT = 3    # edge-flat walk over row groups (degree < 6)
+
+
 def agg_variant(width: int, nnz: int, rows: int) -> int:
-    """Aggregation kernel for a CSR: the lane-group-per-row kernel for low-degree rows
-    (measured B200, 6 M rows x 64: 1.8x at degree 2.6, 1.2x at 12, parity at 25) and
-    for 48-wide rows (12 lanes: 5% faster at degree 492); warp-per-row otherwise."""
-    if rows and nnz / rows < 20:
-        return AGG_ROWS
+    """Aggregation kernel for a CSR (measured B200, 6 M rows x 64, tools/agg_bench.py):
+    degree 2.6 -> edge-flat 1.61 ms (row groups 1.68, warp per row 2.89); degree 12 ->
+    half-width row groups 3.60 ms (row groups 3.96); 48-wide rows -> row groups (5%
+    faster at degree 492); warp per row otherwise."""
+    deg = nnz / rows if rows else 0.0
+    if rows and deg < 6:
+        return AGG_FLAT
+    if rows and deg < 20:
+        return AGG_ROWS2
     return AGG_ROWS if pad4(width) == 48 else 0
 
 
