@@ -47,6 +47,14 @@ uint64_t gdx_host_gen_random_graph_count(uint32_t n, double avg_degree, uint64_t
                                          uint64_t* row_offsets);
 int gdx_host_gen_random_graph_fill(uint32_t n, double avg_degree, uint64_t seed,
                                    const uint64_t* row_offsets, uint32_t* cols);
+/* SampleTrace of extract_sampled (extract.hpp:49-64): per step (frontier vertex, hop,
+ * taken[step_off[i] .. step_off[i+1])) in the reference's sequential attribution order.
+ * Call with null outputs to get nsteps / ntaken, then with capacities (step_off has
+ * cap_steps + 1 entries).  Host diagnostics (the taken sets equal the device growth's). */
+int gdx_host_sample_trace(uint32_t n, const uint64_t* row_offsets, const uint32_t* cols, const uint8_t* inner,
+                          uint32_t max_hop, uint32_t fanout, uint64_t seed, uint64_t cap_steps, uint64_t cap_taken,
+                          uint64_t* nsteps, uint64_t* ntaken, uint32_t* step_vertex, uint32_t* step_hop,
+                          uint64_t* step_off, uint32_t* taken);
 /* partition_random (partition.cpp:51-61). */
 int gdx_host_partition_random(uint32_t n, uint32_t parts, uint64_t seed, uint32_t* assignment);
 /* partition_mincut (partition.cpp:63-170) over a host CSR (bit-identical assignment). */

@@ -57,6 +57,8 @@ _SIGS = {
     "gdx_host_gen_random_graph_count": (u64, [u32, C.c_double, u64, vp]),
     "gdx_host_gen_random_graph_fill": (C.c_int, [u32, C.c_double, u64, vp, vp]),
     "gdx_host_partition_random": (C.c_int, [u32, u32, u64, vp]),
+    "gdx_host_sample_trace": (C.c_int, [u32, vp, vp, vp, u32, u32, u64, u64, u64, C.POINTER(u64), C.POINTER(u64),
+                                        vp, vp, vp, vp]),
     "gdx_host_partition_mincut": (C.c_int, [u32, vp, vp, u32, u64, C.c_double, vp]),
     "gdx_init_uniform": (C.c_int, [u64, u64, u64, u64, u32, u32, C.c_double, C.c_double, vp, u64, vp]),
     "gdx_init_uniform_f64": (C.c_int, [u64, u64, u64, u64, u32, u32, C.c_double, C.c_double, vp, u64, vp]),

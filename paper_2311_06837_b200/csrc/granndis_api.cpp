@@ -255,40 +255,18 @@ DependencySubgraph grow(const Graph& g, const Partition& p, std::uint32_t server
 // for (diagnostics; extract.hpp:49-54).
 void build_trace(const Graph& g, const std::vector<uint8_t>& inner, const DependencySubgraph& sub,
                  const SamplingConfig& cfg, SampleTrace* trace) {
-    std::vector<uint32_t> hop(g.num_vertices(), GDX_UNSEEN);
-    for (VertexId v : sub.inner_vertices) hop[v] = 0;
-    for (size_t i = 0; i < sub.halo_vertices.size(); ++i) hop[sub.halo_vertices[i]] = sub.halo_hops[i];
-    std::vector<uint8_t> included(inner.begin(), inner.end());
-    std::vector<VertexId> frontier;
-    for (VertexId v : sub.inner_vertices)
-        for (VertexId u : g.neighbors(v))
-            if (!inner[u]) {
-                frontier.push_back(v);
-                break;
-            }
-    for (std::uint32_t h = 1; h <= cfg.max_hop && !frontier.empty(); ++h) {
-        std::vector<VertexId> added;
-        for (VertexId v : frontier) {
-            std::vector<VertexId> c;
-            for (VertexId u : g.neighbors(v))
-                if (!inner[u]) c.push_back(u);
-            if (!(cfg.unlimited() || c.size() <= cfg.fanout)) {
-                KeyedRng rng(cfg.seed, v, 0x73616d70ULL);
-                keyed_shuffle(c, rng);
-                c.resize(cfg.fanout);
-            }
-            SampleTraceStep step{v, h, {}};
-            for (VertexId u : c) {
-                if (included[u]) continue;
-                included[u] = 1;
-                step.taken.push_back(u);
-                added.push_back(u);
-            }
-            trace->push_back(std::move(step));
-        }
-        std::sort(added.begin(), added.end());
-        frontier = std::move(added);
-    }
+    (void)sub;
+    const uint32_t n = g.num_vertices();
+    const uint32_t* cols = g.col_indices().empty() ? nullptr : g.col_indices().data();
+    uint64_t ns = 0, nt = 0;
+    check(gdx_host_sample_trace(n, g.row_offsets().data(), cols, inner.data(), cfg.max_hop, cfg.fanout, cfg.seed,
+                                0, 0, &ns, &nt, nullptr, nullptr, nullptr, nullptr));
+    std::vector<uint32_t> sv(std::max<uint64_t>(ns, 1)), sh(std::max<uint64_t>(ns, 1)), tk(std::max<uint64_t>(nt, 1));
+    std::vector<uint64_t> so(ns + 1);
+    check(gdx_host_sample_trace(n, g.row_offsets().data(), cols, inner.data(), cfg.max_hop, cfg.fanout, cfg.seed,
+                                ns, nt, &ns, &nt, sv.data(), sh.data(), so.data(), tk.data()));
+    for (uint64_t i = 0; i < ns; ++i)
+        trace->push_back({sv[i], sh[i], std::vector<VertexId>(tk.begin() + so[i], tk.begin() + so[i + 1])});
 }
 
 // G(n,p) scan of graph.cpp:86-111 for the planted generator (host preprocessing)

@@ -183,6 +183,64 @@ extern "C" int gdx_host_gen_random_graph_fill(uint32_t n, double d, uint64_t see
     return GDX_OK;
 }
 
+// SampleTrace of extract_sampled (extract.hpp:49-64; the attribution order of
+// extract.cpp:158-178): frontier vertices hop by hop in ascending order, each taking the
+// not-yet-included vertices of its sampled prefix.  Host diagnostics: the set of taken
+// vertices is what the device growth computes; this replays the sequential order only
+// to attribute each one to its first exposing frontier vertex.
+extern "C" int gdx_host_sample_trace(uint32_t n, const uint64_t* ro, const uint32_t* cols, const uint8_t* inner,
+                                     uint32_t max_hop, uint32_t fanout, uint64_t seed, uint64_t cap_steps,
+                                     uint64_t cap_taken, uint64_t* nsteps, uint64_t* ntaken, uint32_t* step_vertex,
+                                     uint32_t* step_hop, uint64_t* step_off, uint32_t* taken) {
+    if (!ro || (!cols && n && ro[n]) || !inner || !nsteps || !ntaken)
+        return fail(GDX_INPUT, "gdx_host_sample_trace: null pointer");
+    std::vector<uint8_t> incl(inner, inner + n);
+    std::vector<uint32_t> frontier, added, cand;
+    for (uint32_t v = 0; v < n; ++v) {
+        if (!inner[v]) continue;
+        for (uint64_t e = ro[v]; e < ro[v + 1]; ++e)
+            if (!inner[cols[e]]) {
+                frontier.push_back(v);
+                break;
+            }
+    }
+    uint64_t ns = 0, nt = 0;
+    for (uint32_t hop = 1; hop <= max_hop && !frontier.empty(); ++hop) {
+        added.clear();
+        for (uint32_t v : frontier) {
+            cand.clear();
+            for (uint64_t e = ro[v]; e < ro[v + 1]; ++e)
+                if (!inner[cols[e]]) cand.push_back(cols[e]);
+            if (fanout != GDX_UNLIMITED_FANOUT && cand.size() > fanout) {
+                Stream r(seed, v, 0x73616d70ULL);   // keyed_shuffle (rng.hpp:55-61)
+                for (size_t i = cand.size(); i > 1; --i) std::swap(cand[i - 1], cand[r.below(i)]);
+                cand.resize(fanout);
+            }
+            if (step_vertex && ns < cap_steps) {
+                step_vertex[ns] = v;
+                step_hop[ns] = hop;
+                step_off[ns] = nt;
+            }
+            ++ns;
+            for (uint32_t u : cand) {
+                if (incl[u]) continue;
+                incl[u] = 1;
+                if (taken && nt < cap_taken) taken[nt] = u;
+                ++nt;
+                added.push_back(u);
+            }
+        }
+        std::sort(added.begin(), added.end());
+        frontier.swap(added);
+    }
+    if (step_off && ns <= cap_steps) step_off[ns < cap_steps ? ns : cap_steps] = nt;
+    *nsteps = ns;
+    *ntaken = nt;
+    if ((step_vertex && ns > cap_steps) || (taken && nt > cap_taken))
+        return fail(GDX_CAPACITY, "gdx_host_sample_trace: output capacity too small");
+    return GDX_OK;
+}
+
 // partition.cpp:51-61
 extern "C" int gdx_host_partition_random(uint32_t n, uint32_t parts, uint64_t seed,
                                          uint32_t* assignment) {

@@ -16,6 +16,8 @@
 // shuffled list.  Candidates are then selected by rank with warp ballots.
 #include <cub/device/device_scan.cuh>
 
+#include <vector>
+
 #include "gdx_common.cuh"
 
 namespace gdx {
@@ -62,11 +64,12 @@ __global__ void seed_frontier(const uint64_t* row_ptr, const uint32_t* col, uint
 // One hop of sampled growth.  frontier[i] exposes min(fanout, c) candidates.
 __global__ void __launch_bounds__(256) expand_hop(const uint64_t* row_ptr, const uint32_t* col,
                                                   const uint8_t* excluded, const uint8_t* allowed,
-                                                  const uint32_t* frontier, uint32_t nf,
+                                                  const uint32_t* frontier, const uint32_t* count_in,
                                                   uint32_t fanout, uint64_t seed, uint32_t hop,
                                                   uint32_t* mark, uint32_t* next,
                                                   uint32_t* next_count) {
     const int lane = threadIdx.x & 31;
+    const uint32_t nf = *count_in;  // frontier size from device memory: no host round trip per hop
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nf; i += nw) {
         const uint32_t v = frontier[i];
@@ -150,9 +153,10 @@ __global__ void peel_init(const uint32_t* targets, uint64_t nt, uint32_t* in_set
 }
 
 __global__ void peel_step(const uint64_t* row_ptr, const uint32_t* col, const uint8_t* in_batch,
-                          const uint32_t* frontier, uint32_t nf, uint32_t* in_set, uint32_t* next,
+                          const uint32_t* frontier, const uint32_t* count_in, uint32_t* in_set, uint32_t* next,
                           uint32_t* next_count) {
     const int lane = threadIdx.x & 31;
+    const uint32_t nf = *count_in;  // frontier size from device memory
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nf; i += nw) {
         const uint32_t v = frontier[i];
@@ -359,20 +363,31 @@ extern "C" int gdx_sampled_growth(const uint64_t* row_ptr, const uint32_t* col, 
                                                                           allowed, fa, cnt);
     note_launch();
     GDX_CUDA(cudaGetLastError());
-    uint32_t nf = 0;
-    GDX_CUDA(cudaMemcpyAsync(&nf, cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    GDX_CUDA(cudaStreamSynchronize(s));
-    for (uint32_t h = 1; h <= max_hop && nf > 0; ++h) {
-        GDX_CUDA(cudaMemsetAsync(cnt + 1, 0, sizeof(uint32_t), s));
-        expand_hop<<<grid_for(static_cast<uint64_t>(nf) * 32), 256, 0, s>>>(
-            row_ptr, col, excluded, allowed, fa, nf, fanout, seed, h, mark, fb, cnt + 1);
-        note_launch();
-        GDX_CUDA(cudaGetLastError());
-        GDX_CUDA(cudaMemcpyAsync(&nf, cnt + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    // Hops are enqueued in batches with no host round trip: each expand kernel reads its
+    // frontier size from device memory (cnt alternates in / out) over a fixed grid.  The
+    // host looks once per batch of kHopBatch hops whether the frontier emptied (a BFS to
+    // depth max_hop would otherwise enqueue max_hop launches).
+    constexpr uint32_t kHopBatch = 16;
+    const unsigned grid = static_cast<unsigned>(device_sms()) * 8;
+    for (uint32_t h = 1; h <= max_hop;) {
+        const uint32_t stop = (max_hop - h + 1 > kHopBatch) ? h + kHopBatch : max_hop + 1;
+        for (; h < stop; ++h) {
+            uint32_t* cin = cnt + ((h - 1) & 1);
+            uint32_t* cout = cnt + (h & 1);
+            GDX_CUDA(cudaMemsetAsync(cout, 0, sizeof(uint32_t), s));
+            expand_hop<<<grid, 256, 0, s>>>(row_ptr, col, excluded, allowed, fa, cin, fanout, seed, h, mark, fb,
+                                            cout);
+            note_launch();
+            GDX_CUDA(cudaGetLastError());
+            uint32_t* t = fa;
+            fa = fb;
+            fb = t;
+        }
+        if (h > max_hop) break;
+        uint32_t nf = 0;
+        GDX_CUDA(cudaMemcpyAsync(&nf, cnt + ((h - 1) & 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         GDX_CUDA(cudaStreamSynchronize(s));
-        uint32_t* t = fa;
-        fa = fb;
-        fb = t;
+        if (nf == 0) break;
     }
     return GDX_OK;
 }
@@ -412,24 +427,38 @@ extern "C" int gdx_peel_mfg(const uint64_t* row_ptr, const uint32_t* col, uint32
         note_launch();
         GDX_CUDA(cudaGetLastError());
     }
-    counts[layers] = nt;
-    uint64_t total = nt;
-    uint32_t nf = static_cast<uint32_t>(nt);
+    // every back-peel step enqueued with device-resident frontier sizes (no host round
+    // trip per step); each step's number of added vertices is copied aside and read back
+    // once at the end
+    uint32_t* adds = nullptr;
+    GDX_CUDA(cudaMallocAsync(&adds, sizeof(uint32_t) * (layers + 1), s));
+    GDX_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t), s));
+    if (nt) {
+        const uint32_t nt32 = static_cast<uint32_t>(nt);
+        GDX_CUDA(cudaMemcpyAsync(cnt, &nt32, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    }
+    const unsigned grid = static_cast<unsigned>(device_sms()) * 8;
     for (uint32_t back = 1; back <= layers; ++back) {
-        GDX_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), s));
-        if (nf) {
-            peel_step<<<grid_for(static_cast<uint64_t>(nf) * 32), 256, 0, s>>>(row_ptr, col, in_batch, fa,
-                                                                              nf, in_set, fb, cnt);
-            note_launch();
-            GDX_CUDA(cudaGetLastError());
-        }
-        GDX_CUDA(cudaMemcpyAsync(&nf, cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        GDX_CUDA(cudaStreamSynchronize(s));
-        total += nf;
-        counts[layers - back] = total;
+        uint32_t* cin = cnt + ((back - 1) & 1);
+        uint32_t* cout = cnt + (back & 1);
+        GDX_CUDA(cudaMemsetAsync(cout, 0, sizeof(uint32_t), s));
+        peel_step<<<grid, 256, 0, s>>>(row_ptr, col, in_batch, fa, cin, in_set, fb, cout);
+        note_launch();
+        GDX_CUDA(cudaGetLastError());
+        GDX_CUDA(cudaMemcpyAsync(adds + back, cout, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         uint32_t* t = fa;
         fa = fb;
         fb = t;
+    }
+    std::vector<uint32_t> h(layers + 1, 0);
+    if (layers) GDX_CUDA(cudaMemcpyAsync(h.data() + 1, adds + 1, sizeof(uint32_t) * layers, cudaMemcpyDeviceToHost, s));
+    GDX_CUDA(cudaFreeAsync(adds, s));
+    GDX_CUDA(cudaStreamSynchronize(s));
+    counts[layers] = nt;
+    uint64_t total = nt;
+    for (uint32_t back = 1; back <= layers; ++back) {
+        total += h[back];
+        counts[layers - back] = total;
     }
     return GDX_OK;
 }

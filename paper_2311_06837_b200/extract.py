@@ -142,18 +142,48 @@ def extract_full(g: Graph, server_partition: Partition, server_id: int, layers: 
     return _finish(g, server_id, mark, layers, False)
 
 
+@dataclass
+class SampleTraceStep:
+    """extract.hpp:49-53."""
+    frontier_vertex: int
+    hop: int
+    taken: list
+
+
+def sample_trace(g: Graph, inner_mask: np.ndarray, cfg: SamplingConfig) -> list:
+    """The reference's SampleTrace (which frontier vertex took which halo vertex, in the
+    sequential order of extract.cpp:158-178), from the host attribution replay
+    (gdx_host_sample_trace)."""
+    ro, ci = g.row_offsets(), g.col_indices()
+    im = np.ascontiguousarray(inner_mask, np.uint8)
+    ns, nt = _lib.u64(0), _lib.u64(0)
+    args = (g.num_vertices(), ro.ctypes.data, ci.ctypes.data if len(ci) else None, im.ctypes.data, cfg.max_hop,
+            cfg.fanout & 0xFFFFFFFF, cfg.seed)
+    call("gdx_host_sample_trace", *args, 0, 0, _lib.C.byref(ns), _lib.C.byref(nt), None, None, None, None)
+    S, T = int(ns.value), int(nt.value)
+    sv = np.zeros(max(S, 1), np.uint32)
+    sh = np.zeros(max(S, 1), np.uint32)
+    so = np.zeros(S + 1, np.uint64)
+    tk = np.zeros(max(T, 1), np.uint32)
+    call("gdx_host_sample_trace", *args, S, T, _lib.C.byref(ns), _lib.C.byref(nt), sv.ctypes.data, sh.ctypes.data,
+         so.ctypes.data, tk.ctypes.data)
+    return [SampleTraceStep(int(sv[i]), int(sh[i]), [int(x) for x in tk[int(so[i]):int(so[i + 1])]])
+            for i in range(S)]
+
+
 def extract_sampled(g: Graph, server_partition: Partition, server_id: int, cfg: SamplingConfig,
                     trace=None) -> DependencySubgraph:
-    """Expansion-aware sampling (extract.cpp:135-182), bit-exact on device.
-    ``trace`` (SampleTrace attribution) is order-dependent in the reference and is
-    not produced by the parallel engine; passing one raises InputError."""
-    if trace is not None:
-        raise InputError("extract_sampled: SampleTrace is not supported by the device engine")
+    """Expansion-aware sampling (extract.cpp:135-182), bit-exact on device.  ``trace``: a
+    list that receives the SampleTrace steps (extract.hpp:49-64) -- the order-dependent
+    attribution, replayed on the host."""
     require_cuda()
     _check_server(g, server_partition, server_id)
     inner = _inner_mask(g, server_partition, server_id)
     mark = sampled_growth_device(g, inner, None, cfg.max_hop, cfg.fanout, cfg.seed)
-    return _finish(g, server_id, mark, cfg.max_hop, not cfg.unlimited())
+    sub = _finish(g, server_id, mark, cfg.max_hop, not cfg.unlimited())
+    if trace is not None:
+        trace.extend(sample_trace(g, inner.cpu().numpy(), cfg))
+    return sub
 
 
 def neighbor_explosion_profile(g: Graph, server_partition: Partition, server_id: int,

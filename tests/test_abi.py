@@ -161,3 +161,28 @@ def test_every_push_path_takes_seven_peers():
         assert ("world must be 1..8" in msg) != ok, (world, rc, msg)
         if rc == 0:
             L.gdx_trainer_destroy(h)
+
+
+@pytest.mark.parametrize("m,k,seed", [(1, 3, 5), (2, 4, 9), (3, 2, 1), (2, 0xFFFFFFFF, 0)])
+def test_host_sample_trace_attribution(m, k, seed):
+    """gdx_host_sample_trace (extract.hpp:49-64): the taken vertices are exactly the halo
+    of extract_sampled (oracle, bit-exact to the reference), each once, at its hop, and a
+    step's vertex is in the frontier of its hop."""
+    import oracle as O
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.extract import sample_trace
+
+    n = 400
+    g = G.gen_random_graph(n, 8.0, 13)
+    p = G.partition_random(g, 3, 2)
+    inner = (p.assignment == 1).astype(np.uint8)
+    cfg = G.SamplingConfig(m, k, seed)
+    tr = sample_trace(g, inner, cfg)
+    c = O.CSR(n, g.row_offsets(), g.col_indices())
+    hop, _ = O.extract_sampled(c, p.assignment, 1, m, k, seed)
+    taken = [(u, s.hop) for s in tr for u in s.taken]
+    assert len({u for u, _ in taken}) == len(taken)
+    halo = {int(v): int(hop[v]) for v in range(n) if hop[v] not in (0, 0xFFFFFFFF)}
+    assert dict(taken) == halo
+    for s in tr:
+        assert (s.hop == 1 and inner[s.frontier_vertex]) or hop[s.frontier_vertex] == s.hop - 1
