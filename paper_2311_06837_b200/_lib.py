@@ -12,7 +12,8 @@ import threading
 from .errors import raise_for_status, InternalError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgdx.so")
+# GDX_LIB_PATH: load another build of the library (A/B measurements of a kernel change)
+LIB_PATH = os.environ.get("GDX_LIB_PATH") or os.path.join(_HERE, "libgdx.so")
 
 u8p = C.POINTER(C.c_uint8)
 vp = C.c_void_p
