@@ -24,6 +24,7 @@
 // epilogue of tile i overlaps the TMA + MMA of tile i+1.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "gdx_common.cuh"
@@ -608,7 +609,13 @@ int launch_majors_ew(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
 template <int BN, int STAGES>
 int launch_majors(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     // the fused ReLU-backward epilogue (mask loads) runs with 16 epilogue warps
-    if (g->mask && !g->a_mn_major && g->b_mn_major) return launch_tc<BN, STAGES, false, true, 16>(g, ep, s);
+    // (GDX_MASK_EW=8: 8 warps with the store-transpose staging, a tuning knob)
+    static const bool mask_ew8 = [] {
+        const char* e = std::getenv("GDX_MASK_EW");
+        return e && std::atoi(e) == 8;
+    }();
+    if (g->mask && !g->a_mn_major && g->b_mn_major && !mask_ew8)
+        return launch_tc<BN, STAGES, false, true, 16>(g, ep, s);
     return launch_majors_ew<BN, STAGES, 8>(g, ep, s);
 }
 

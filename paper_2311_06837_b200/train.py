@@ -144,6 +144,9 @@ def agg_variant(width: int, nnz: int, rows: int) -> int:
     half-width row groups 3.60 ms (row groups 3.96); 48-wide rows -> row groups (5%
     faster at degree 492); warp per row otherwise."""
     deg = nnz / rows if rows else 0.0
+    forced = os.environ.get("GDX_AGG_LOWDEG")   # tuning: force the low-degree kernel (1, 2, 3)
+    if forced and rows and deg < 20:
+        return int(forced)
     if rows and deg < 6:
         return AGG_FLAT
     if rows and deg < 20:

@@ -52,6 +52,15 @@ def main():
         for _ in range(args.epochs):
             tr.train_epoch(sync_loss=False)
         torch.cuda.synchronize()
+        if os.environ.get("TIME_EPOCHS"):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                tr.train_epoch(sync_loss=False)
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"cobatch ms per batch step: {e0.elapsed_time(e1) / 5 / len(plan.batches):.3f} "
+                  f"(GDX_AGG_LOWDEG={os.environ.get('GDX_AGG_LOWDEG', 'auto')})")
     else:
         raise SystemExit(f"unknown target {args.what}")
 
