@@ -608,13 +608,16 @@ int launch_majors_ew(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
 
 template <int BN, int STAGES>
 int launch_majors(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
-    // the fused ReLU-backward epilogue (mask loads) runs with 16 epilogue warps
-    // (GDX_MASK_EW=8: 8 warps with the store-transpose staging, a tuning knob)
-    static const bool mask_ew8 = [] {
+    // the fused ReLU-backward epilogue (mask loads) runs with 16 epilogue warps, except on
+    // very long GEMMs where 8 warps + the store-transpose staging win (6 M rows: 2.35 ->
+    // 2.19 ms; 2.4 M rows: 0.84 -> 0.88, 233 K: 0.092 -> 0.110 -- tools/gemm_bench.py).
+    // GDX_MASK_EW=8|16 overrides.
+    static const int mask_ew = [] {
         const char* e = std::getenv("GDX_MASK_EW");
-        return e && std::atoi(e) == 8;
+        return e ? std::atoi(e) : 0;
     }();
-    if (g->mask && !g->a_mn_major && g->b_mn_major && !mask_ew8)
+    const bool ew8 = mask_ew ? mask_ew == 8 : g->m >= (4u << 20);
+    if (g->mask && !g->a_mn_major && g->b_mn_major && !ew8)
         return launch_tc<BN, STAGES, false, true, 16>(g, ep, s);
     return launch_majors_ew<BN, STAGES, 8>(g, ep, s);
 }

@@ -139,16 +139,15 @@ AGG_FLAT = 3    # edge-flat walk over row groups (degree < 6)
 
 
 def agg_variant(width: int, nnz: int, rows: int) -> int:
-    """Aggregation kernel for a CSR (measured B200, 6 M rows x 64, tools/agg_bench.py):
-    degree 2.6 -> edge-flat 1.61 ms (row groups 1.68, warp per row 2.89); degree 12 ->
-    half-width row groups 3.60 ms (row groups 3.96); 48-wide rows -> row groups (5%
-    faster at degree 492); warp per row otherwise."""
+    """Aggregation kernel for a CSR.  Low degree (< 20): half-width row groups -- on a
+    papers-shape cooperative batch step 20.8 ms vs 21.5 (edge-flat) and 21.6 (row groups),
+    tools/profile_target.py; degree 12 alone 3.60 vs 3.96 ms (tools/agg_bench.py; the
+    edge-flat walk wins only on isolated degree-2.6 passes, 1.61 vs 1.68 ms).  48-wide
+    rows: row groups (5% faster at degree 492).  Warp per row otherwise."""
     deg = nnz / rows if rows else 0.0
     forced = os.environ.get("GDX_AGG_LOWDEG")   # tuning: force the low-degree kernel (1, 2, 3)
     if forced and rows and deg < 20:
         return int(forced)
-    if rows and deg < 6:
-        return AGG_FLAT
     if rows and deg < 20:
         return AGG_ROWS2
     return AGG_ROWS if pad4(width) == 48 else 0
