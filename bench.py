@@ -530,7 +530,8 @@ def run_cobatch(args, C, world, rank, local, dev, pg):
             "roofline": {
                 "bound": "hbm", "kernel": "gdx aggregate (K1/K3 gather-reduce, row-group variant)",
                 "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
+                "frac": round(achieved / peak, 4) if achieved else None,
+                "traffic": load_traffic(args.config)[0], "traffic_source": load_traffic(args.config)[1],
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "algorithmic_bytes_per_launch": int(agg_bytes / agg_launches) if agg_launches else None,
                 "avg_launch_ms": round(agg_avg_ms, 4) if agg_avg_ms else None,
