@@ -244,6 +244,20 @@ int gdx_push_rows(const void* base, uint64_t row_bytes, const uint32_t* idx, con
 int gdx_push_multicast(const void* src, uint64_t bytes, void* mc_dst, uint32_t npeers,
                        unsigned long long* const* peer_slots_dev, unsigned int* done, uint32_t ctas,
                        gdx_stream stream);
+/* The layer exchange and the aggregation in ONE cooperative kernel: every block pushes
+ * its share of this rank's row block (push_src, push_bytes) into every peer's copy
+ * (push_src + peer_delta[r]), aggregates the locally owned source segment of its rows
+ * ([seg_lo, seg_hi), into `partial`) while the stores drain, releases them (the last
+ * block bumps this rank's slot in every peer), waits until every peer's slot reached
+ * the round (*expected + 1; the last block to finish stores it), then aggregates the
+ * remote segments with the fused epilogue of `a` (a->row_end / skip / partial unused).
+ * Widths 32, 48, 64, 128.  counters: 2 zeroed u32.  Replaces gdx_push_peers +
+ * two gdx_aggregate passes + gdx_peer_wait. */
+int gdx_aggregate_exchange(const gdx_aggregate_args* a, const uint64_t* seg_lo, const uint64_t* seg_hi,
+                           float* partial, uint64_t ld_partial, const void* push_src, uint64_t push_bytes,
+                           const int64_t* peer_delta, uint32_t npeers, unsigned long long* const* peer_slots_dev,
+                           unsigned long long* slots, unsigned long long* expected, uint32_t world, uint32_t self,
+                           unsigned int* counters, uint64_t timeout_ns, gdx_stream stream);
 /* One copy-engine push (cudaMemcpyAsync D2D; dst may be an IPC-mapped peer address). */
 int gdx_memcpy_async(void* dst, const void* src, uint64_t bytes, gdx_stream stream);
 /* rows x width_bytes of a pitched buffer set to `value` (stream-ordered, graph-capturable). */
@@ -409,6 +423,8 @@ typedef struct gdx_trainer_config {
     double peer_timeout_s;    /* peer wait traps after this (0: 20 s); a trap poisons the context */
     uint32_t heavy_degree;    /* rows above this degree run chunked (gdx_row_bins); 0: auto
                                * (max(4096, 32 x mean degree)), 0xFFFFFFFF: never */
+    int fused_exchange;       /* world > 1: 1 = gdx_aggregate_exchange (one kernel per layer
+                               * exchange), 0 = push kernel + two passes + wait kernel */
 } gdx_trainer_config;
 typedef struct gdx_trainer_graph {
     uint32_t num_vertices;          /* V of the whole graph */

@@ -91,6 +91,8 @@ _SIGS = {
     "gdx_memset2d_async": (C.c_int, [vp, u64, C.c_int, u64, u64, vp]),
     "gdx_set_l2_window": (C.c_int, [vp, u64, C.c_float, vp]),
     "gdx_push_peers": (C.c_int, [vp, u64, vp, u32, vp, vp, u32, vp]),
+    "gdx_aggregate_exchange": (C.c_int, [C.POINTER(AggregateArgs), vp, vp, vp, u64, vp, u64, vp, u32, vp, vp, vp,
+                                         u32, u32, vp, u64, vp]),
     "gdx_peer_wait_src": (C.c_int, [vp, vp, u32, C.c_int, u64, vp]),
     "gdx_push_multicast": (C.c_int, [vp, u64, vp, u32, vp, vp, u32, vp]),
     "gdx_push_rows": (C.c_int, [vp, u64, vp, vp, vp, u32, vp, vp, u32, vp]),

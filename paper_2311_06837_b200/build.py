@@ -27,7 +27,7 @@ CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
              "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include"]
 
 SOURCES_CU = ["aggregate.cu", "gemm_tcgen05.cu", "dense_ops.cu", "sampling.cu", "exchange.cu",
-              "cobatch_plan.cu", "trainer.cu"]
+              "cobatch_plan.cu", "trainer.cu", "aggregate_exchange.cu"]
 SOURCES_CXX = ["host.cpp"]
 
 

@@ -140,6 +140,11 @@ struct gdx_trainer {
     uint64_t issued = 0, consumed = 0;
     double* loss_host = nullptr;  // pinned
     gdx_row_bins* bins = nullptr;  // degree bins (skewed graphs), else null
+    // fused exchange (cfg.fused_exchange): the pending push of the last publish, done by
+    // the next exchange_aggregate's kernel
+    const float* pending = nullptr;
+    uint64_t pending_bytes = 0;
+    unsigned int* xcounters = nullptr;
     // kernel profiling (eager epochs)
     bool profile = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -294,8 +299,19 @@ const int64_t* deltas_for(gdx_trainer* t, const void* p) {
     return nullptr;
 }
 
+int push_now(gdx_trainer* t, const float* own, uint64_t bytes);
+
 int publish(gdx_trainer* t, const float* own, uint64_t bytes) {
     if (t->world == 1 || t->subgraph) return GDX_OK;
+    if (t->cfg.fused_exchange) {  // pushed by the consuming exchange_aggregate's kernel
+        t->pending = own;
+        t->pending_bytes = bytes;
+        return GDX_OK;
+    }
+    return push_now(t, own, bytes);
+}
+
+int push_now(gdx_trainer* t, const float* own, uint64_t bytes) {
     const int64_t* deltas = deltas_for(t, own);
     if (!deltas) return err(GDX_INTERNAL, "publish: buffer outside the shared regions");
     TR_CUDA(cudaEventRecord(t->ev_fork, t->stream));
@@ -319,6 +335,38 @@ int wait_peers(gdx_trainer* t) {
 int exchange_aggregate(gdx_trainer* t, const Mat& full, uint32_t width, uint32_t rows, const AggEpi& e) {
     if (t->world == 1 || t->subgraph)
         return aggregate(t, full, width, rows, e, nullptr, nullptr, nullptr, nullptr, nullptr, t->nnz);
+    if (t->cfg.fused_exchange) {
+        const float* own = t->pending;
+        const uint64_t bytes = t->pending_bytes;
+        t->pending = nullptr;
+        const uint32_t c4 = width / 4;
+        const bool ok = width % 4 == 0 && (c4 == 8 || c4 == 12 || c4 == 16 || c4 == 32) && !t->bins && !t->profile &&
+                        own && rows == t->nloc;
+        if (!ok) {  // not fusable here: the two-pass path with the deferred push
+            if (own) TR_OK(push_now(t, own, bytes));
+        } else {
+            gdx_aggregate_args a{};
+            a.row_ptr = t->row_ptr;
+            a.col = t->col;
+            a.rows = rows;
+            a.width = width;
+            a.src = full.p;
+            a.ld_src = full.ld;
+            a.self_coef = e.self_coef;
+            a.self_base = t->lo;
+            a.post_scale = e.post_scale;
+            if (e.add.p) { a.add = e.add.p; a.ld_add = e.add.ld; }
+            a.relu = e.relu;
+            if (e.has_out) { a.out = e.out.p; a.ld_out = e.out.ld; }
+            if (e.has_split) { a.out_hi = e.out_split.hi; a.out_lo = e.out_split.lo; a.ld_split = e.out_split.ld; }
+            const uint64_t timeout = t->cfg.peer_timeout_s > 0 ? static_cast<uint64_t>(t->cfg.peer_timeout_s * 1e9)
+                                                                : 20000000000ull;
+            return gdx_aggregate_exchange(&a, t->seg_lo, t->seg_hi, t->partial.p, t->partial.ld, own, bytes,
+                                          deltas_for(t, own), t->world - 1, t->peer_slots_dev, t->slots, t->expected,
+                                          t->world, t->rank, t->xcounters, timeout,
+                                          reinterpret_cast<gdx_stream>(t->stream));
+        }
+    }
     Mat P = t->partial;  // first pad4(width) columns, pitch of the widest layer
     AggEpi pe;
     pe.out = P;
@@ -596,6 +644,7 @@ int setup_model(gdx_trainer* t) {
     t->slots = reinterpret_cast<unsigned long long*>(t->arena + slots_off + 256);
     TR_OK(dalloc(t, &t->expected, 1));
     TR_OK(dalloc(t, &t->push_done, 1));
+    TR_OK(dalloc(t, &t->xcounters, 2));
     TR_OK(dalloc(t, &t->peer_slots_dev, 8));
     for (uint32_t l = 0; l < t->L; ++l) {
         Layer& Ly = t->layers[l];

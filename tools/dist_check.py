@@ -23,7 +23,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 KNOBS = ("GDX_EXCHANGE", "GDX_PUSH", "GDX_P2P_SPLIT", "GDX_P2P_RING", "GDX_OVERLAP",
-         "GDX_DW_OVERLAP", "GDX_CE_SPLIT", "GDX_AGG_FIRST")
+         "GDX_DW_OVERLAP", "GDX_CE_SPLIT", "GDX_AGG_FIRST", "GDX_FUSED_EXCHANGE")
 # every exchange path the trainers can take (train.py P2PExchange / RowExchange)
 MODES = {
     "sm": {},                                              # default: SM push + local/remote split
@@ -37,7 +37,8 @@ MODES = {
     "nccl": {"GDX_EXCHANGE": "nccl"},                      # all_gather_into_tensor, overlapped
     "nccl-nooverlap": {"GDX_EXCHANGE": "nccl", "GDX_OVERLAP": "0"},
     "dw-overlap": {"GDX_DW_OVERLAP": "1"},                 # dW GEMMs on a side stream
-    "native": {"_NATIVE": "1"},                            # C-ABI trainer (csrc/trainer.cu): IPC arena
+    "native": {"_NATIVE": "1"},                            # C-ABI trainer (csrc/trainer.cu): IPC buffers
+    "native-fused": {"_NATIVE": "1", "GDX_FUSED_EXCHANGE": "1"},  # one kernel: push + aggregate + wait
     "native-eas": {"_NATIVE": "eas"},                      # C-ABI trainer, per-rank EAS subgraphs
 }
 FULL_CASES = (("sage", 5001, 24.0, [96, 64, 64, 41], 5),

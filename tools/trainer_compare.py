@@ -61,6 +61,12 @@ def main():
     ft.capture(warmup=2)
     out["torch_ms"] = timeit(ft.replay, torch.cuda.current_stream())
     out["native_ms_again"] = timeit(lambda: nt.train_epoch(sync_loss=False), nt.stream())
+    if world > 1:   # the one-kernel exchange + aggregation
+        nf = NativeTrainer(g, cfg, rank=rank, world=world, pg=pg, fused_exchange=True)
+        out["native_fused_ms"] = timeit(lambda: nf.train_epoch(sync_loss=False), nf.stream())
+        torch.cuda.synchronize()
+        dist.barrier()
+        nf.close()
     # aggregation launches of eager epochs (CUDA events on each trainer's stream)
     nt2 = NativeTrainer(g, cfg, rank=rank, world=world, pg=pg, use_graph=False)
     nt2.profile(True)
