@@ -66,6 +66,13 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t po
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
+__device__ __forceinline__ float4 ld_row4_nc(const void* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
 // coherent 16-byte row load (rows written by peers during this kernel must not use .nc)
 __device__ __forceinline__ float4 ld_row4_coherent(const void* p, uint64_t pol) {
     float4 v;
@@ -88,7 +95,7 @@ __device__ __forceinline__ void add4(float4& a, const float4& b) {
 
 // One warp gathers edges [b, e) of a row: LPE lanes per neighbour row (one float4 each),
 // EPW rows per step, UNROLL steps in flight.  Partial sums stay per lane group.
-template <int LPE, int UNROLL>
+template <int LPE, int UNROLL, bool NC>
 __device__ __forceinline__ void gather(const Agg& p, uint64_t b, uint64_t e, int lane, int sub, bool lane_on,
                                        uint64_t base, uint64_t pol_keep, uint64_t pol_stream, float4& acc) {
     constexpr int EPW = 32 / LPE >= 32 ? 32 : (32 / LPE >= 16 ? 16 : (32 / LPE >= 8 ? 8 : (32 / LPE >= 4 ? 4 : (32 / LPE >= 2 ? 2 : 1))));
@@ -104,7 +111,8 @@ __device__ __forceinline__ void gather(const Agg& p, uint64_t b, uint64_t e, int
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
                 const uint32_t nb = __shfl_sync(0xffffffffu, my, (j + u * EPW + sub) & 31);
-                v[u] = lane_on ? ld_row4_coherent(row_addr(base, nb, p.ld_bytes), pol_keep)
+                const char* rp = row_addr(base, nb, p.ld_bytes);
+                v[u] = lane_on ? (NC ? ld_row4_nc(rp, pol_keep) : ld_row4_coherent(rp, pol_keep))
                                : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
@@ -113,7 +121,10 @@ __device__ __forceinline__ void gather(const Agg& p, uint64_t b, uint64_t e, int
         for (; j < cnt; j += EPW) {
             const uint32_t slot = j + sub;
             const uint32_t nb = __shfl_sync(0xffffffffu, my, slot & 31);
-            if (lane_on && slot < cnt) add4(acc, ld_row4_coherent(row_addr(base, nb, p.ld_bytes), pol_keep));
+            if (lane_on && slot < cnt) {
+                const char* rp = row_addr(base, nb, p.ld_bytes);
+                add4(acc, NC ? ld_row4_nc(rp, pol_keep) : ld_row4_coherent(rp, pol_keep));
+            }
         }
         my = nxt;
     }
@@ -131,8 +142,8 @@ __device__ __forceinline__ void combine(float4& acc) {
     }
 }
 
-template <int LPE, int UNROLL>
-__global__ void __launch_bounds__(256) aggregate_exchange(const Agg p, const Xchg x) {
+template <int LPE, int UNROLL, bool REMOTE_NC>
+__global__ void __launch_bounds__(256, 8) aggregate_exchange(const Agg p, const Xchg x) {
     constexpr int EPW = 32 / LPE >= 32 ? 32 : (32 / LPE >= 16 ? 16 : (32 / LPE >= 8 ? 8 : (32 / LPE >= 4 ? 4 : (32 / LPE >= 2 ? 2 : 1))));
     __shared__ unsigned long long s_target;
     const int lane = threadIdx.x & 31;
@@ -152,14 +163,17 @@ __global__ void __launch_bounds__(256) aggregate_exchange(const Agg p, const Xch
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < x.push_n16; i += stride) {
             const uint4 v = __ldg(x.push_src + i);
-            for (uint32_t r = 0; r < x.npeers; ++r)
-                reinterpret_cast<uint4*>(reinterpret_cast<char*>(const_cast<uint4*>(x.push_src)) + x.delta[r])[i] = v;
+#pragma unroll
+            for (int r = 0; r < 7; ++r)  // static indices: the deltas stay in the parameter bank
+                if (static_cast<uint32_t>(r) < x.npeers)
+                    reinterpret_cast<uint4*>(reinterpret_cast<char*>(const_cast<uint4*>(x.push_src)) + x.delta[r])[i] = v;
         }
     }
     // 1. local-source segments -> partial
     for (uint32_t row = warp0; row < p.rows; row += warps_total) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        gather<LPE, UNROLL>(p, p.seg_lo[row], p.seg_hi[row], lane, sub, lane_on, base, pol_keep, pol_stream, acc);
+        // our own rows: not written by anyone during this kernel, the read-only path is legal
+        gather<LPE, UNROLL, true>(p, p.seg_lo[row], p.seg_hi[row], lane, sub, lane_on, base, pol_keep, pol_stream, acc);
         combine<LPE>(acc);
         if (sub == 0) *reinterpret_cast<float4*>(p.partial + row * p.ld_partial + 4 * lin) = acc;
     }
@@ -170,7 +184,7 @@ __global__ void __launch_bounds__(256) aggregate_exchange(const Agg p, const Xch
         const unsigned int prev = atomicAdd(&x.counters[0], 1u);
         if (prev == gridDim.x - 1) {
             __threadfence_system();
-            for (uint32_t r = 0; r < x.npeers; ++r) atomicAdd_system(x.peer_slots[r], 1ull);
+            for (uint32_t r = 0; r < x.npeers; ++r) atomicAdd_system(x.peer_slots[r], 1ull);  // (once per kernel)
             x.counters[0] = 0;
         }
         // 3. wait for every peer's rows of this round
@@ -196,8 +210,8 @@ __global__ void __launch_bounds__(256) aggregate_exchange(const Agg p, const Xch
     for (uint32_t row = warp0; row < p.rows; row += warps_total) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         const uint64_t rb = p.row_ptr[row], re = p.row_ptr[row + 1];
-        gather<LPE, UNROLL>(p, rb, p.seg_lo[row], lane, sub, lane_on, base, pol_keep, pol_stream, acc);
-        gather<LPE, UNROLL>(p, p.seg_hi[row], re, lane, sub, lane_on, base, pol_keep, pol_stream, acc);
+        gather<LPE, UNROLL, REMOTE_NC>(p, rb, p.seg_lo[row], lane, sub, lane_on, base, pol_keep, pol_stream, acc);
+        gather<LPE, UNROLL, REMOTE_NC>(p, p.seg_hi[row], re, lane, sub, lane_on, base, pol_keep, pol_stream, acc);
         combine<LPE>(acc);
         if (sub != 0) continue;
         const uint32_t ch = lin;
@@ -247,7 +261,8 @@ __global__ void __launch_bounds__(256) aggregate_exchange(const Agg p, const Xch
 
 template <int LPE>
 int launch(const Agg& p, const Xchg& x, cudaStream_t s) {
-    auto kern = aggregate_exchange<LPE, 4>;
+    // remote rows through the coherent path (reading them via .nc measured no faster)
+    auto kern = aggregate_exchange<LPE, 4, false>;
     static int per_sm[64] = {0};  // resident blocks per SM (per device)
     int dev = 0;
     GDX_CUDA(cudaGetDevice(&dev));
