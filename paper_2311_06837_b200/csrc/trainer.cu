@@ -376,10 +376,9 @@ int exchange_aggregate(gdx_trainer* t, const Mat& full, uint32_t width, uint32_t
     return aggregate(t, full, width, rows, e, nullptr, nullptr, t->seg_lo, t->seg_hi, &P, t->nnz - t->nnz_src);
 }
 
-const Mat& act(gdx_trainer* t, uint32_t l) {  // fp32 output rows of layer l (ReLU mask)
+Mat act(gdx_trainer* t, uint32_t l) {  // fp32 output rows of layer l (ReLU mask)
     if (l + 1 < t->L && t->layers[l + 1].agg_first) {
-        static thread_local Mat v;
-        v = t->layers[l + 1].Xin_full;
+        Mat v = t->layers[l + 1].Xin_full;
         v.p = v.row(t->lo);
         return v;
     }
@@ -489,7 +488,7 @@ int backward_agg_first(gdx_trainer* t, uint32_t l) {
     e.add = Ly.dself;
     TR_OK(exchange_aggregate(t, Ly.dAfull, Ly.w, t->rows_in[l], e));
     GradTargets gt = grad_targets(t, l - 1);
-    const Mat& a = act(t, l - 1);
+    const Mat a = act(t, l - 1);
     TR_OK(gdx_grad_prepare(Ly.dtmp.p, Ly.dtmp.ld, a.p, a.ld, t->rows_out[l - 1], Ly.w, gt.scale, nullptr, 0, gt.own.p,
                            gt.own.ld, gt.split ? gt.split->hi : nullptr, gt.split ? gt.split->lo : nullptr,
                            gt.split ? gt.split->ld : 0, reinterpret_cast<gdx_stream>(t->stream)));
@@ -518,7 +517,7 @@ int backward_and_step(gdx_trainer* t) {
         TR_OK(exchange_aggregate(t, Ly.dfull, Ly.w, r_in, e));
         if (l > 0) {  // dH_{l-1} = G W_cat, ReLU mask + scale + split fused in the epilogue
             GradTargets gt = grad_targets(t, l - 1);
-            const Mat& a = act(t, l - 1);
+            const Mat a = act(t, l - 1);
             TR_OK(gemm(t, Ly.G, Ly.Wsp, false, true, t->rows_out[l - 1], gt.own, Mat{}, 0, gt.scale, false,
                        gt.split, 1, &a, true));
             TR_OK(publish(t, gt.own.p, t->nloc * t->layers[l - 1].dfull.ld * 4));
