@@ -137,6 +137,7 @@ struct gdx_trainer {
     float* stage[2] = {nullptr, nullptr};
     int32_t* stage_labels[2] = {nullptr, nullptr};
     cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+    bool staged_labels[2] = {false, false};
     uint64_t issued = 0, consumed = 0;
     double* loss_host = nullptr;  // pinned
     gdx_row_bins* bins = nullptr;  // degree bins (skewed graphs), else null
@@ -1094,6 +1095,7 @@ extern "C" int gdx_trainer_stage_inputs(gdx_trainer* t, const float* x_host, con
     GDX_CUDA(cudaMemcpyAsync(t->stage[i], x_host, t->nloc * t->F * 4, cudaMemcpyHostToDevice, t->copy));
     if (labels_host)
         GDX_CUDA(cudaMemcpyAsync(t->stage_labels[i], labels_host, t->nloc * 4, cudaMemcpyHostToDevice, t->copy));
+    t->staged_labels[i] = labels_host != nullptr;
     GDX_CUDA(cudaEventRecord(t->ready[i], t->copy));
     t->issued++;
     return GDX_OK;
@@ -1104,6 +1106,8 @@ extern "C" int gdx_trainer_step_staged(gdx_trainer* t, int with_labels, double* 
     GDX_REQUIRE(t->consumed < t->issued, GDX_CONTRACT, "gdx_trainer_step_staged: nothing staged");
     GDX_CUDA(cudaSetDevice(t->dev));
     const int i = static_cast<int>(t->consumed % 2);
+    GDX_REQUIRE(!with_labels || t->staged_labels[i], GDX_CONTRACT,
+                "gdx_trainer_step_staged: labels requested but none were staged");
     GDX_CUDA(cudaStreamWaitEvent(t->stream, t->ready[i], 0));
     if (t->nloc)
         TR_OK(gdx_split_bf16(t->stage[i], t->F, static_cast<uint32_t>(t->nloc), t->F, t->Xsp.hi, t->Xsp.lo, t->Xsp.ld, 0,
