@@ -472,6 +472,9 @@ int gdx_trainer_info(const gdx_trainer* t, uint64_t* out, uint32_t count);
 /* Per-aggregation CUDA events on eager epochs (on = 1); reading (non-null outputs)
  * returns the total ms, launch count and algorithmic bytes since on. */
 int gdx_trainer_profile(gdx_trainer* t, int on, double* ms, uint64_t* launches, double* bytes);
+/* The tcgen05 GEMMs of the same profiled epochs: total ms, launches, useful flops
+ * (2 m n k each; read it BEFORE the gdx_trainer_profile read that resets the events). */
+int gdx_trainer_profile_gemm(gdx_trainer* t, double* ms, uint64_t* launches, double* flops);
 
 #ifdef __cplusplus
 }

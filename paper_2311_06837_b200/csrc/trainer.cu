@@ -150,6 +150,8 @@ struct gdx_trainer {
     bool profile = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
     std::vector<double> prof_bytes;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gemm_events;  // tcgen05 GEMMs (useful flops)
+    std::vector<double> gemm_flops;
 
     ~gdx_trainer();
 };
@@ -249,7 +251,16 @@ int gemm(gdx_trainer* t, const Spl& A, const Spl& B, bool a_mn, bool b_mn, uint3
     g.split_k = split_k;
     if (mask) { g.mask = mask->p; g.ld_mask = mask->ld; }
     g.split_unscaled = split_unscaled;
-    return gdx_gemm_tn(&g, reinterpret_cast<gdx_stream>(t->stream));
+    if (!t->profile) return gdx_gemm_tn(&g, reinterpret_cast<gdx_stream>(t->stream));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    TR_CUDA(cudaEventCreate(&e0));
+    TR_CUDA(cudaEventCreate(&e1));
+    TR_CUDA(cudaEventRecord(e0, t->stream));
+    TR_OK(gdx_gemm_tn(&g, reinterpret_cast<gdx_stream>(t->stream)));
+    TR_CUDA(cudaEventRecord(e1, t->stream));
+    t->gemm_events.push_back({e0, e1});
+    t->gemm_flops.push_back(2.0 * m * nB * kA);  // useful flops (the split operands issue 3 bf16 MMAs per product)
+    return GDX_OK;
 }
 
 int aggregate(gdx_trainer* t, const Mat& src, uint32_t width, uint32_t rows, const AggEpi& e,
@@ -771,6 +782,10 @@ gdx_trainer::~gdx_trainer() {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
+    for (auto& e : gemm_events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
     for (void* p : opened) cudaIpcCloseMemHandle(p);
     for (void* p : owned) cudaFree(p);
     for (int i = 0; i < 2; ++i) {
@@ -1130,6 +1145,23 @@ extern "C" int gdx_trainer_info(const gdx_trainer* t, uint64_t* out, uint32_t co
     return GDX_OK;
 }
 
+extern "C" int gdx_trainer_profile_gemm(gdx_trainer* t, double* ms, uint64_t* launches, double* flops) {
+    GDX_REQUIRE(t && ms && launches && flops, GDX_INPUT, "gdx_trainer_profile_gemm: null pointer");
+    GDX_CUDA(cudaSetDevice(t->dev));
+    GDX_CUDA(cudaStreamSynchronize(t->stream));
+    double tot = 0, fl = 0;
+    for (size_t i = 0; i < t->gemm_events.size(); ++i) {
+        float x = 0;
+        GDX_CUDA(cudaEventElapsedTime(&x, t->gemm_events[i].first, t->gemm_events[i].second));
+        tot += x;
+        fl += t->gemm_flops[i];
+    }
+    *ms = tot;
+    *launches = t->gemm_events.size();
+    *flops = fl;
+    return GDX_OK;
+}
+
 extern "C" int gdx_trainer_profile(gdx_trainer* t, int on, double* ms, uint64_t* launches, double* bytes) {
     GDX_REQUIRE(t, GDX_INPUT, "gdx_trainer_profile: null trainer");
     GDX_CUDA(cudaSetDevice(t->dev));
@@ -1152,6 +1184,12 @@ extern "C" int gdx_trainer_profile(gdx_trainer* t, int on, double* ms, uint64_t*
     }
     t->prof_events.clear();
     t->prof_bytes.clear();
+    for (auto& e : t->gemm_events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    t->gemm_events.clear();
+    t->gemm_flops.clear();
     t->profile = on != 0;
     return GDX_OK;
 }

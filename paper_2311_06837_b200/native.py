@@ -56,6 +56,8 @@ _SIGS = {
     "gdx_trainer_info": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32]),
     "gdx_trainer_profile": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                       C.POINTER(C.c_double)]),
+    "gdx_trainer_profile_gemm": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                           C.POINTER(C.c_double)]),
 }
 _bound = False
 
@@ -231,6 +233,12 @@ class NativeTrainer:
 
     def profile(self, on: bool):
         call("gdx_trainer_profile", self._h, int(on), None, None, None)
+
+    def profile_read_gemm(self):
+        """(ms, launches, useful flops) of the profiled epochs' GEMMs (call before profile_read)."""
+        ms, n, fl = C.c_double(), C.c_uint64(), C.c_double()
+        call("gdx_trainer_profile_gemm", self._h, C.byref(ms), C.byref(n), C.byref(fl))
+        return ms.value, int(n.value), fl.value
 
     def profile_read(self):
         ms, n, by = C.c_double(), C.c_uint64(), C.c_double()
