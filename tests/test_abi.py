@@ -186,3 +186,31 @@ def test_host_sample_trace_attribution(m, k, seed):
     assert dict(taken) == halo
     for s in tr:
         assert (s.hop == 1 and inner[s.frontier_vertex]) or hop[s.frontier_vertex] == s.hop - 1
+
+
+def test_trainer_create_validates_before_device_work():
+    """gdx_trainer_create's argument checks (status + message, no GPU needed): model kind,
+    layer dims, class count, world/rank, CSR pointers."""
+    import ctypes as C
+
+    from paper_2311_06837_b200 import _lib, native
+    L = native._bind()
+    ro = (C.c_uint64 * 3)(0, 1, 2)
+    ci = (C.c_uint32 * 2)(1, 0)
+    gr = native.TrainerGraph(2, 2, C.cast(ro, C.c_void_p), C.cast(ci, C.c_void_p))
+
+    def create(kind=2, dims=(8, 8, 4), world=1, rank=0, graph=gr):
+        d = (C.c_uint32 * len(dims))(*dims)
+        cfg = native.TrainerConfig(kind, len(dims) - 1, d, 0.1, rank, world, 0, 1, 2, 1, 0, 0, 0.0)
+        h = C.c_void_p()
+        rc = L.gdx_trainer_create(C.byref(cfg), C.byref(graph), C.byref(h))
+        if rc == 0:
+            L.gdx_trainer_destroy(h)
+        return rc, L.gdx_last_error().decode()
+
+    assert create(kind=7) == (1, "gdx_trainer_create: unknown model kind")
+    assert create(dims=(8, 0, 4))[0] == 1 and "dims must be >= 1" in create(dims=(8, 0, 4))[1]
+    assert "classes must be <= 256" in create(dims=(8, 8, 300))[1]
+    assert "rank < world" in create(world=2, rank=2)[1]
+    bad = native.TrainerGraph(2, 2, None, None)
+    assert "null CSR" in create(graph=bad)[1]
