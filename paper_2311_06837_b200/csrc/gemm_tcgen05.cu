@@ -167,13 +167,27 @@ struct Epi {
     int peer_target;
     int64_t peer_delta[7];
     int stage_stores;       // row-contiguous (smem-transposed) fp32 stores
+    int tma_store;          // ... leaving smem through TMA bulk tensor stores (map_c0 / map_c1)
 };
 
-// Store transpose buffer: per epilogue warp 32 rows x 16 fp32, row pitch 20 floats
-// (16-byte aligned rows; a quarter-warp's 8 float4 accesses hit distinct bank groups
-// in both the row-per-thread writes and the row-contiguous reads).
+// Store transpose buffers, 4 KB per epilogue warp (32 KB at EW = 8):
+//  * TMA stores: two 32 rows x 16 fp32 boxes (2 KB each, 64-byte rows in the SWIZZLE_64B
+//    layout, so the row-per-thread float4 writes of a quarter-warp hit 8 distinct bank
+//    groups); one elected lane issues cp.async.bulk.tensor per box and the warp moves on,
+//    double-buffered on bulk_group completion;
+//  * register stores (peer copies): one 32 x 16 box at row pitch 20 floats.
 constexpr uint32_t kStgPitch = 20;
-constexpr uint32_t kStgBytesFor(int ew) { return ew <= 8 ? ew * 32 * kStgPitch * 4 : 0; }  // 20 KB at 8
+constexpr uint32_t kStgWarpFloats = 1024;
+constexpr uint32_t kStgBytesFor(int ew) { return ew <= 8 ? ew * kStgWarpFloats * 4 : 0; }
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c_inner,
+                                             int32_t c_outer) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c_inner), "r"(c_outer)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 
 // store one float4 locally and, for the exchanged output, into every peer buffer
 __device__ __forceinline__ void store4x(float* p, const float4& v, const Epi& ep, bool xchg) {
@@ -216,6 +230,7 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EW>
 __global__ void __launch_bounds__(kThreadsFor(EW), 1)
     gemm_bf16x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                const __grid_constant__ CUtensorMap map_c0, const __grid_constant__ CUtensorMap map_c1,
                 const Epi ep) {
     using S = Smem<BN, STAGES, EW>;
     constexpr int kEpiWarps = EW;
@@ -252,6 +267,10 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+        if (ep.tma_store) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_c0)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_c1)) : "memory");
+        }
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -339,6 +358,8 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
         constexpr int kCols = BN / (kEpiWarps / 4);       // columns per epilogue warp
         constexpr int kChunk = kCols < 32 ? kCols : 32;   // columns per TMEM load
         const uint32_t col_base = (warp - 2) / 4 * kCols;  // which part of the tile
+        float* wstage = epi_stage + (warp - 2) * kStgWarpFloats;
+        uint32_t sbuf = 0;  // TMA store buffer toggle
         uint32_t tl = 0;
         for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
             uint32_t mt, nt, z;
@@ -378,6 +399,8 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
                     float* fdst = nullptr;
                     uint64_t fld = 0;
                     bool fx = false;
+                    const CUtensorMap* fmap = &map_c0;
+                    int32_t fcol = static_cast<int32_t>(col0);
                     if (kStgBytes && ep.stage_stores && ep.split_k <= 1 && col0 + 16 <= ep.n) {
                         if (col0 + 16 <= ep.split && ep.c0 && ep.ldc0 % 4 == 0) {
                             fdst = ep.c0 + col0;
@@ -387,6 +410,8 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
                             fdst = ep.c1 + (col0 - ep.split);
                             fld = ep.ldc1;
                             fx = ep.npeers && ep.peer_target == 1;
+                            fmap = &map_c1;
+                            fcol = static_cast<int32_t>(col0 - ep.split);
                         }
                         if (fdst && (reinterpret_cast<uintptr_t>(fdst) & 15) != 0) fdst = nullptr;
                     }
@@ -431,15 +456,34 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
                         vv[j] *= rs;
                         if (ep.relu) vv[j] = fmaxf(vv[j], 0.f);
                     }
+                    if (fdst && ep.tma_store && !fx) {
+                        float* buf = wstage + sbuf * 512;
+                        if (lane == 0)  // the box written two stores ago has been read out
+                            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        __syncwarp();
+                        const uint32_t sw = (lane >> 1) & 3;  // SWIZZLE_64B: chunk ^= row bits [2:1]
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            *reinterpret_cast<float4*>(buf + lane * 16 + ((j ^ sw) << 2)) =
+                                make_float4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) tma_store_2d(fmap, buf, fcol, static_cast<int32_t>(mt * BM + lane_base));
+                        sbuf ^= 1;
+                        if (ep.out_hi && !ep.split_unscaled && row_ok)
+                            store_split16(vv, ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0,
+                                          ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0, col0, ep.n);
+                        continue;
+                    }
                     if (fdst) {
-                        float* srow = epi_stage + ((warp - 2) * 32 + lane) * kStgPitch;
+                        float* srow = wstage + lane * kStgPitch;
                         __syncwarp();
 #pragma unroll
                         for (int j = 0; j < 16; j += 4)
                             *reinterpret_cast<float4*>(srow + j) = make_float4(vv[j], vv[j + 1], vv[j + 2], vv[j + 3]);
                         __syncwarp();
                         const uint32_t sr = lane >> 2, sc = (lane & 3) * 4;
-                        const float* sbase = epi_stage + (warp - 2) * 32 * kStgPitch;
+                        const float* sbase = wstage;
 #pragma unroll
                         for (int pass = 0; pass < 4; ++pass) {
                             const uint32_t r = pass * 8 + sr;
@@ -494,6 +538,7 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if (ep.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -568,6 +613,31 @@ int make_map(CUtensorMap* map, const uint16_t* base, uint64_t inner, uint64_t ou
     return GDX_OK;
 }
 
+// fp32 output map for the TMA-store epilogue: (cols inner, rows outer), box {16, 32},
+// 64-byte rows swizzled as the epilogue writes them.
+int make_out_map(CUtensorMap* map, float* base, uint64_t cols, uint64_t rows, uint64_t ld) {
+    auto fn = encode_fn();
+    GDX_REQUIRE(fn != nullptr, GDX_INTERNAL, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * 4};
+    cuuint32_t box[2] = {16u, 32u};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    GDX_REQUIRE(r == CUDA_SUCCESS, GDX_INTERNAL,
+                "cuTensorMapEncodeTiled (output) failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return GDX_OK;
+}
+
+bool tma_store_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("GDX_GEMM_TMA_STORE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // Operand maps: K-major = (k inner, rows outer, box {64, rows_per_tile});
 // MN-major = (rows inner, k outer, box {64, BK}).
 int operand_maps(CUtensorMap* hi, CUtensorMap* lo, const uint16_t* phi, const uint16_t* plo,
@@ -587,13 +657,29 @@ int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     int rc;
     if ((rc = operand_maps(&ma_hi, &ma_lo, g->a_hi, g->a_lo, g->m, g->k, g->lda, A_MN, BM))) return rc;
     if ((rc = operand_maps(&mb_hi, &mb_lo, g->b_hi, g->b_lo, g->n, g->k, g->ldb, B_MN, BN))) return rc;
+    // TMA-store epilogue for the staged fp32 outputs (16-byte aligned bases, pitch % 4)
+    CUtensorMap mc0{}, mc1{};
+    Epi e = ep;
+    e.tma_store = 0;
+    if (kStgBytesFor(EW) && ep.stage_stores && ep.split_k <= 1 && tma_store_enabled()) {
+        const bool ok0 = !ep.c0 || (ep.split >= 16 && ep.ldc0 % 4 == 0 &&
+                                    (reinterpret_cast<uintptr_t>(ep.c0) & 15) == 0);
+        const bool ok1 = !ep.c1 || ep.split >= ep.n ||
+                         (ep.ldc1 % 4 == 0 && (reinterpret_cast<uintptr_t>(ep.c1) & 15) == 0);
+        if (ok0 && ok1) {
+            if (ep.c0 && ep.split >= 16 && (rc = make_out_map(&mc0, ep.c0, ep.split, ep.m, ep.ldc0))) return rc;
+            if (ep.c1 && ep.split < ep.n && (rc = make_out_map(&mc1, ep.c1, ep.n - ep.split, ep.m, ep.ldc1)))
+                return rc;
+            e.tma_store = 1;
+        }
+    }
     auto kern = gemm_bf16x3<BN, STAGES, A_MN, B_MN, EW>;
     const int bytes = Smem<BN, STAGES, EW>::kBytes;
     if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), bytes))) return rc;
     const uint64_t sms = static_cast<uint64_t>(device_sms());
     const uint64_t tiles = static_cast<uint64_t>(ep.m_tiles) * ep.n_tiles * ep.split_k;
     const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
-    kern<<<grid, kThreadsFor(EW), bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, ep);
+    kern<<<grid, kThreadsFor(EW), bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, mc0, mc1, e);
     note_launch();
     return check_launch("gdx_gemm_tn");
 }
@@ -646,7 +732,7 @@ Epi make_epi(const gdx_gemm_args* g, int bn) {
            g->mask, g->ld_mask, g->split_unscaled, g->npeers, g->peer_target, {},
            // measured (tools/gemm_bench.py): the transposed stores win on long
            // write-bound GEMMs (6 M rows: 1.2-1.25x) and lose on short ones (233 K rows)
-           g->m >= (1u << 20) ? 1 : 0};
+           g->m >= (1u << 20) ? 1 : 0, 0};
     for (int r = 0; r < 7; ++r) ep.peer_delta[r] = g->peer_delta[r];
     return ep;
 }

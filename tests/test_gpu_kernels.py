@@ -224,12 +224,13 @@ def test_gemm_mask_epilogue_fused_backward(gdx, cuda, m):
     close(out[ri, :n].double().cpu().numpy(), gref * scale[rows, None])
 
 
-@pytest.mark.parametrize("relu", [False, True])
-def test_gemm_staged_split_outputs(gdx, cuda, relu):
-    """Long forward GEMM (staged epilogue): c0/c1 column split + scaled split copy."""
+@pytest.mark.parametrize("relu,split", [(False, 64), (True, 64), (False, 40)])
+def test_gemm_staged_split_outputs(gdx, cuda, relu, split):
+    """Long forward GEMM (staged epilogue: TMA bulk stores of swizzled 32 x 16 boxes, the
+    register path for groups straddling the split): c0/c1 column split + split copy."""
     import torch
     rng = np.random.default_rng(5)
-    m, n, k, split = 1_050_001, 128, 64, 64
+    m, n, k = 1_050_001, 128, 64
     a = rng.uniform(-1, 1, (m, k))
     b = rng.uniform(-1, 1, (n, k))
     A, B = _split(gdx, a, cuda), _split(gdx, b, cuda)
