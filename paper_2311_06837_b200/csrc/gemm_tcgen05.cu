@@ -29,6 +29,9 @@
 
 #include "gdx_common.cuh"
 
+// the MT instantiation leaves the generic epilogue loop unreachable by design
+#pragma nv_diag_suppress 128
+
 namespace gdx {
 namespace {
 
@@ -180,14 +183,26 @@ constexpr uint32_t kStgPitch = 20;
 constexpr uint32_t kStgWarpFloats = 1024;
 constexpr uint32_t kStgBytesFor(int ew) { return ew <= 8 ? ew * kStgWarpFloats * 4 : 0; }
 
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c_inner,
-                                             int32_t c_outer) {
+__device__ __forceinline__ void tma_store_2d_nc(const CUtensorMap* map, const void* src, int32_t c_inner,
+                                                int32_t c_outer) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                      reinterpret_cast<uint64_t>(map)),
                  "r"(smem_u32(src)), "r"(c_inner), "r"(c_outer)
                  : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c_inner,
+                                             int32_t c_outer) {
+    tma_store_2d_nc(map, src, c_inner, c_outer);
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+
+// Fused ReLU-backward (MT) variant, BN = 64 only: the producer warp also TMA-loads the
+// tile's 128 x 64 fp32 mask (two 128B-swizzled 128 x 32 boxes, double-buffered with the
+// accumulators), and every output -- the scaled fp32 c0 and the split hi/lo copy --
+// leaves through TMA stores. Per epilogue warp and store buffer: fp32 box 2 KB
+// (SWIZZLE_64B) + hi 1 KB + lo 1 KB (32 x 16 u16, SWIZZLE_32B), two buffers.
+constexpr uint32_t kMaskTile = BM * 64 * 4;       // 32 KB
+constexpr uint32_t kMtWarpBytes = 2 * 4096;       // per epilogue warp
 
 // store one float4 locally and, for the exchanged output, into every peer buffer
 __device__ __forceinline__ void store4x(float* p, const float4& v, const Epi& ep, bool xchg) {
@@ -202,13 +217,14 @@ __device__ __forceinline__ void store1x(float* p, float v, const Epi& ep, bool x
         for (uint32_t r = 0; r < ep.npeers; ++r) *reinterpret_cast<float*>(reinterpret_cast<char*>(p) + ep.peer_delta[r]) = v;
 }
 
-template <int BN, int STAGES, int EW>
+template <int BN, int STAGES, int EW, bool MT = false>
 struct Smem {
     static constexpr uint32_t kA = BM * BK * 2;  // bytes per A operand tile (hi or lo)
     static constexpr uint32_t kB = BN * BK * 2;
     static constexpr uint32_t kStage = 2 * kA + 2 * kB;
-    static constexpr uint32_t kStaging = kStgBytesFor(EW);  // epilogue store transposes
-    static constexpr uint32_t kBytes = STAGES * kStage + kStaging + 1024 /*align*/ + 512 /*barriers*/;
+    static constexpr uint32_t kStaging = MT ? EW * kMtWarpBytes : kStgBytesFor(EW);  // epilogue store transposes
+    static constexpr uint32_t kMask = MT ? 2 * kMaskTile : 0;
+    static constexpr uint32_t kBytes = STAGES * kStage + kStaging + kMask + 1024 /*align*/ + 512 /*barriers*/;
     static_assert(kBytes <= 232448, "227 KB shared memory per CTA");
 };
 
@@ -226,24 +242,29 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* ma
     }
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, int EW>
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EW, bool MT>
 __global__ void __launch_bounds__(kThreadsFor(EW), 1)
     gemm_bf16x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                 const __grid_constant__ CUtensorMap map_c0, const __grid_constant__ CUtensorMap map_c1,
-                const Epi ep) {
-    using S = Smem<BN, STAGES, EW>;
+                const __grid_constant__ CUtensorMap map_mask, const __grid_constant__ CUtensorMap map_shi,
+                const __grid_constant__ CUtensorMap map_slo, const Epi ep) {
+    static_assert(!MT || (BN == 64 && EW == 8), "mask-TMA variant: BN 64, 8 epilogue warps");
+    using S = Smem<BN, STAGES, EW, MT>;
     constexpr int kEpiWarps = EW;
     constexpr uint32_t kStgBytes = kStgBytesFor(EW);
     constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     float* epi_stage = reinterpret_cast<float*>(smem + STAGES * S::kStage);  // store transposes
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage + S::kStaging);
+    float* mask_s = reinterpret_cast<float*>(smem + STAGES * S::kStage + S::kStaging);  // MT: [2] tiles
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage + S::kStaging + S::kMask);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2]
     uint64_t* tempty = tfull + 2;      // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* mfull = tempty + 2;      // [2] mask tile landed (MT)
+    uint64_t* mempty = mfull + 2;      // [2] mask tile consumed (MT)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -258,6 +279,8 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
+            mbar_init(&mfull[a], 1);
+            mbar_init(&mempty[a], kEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -270,6 +293,11 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
         if (ep.tma_store) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_c0)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_c1)) : "memory");
+        }
+        if constexpr (MT) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_mask)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_shi)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_slo)) : "memory");
         }
     }
     if (warp == 2) {
@@ -293,11 +321,19 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer ----------------
-            uint32_t it = 0;
-            for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+            uint32_t it = 0, tl = 0;
+            for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
                 uint32_t mt, nt, z;
                 tile_coords(t, mt, nt, z);
                 const uint32_t kb0 = z * per, kb1 = min(ep.kblocks, kb0 + per);
+                if constexpr (MT) {  // the tile's mask, ahead of its operands
+                    const uint32_t mb = tl & 1;
+                    mbar_wait(&mempty[mb], ((tl >> 1) & 1) ^ 1);
+                    mbar_expect_tx(&mfull[mb], kMaskTile);
+                    float* dst = mask_s + mb * (kMaskTile / 4);
+                    tma_load_2d(dst, &map_mask, &mfull[mb], 0, static_cast<int32_t>(mt * BM));
+                    tma_load_2d(dst + BM * 32, &map_mask, &mfull[mb], 32, static_cast<int32_t>(mt * BM));
+                }
                 for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -358,7 +394,7 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
         constexpr int kCols = BN / (kEpiWarps / 4);       // columns per epilogue warp
         constexpr int kChunk = kCols < 32 ? kCols : 32;   // columns per TMEM load
         const uint32_t col_base = (warp - 2) / 4 * kCols;  // which part of the tile
-        float* wstage = epi_stage + (warp - 2) * kStgWarpFloats;
+        float* wstage = epi_stage + (warp - 2) * (MT ? kMtWarpBytes / 4 : kStgWarpFloats);
         uint32_t sbuf = 0;  // TMA store buffer toggle
         uint32_t tl = 0;
         for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
@@ -371,6 +407,90 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
             const uint32_t row = mt * BM + lane_base + lane;
             const bool row_ok = row < ep.m;
             const float rs = (row_ok && ep.row_scale && ep.split_k <= 1) ? ep.row_scale[row] : 1.f;
+            if constexpr (MT) {
+                // 32 columns per warp: one TMEM load, two 16-column store groups
+                uint32_t raw[32];
+                tmem_ld32_nowait(tmem + (lane_base << 16) + acc * BN + col_base, raw);
+                mbar_wait(&mfull[acc], (tl >> 1) & 1);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const uint32_t rl = lane_base + lane;  // tile-local row
+                const float* mrow = mask_s + acc * (kMaskTile / 4) + (col_base >> 5) * (BM * 32) + rl * 32;
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {  // 128B swizzle: 16-byte chunk ^= row & 7
+                    const float4 q = *reinterpret_cast<const float4*>(mrow + (((j >> 2) ^ (rl & 7)) << 2));
+                    v[j] = q.x > 0.f ? __uint_as_float(raw[j]) : 0.f;
+                    v[j + 1] = q.y > 0.f ? __uint_as_float(raw[j + 1]) : 0.f;
+                    v[j + 2] = q.z > 0.f ? __uint_as_float(raw[j + 2]) : 0.f;
+                    v[j + 3] = q.w > 0.f ? __uint_as_float(raw[j + 3]) : 0.f;
+                }
+                // TMEM and the mask tile are consumed: release both
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&tempty[acc]);
+                    mbar_arrive(&mempty[acc]);
+                }
+#pragma unroll
+                for (int h = 0; h < 32; h += 16) {
+                    const int32_t col0 = static_cast<int32_t>(col_base + h);
+                    uint8_t* buf = reinterpret_cast<uint8_t*>(wstage) + sbuf * 4096;
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
+                    const float* vv = v + h;
+                    if (ep.out_hi) {
+                        const uint32_t sw = (lane >> 2) & 1;  // SWIZZLE_32B: chunk ^= row bit 2
+                        float sv[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            sv[j] = ep.split_unscaled ? vv[j] : vv[j] * rs;
+                            if (!ep.split_unscaled && ep.relu) sv[j] = fmaxf(sv[j], 0.f);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            uint32_t hw[4], lw[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                uint16_t h0, l0, h1, l1;
+                                split_bf16(sv[8 * c + 2 * j], h0, l0);
+                                split_bf16(sv[8 * c + 2 * j + 1], h1, l1);
+                                hw[j] = static_cast<uint32_t>(h0) | (static_cast<uint32_t>(h1) << 16);
+                                lw[j] = static_cast<uint32_t>(l0) | (static_cast<uint32_t>(l1) << 16);
+                            }
+                            const uint32_t off = lane * 32 + ((c ^ sw) << 4);
+                            *reinterpret_cast<uint4*>(buf + 2048 + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                            *reinterpret_cast<uint4*>(buf + 3072 + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                        }
+                    }
+                    const uint32_t sw = (lane >> 1) & 3;  // SWIZZLE_64B
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        float4 o;
+                        o.x = vv[4 * j] * rs;
+                        o.y = vv[4 * j + 1] * rs;
+                        o.z = vv[4 * j + 2] * rs;
+                        o.w = vv[4 * j + 3] * rs;
+                        if (ep.relu) {
+                            o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f);
+                            o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+                        }
+                        *reinterpret_cast<float4*>(buf + lane * 64 + ((j ^ sw) << 4)) = o;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int32_t r0 = static_cast<int32_t>(mt * BM + lane_base);
+                        if (ep.c0) tma_store_2d_nc(&map_c0, buf, col0, r0);
+                        if (ep.out_hi) {
+                            tma_store_2d_nc(&map_shi, buf + 2048, col0, r0);
+                            tma_store_2d_nc(&map_slo, buf + 3072, col0, r0);
+                        }
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    sbuf ^= 1;
+                }
+                continue;
+            }
 #pragma unroll 1
             for (int cb = 0; cb < kCols; cb += kChunk) {
                 uint32_t raw[32];
@@ -538,7 +658,7 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        if (ep.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if ((MT || ep.tma_store) && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -615,15 +735,21 @@ int make_map(CUtensorMap* map, const uint16_t* base, uint64_t inner, uint64_t ou
 
 // fp32 output map for the TMA-store epilogue: (cols inner, rows outer), box {16, 32},
 // 64-byte rows swizzled as the epilogue writes them.
-int make_out_map(CUtensorMap* map, float* base, uint64_t cols, uint64_t rows, uint64_t ld) {
+int make_out_map(CUtensorMap* map, void* base, uint64_t cols, uint64_t rows, uint64_t ld,
+                 bool u16 = false, uint32_t box_cols = 16, uint32_t box_rows = 32) {
     auto fn = encode_fn();
     GDX_REQUIRE(fn != nullptr, GDX_INTERNAL, "cuTensorMapEncodeTiled unavailable");
+    const uint32_t esz = u16 ? 2 : 4;
     cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {ld * 4};
-    cuuint32_t box[2] = {16u, 32u};
+    cuuint64_t strides[1] = {ld * esz};
+    cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+    const uint32_t row_bytes = box_cols * esz;
+    const CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                    : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r = fn(map, u16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     GDX_REQUIRE(r == CUDA_SUCCESS, GDX_INTERNAL,
                 "cuTensorMapEncodeTiled (output) failed (" + std::to_string(static_cast<int>(r)) + ")");
@@ -651,17 +777,26 @@ int operand_maps(CUtensorMap* hi, CUtensorMap* lo, const uint16_t* phi, const ui
     return make_map(lo, plo, rows, k, ld, BK);
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, int EW>
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EW, bool MT = false>
 int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
     int rc;
     if ((rc = operand_maps(&ma_hi, &ma_lo, g->a_hi, g->a_lo, g->m, g->k, g->lda, A_MN, BM))) return rc;
     if ((rc = operand_maps(&mb_hi, &mb_lo, g->b_hi, g->b_lo, g->n, g->k, g->ldb, B_MN, BN))) return rc;
     // TMA-store epilogue for the staged fp32 outputs (16-byte aligned bases, pitch % 4)
-    CUtensorMap mc0{}, mc1{};
+    CUtensorMap mc0{}, mc1{}, mmask{}, mshi{}, mslo{};
     Epi e = ep;
     e.tma_store = 0;
-    if (kStgBytesFor(EW) && ep.stage_stores && ep.split_k <= 1 && tma_store_enabled()) {
+    if constexpr (MT) {  // gdx_gemm_tn checked the shapes and alignments (mask_tma_ok)
+        if (ep.c0 && (rc = make_out_map(&mc0, ep.c0, ep.n, ep.m, ep.ldc0))) return rc;
+        if ((rc = make_out_map(&mmask, const_cast<float*>(ep.mask), ep.n, ep.m, ep.ld_mask, false, 32, BM)))
+            return rc;
+        if (ep.out_hi) {
+            if ((rc = make_out_map(&mshi, ep.out_hi, ep.n, ep.m, ep.ld_split, true))) return rc;
+            if ((rc = make_out_map(&mslo, ep.out_lo, ep.n, ep.m, ep.ld_split, true))) return rc;
+        }
+        e.tma_store = ep.c0 != nullptr;
+    } else if (kStgBytesFor(EW) && ep.stage_stores && ep.split_k <= 1 && tma_store_enabled()) {
         const bool ok0 = !ep.c0 || (ep.split >= 16 && ep.ldc0 % 4 == 0 &&
                                     (reinterpret_cast<uintptr_t>(ep.c0) & 15) == 0);
         const bool ok1 = !ep.c1 || ep.split >= ep.n ||
@@ -673,13 +808,13 @@ int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
             e.tma_store = 1;
         }
     }
-    auto kern = gemm_bf16x3<BN, STAGES, A_MN, B_MN, EW>;
-    const int bytes = Smem<BN, STAGES, EW>::kBytes;
+    auto kern = gemm_bf16x3<BN, STAGES, A_MN, B_MN, EW, MT>;
+    const int bytes = Smem<BN, STAGES, EW, MT>::kBytes;
     if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), bytes))) return rc;
     const uint64_t sms = static_cast<uint64_t>(device_sms());
     const uint64_t tiles = static_cast<uint64_t>(ep.m_tiles) * ep.n_tiles * ep.split_k;
     const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
-    kern<<<grid, kThreadsFor(EW), bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, mc0, mc1, e);
+    kern<<<grid, kThreadsFor(EW), bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, mc0, mc1, mmask, mshi, mslo, e);
     note_launch();
     return check_launch("gdx_gemm_tn");
 }
@@ -708,6 +843,21 @@ int launch_majors(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     return launch_majors_ew<BN, STAGES, 8>(g, ep, s);
 }
 
+// The fused ReLU-backward GEMM with the mask tile TMA-loaded and all outputs TMA-stored:
+// n == 64 (one column tile), K-major A x MN-major B, a single fp32 output, no peer
+// copies or split-K, 16-byte aligned bases and pitches. GDX_MASK_TMA=0 disables.
+bool mask_tma_ok(const gdx_gemm_args* g, const Epi& ep) {
+    static const bool on = [] {
+        const char* e = std::getenv("GDX_MASK_TMA");
+        return !(e && e[0] == '0');
+    }();
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return on && g->mask && g->n == 64 && g->k > 0 && !g->a_mn_major && g->b_mn_major && ep.split_k <= 1 &&
+           g->npeers == 0 && ep.split >= g->n && !g->c1 && (!g->c0 || (al(g->c0) && g->ldc0 % 4 == 0)) &&
+           al(g->mask) && g->ld_mask % 4 == 0 &&
+           (!g->out_hi || (al(g->out_hi) && al(g->out_lo) && g->ld_split % 8 == 0));
+}
+
 int validate(const gdx_gemm_args* g) {
     GDX_REQUIRE(g != nullptr, GDX_INPUT, "gdx_gemm_tn: null args");
     GDX_REQUIRE(g->a_hi && g->a_lo && g->b_hi && g->b_lo, GDX_INPUT, "gdx_gemm_tn: null operand");
@@ -725,6 +875,15 @@ int validate(const gdx_gemm_args* g) {
     return GDX_OK;
 }
 
+// GDX_STAGE_MIN_ROWS overrides the row count from which the staged epilogue is used
+uint32_t stage_min_rows() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("GDX_STAGE_MIN_ROWS");
+        return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : (1u << 20);
+    }();
+    return v;
+}
+
 Epi make_epi(const gdx_gemm_args* g, int bn) {
     Epi ep{g->m, g->n, g->c0, g->ldc0, g->c1, g->ldc1, g->split, g->row_scale, g->relu,
            g->out_hi, g->out_lo, g->ld_split, g->split_k ? g->split_k : 1,
@@ -732,7 +891,7 @@ Epi make_epi(const gdx_gemm_args* g, int bn) {
            g->mask, g->ld_mask, g->split_unscaled, g->npeers, g->peer_target, {},
            // measured (tools/gemm_bench.py): the transposed stores win on long
            // write-bound GEMMs (6 M rows: 1.2-1.25x) and lose on short ones (233 K rows)
-           g->m >= (1u << 20) ? 1 : 0, 0};
+           g->m >= stage_min_rows() ? 1 : 0, 0};
     for (int r = 0; r < 7; ++r) ep.peer_delta[r] = g->peer_delta[r];
     return ep;
 }
@@ -750,6 +909,7 @@ extern "C" int gdx_gemm_tn(const gdx_gemm_args* g, gdx_stream stream) {
     GDX_REQUIRE(ep.split_k <= ep.kblocks || g->k == 0, GDX_INPUT,
                 "gdx_gemm_tn: split_k exceeds the number of 64-wide k blocks");
     cudaStream_t s = as_cuda(stream);
+    if (bn == 64 && mask_tma_ok(g, ep)) return launch_tc<64, 2, false, true, 8, true>(g, ep, s);
     if (bn == 64) return launch_majors<64, 4>(g, ep, s);
     if (bn == 128) return launch_majors<128, 3>(g, ep, s);
     return launch_majors<256, 2>(g, ep, s);

@@ -199,10 +199,13 @@ def test_labels_bit_exact(cuda):
     assert np.array_equal(out.cpu().numpy(), O.make_labels(5000, 41, 11))
 
 
-@pytest.mark.parametrize("m", [517, 1_100_003])
-def test_gemm_mask_epilogue_fused_backward(gdx, cuda, m):
-    """dH GEMM epilogue of the trainer: ReLU-backward mask, unscaled split copy, row scale
-    (m >= 1M takes the smem-staged, row-contiguous epilogue)."""
+@pytest.mark.parametrize("m,mask_ld,unscaled", [(517, 64, True), (1_100_003, 64, True), (1_100_003, 64, False),
+                                                 (517, 65, True), (1_100_003, 65, True)])
+def test_gemm_mask_epilogue_fused_backward(gdx, cuda, m, mask_ld, unscaled):
+    """dH GEMM epilogue of the trainer: ReLU-backward mask, split copy (unscaled or scaled),
+    row scale. A 16-byte mask pitch takes the TMA variant (mask tile TMA-loaded, c0 and
+    the split copy TMA-stored); pitch 65 the register epilogue (EW 16, or the staged
+    EW 8 form at >= 4 M rows)."""
     import torch
     rng = np.random.default_rng(11)
     n, k = 64, 96
@@ -213,14 +216,16 @@ def test_gemm_mask_epilogue_fused_backward(gdx, cuda, m):
     A, B = _split(gdx, g, cuda), _split(gdx, w, cuda)
     out = gdx.dense(m, n, cuda)
     sp = gdx.Split(m, n, cuda)
-    gdx.gemm_tn(A, B, c0=out, b_mn=True, mask=torch.from_numpy(mask).to(cuda),
-                row_scale=torch.from_numpy(scale).to(cuda), out_split=sp, split_unscaled=True)
+    mk = torch.zeros((m, mask_ld), dtype=torch.float32, device=cuda)
+    mk[:, :n] = torch.from_numpy(mask).to(cuda)
+    gdx.gemm_tn(A, B, c0=out, b_mn=True, mask=mk[:, :n],
+                row_scale=torch.from_numpy(scale).to(cuda), out_split=sp, split_unscaled=unscaled)
     torch.cuda.synchronize()
     rows = np.unique(np.concatenate([rng.integers(0, m, 4000), np.arange(max(0, m - 300), m)]))
     dh = g[rows].astype(np.float32).astype(np.float64) @ w.astype(np.float32).astype(np.float64)
     gref = np.where(mask[rows] > 0, dh, 0.0)
     ri = torch.from_numpy(rows).to(cuda)
-    close(sp.to_float()[ri].double().cpu().numpy(), gref)
+    close(sp.to_float()[ri].double().cpu().numpy(), gref if unscaled else gref * scale[rows, None])
     close(out[ri, :n].double().cpu().numpy(), gref * scale[rows, None])
 
 
