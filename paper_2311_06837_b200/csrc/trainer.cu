@@ -199,10 +199,11 @@ uint32_t agg_width(uint32_t fout, uint64_t rows) {
     if (rows * w8 * 4 <= kL2Resident) return static_cast<uint32_t>(w8);
     return fout <= 32 ? 32u : static_cast<uint32_t>((w8 + 31) / 32 * 32);
 }
-// Kernel per CSR shape (train.agg_variant): half-width row groups below degree 20, row
-// groups for 48-wide rows, warp per row otherwise.
+// Kernel per CSR shape (train.agg_variant): row groups (predicated tail) below degree 7,
+// half-width row groups below 20, row groups for 48-wide rows, warp per row otherwise.
 int agg_variant(uint32_t width, uint64_t nnz, uint64_t rows) {
     const double deg = rows ? static_cast<double>(nnz) / static_cast<double>(rows) : 0.0;
+    if (rows && deg < 7.0) return GDX_AGG_ROWS;
     if (rows && deg < 20.0) return GDX_AGG_ROWS2;
     return pad4(width) == 48 ? GDX_AGG_ROWS : 0;
 }
