@@ -202,6 +202,13 @@ typedef struct gdx_gemm_args {
     uint32_t npeers;
     int peer_target;
     int64_t peer_delta[7];
+    /* Row gather (the cooperative batch's feature LOAD fused into its GEMMs, TMA
+     * tile::gather4): nullable. a_rows [m]: row i of a K-major A is row a_rows[i] of a
+     * source with a_src_rows rows (pitch lda); b_rows [k]: k-row i of an MN-major B is
+     * row b_rows[i] of a source with b_src_rows rows (pitch ldb). Same results as
+     * gdx_gather_split_rows followed by the plain GEMM. */
+    const uint32_t* a_rows; uint64_t a_src_rows;
+    const uint32_t* b_rows; uint64_t b_src_rows;
 } gdx_gemm_args;
 int gdx_gemm_tn(const gdx_gemm_args* g, gdx_stream stream);
 /* Reference-precision SIMT fallback of the same contract, for tests only. */

@@ -48,6 +48,7 @@ class GemmArgs(C.Structure):
         ("ld_split", u64), ("split_k", u32), ("mask", vp), ("ld_mask", u64),
         ("split_unscaled", C.c_int), ("npeers", u32), ("peer_target", C.c_int),
         ("peer_delta", C.c_int64 * 7),
+        ("a_rows", vp), ("a_src_rows", u64), ("b_rows", vp), ("b_src_rows", u64),
     ]
 
 

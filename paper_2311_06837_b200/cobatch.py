@@ -260,6 +260,11 @@ class CobatchTrainer(FullGraphTrainer):
         self.Xsp = Split(self.nloc, F, d)
         self.labels = torch.zeros(self.nloc, dtype=torch.int32, device=d)
         self._init_model(xmode, use_p2p, weights, weight_seed)
+        # fused LOAD (GDX_FUSED_LOAD=1): measured slower on a papers-shape epoch (4.27 s vs
+        # 4.17 s with the separate 6 TB/s gather pass; the gathered 128-byte half-rows cost
+        # the two layer-0 GEMMs more than the pass), so off by default
+        self._fused_load = (os.environ.get("GDX_FUSED_LOAD", "0") == "1"
+                            and not getattr(self.layers[0], "agg_first", False))
         self.epoch_loss = torch.zeros(1, dtype=torch.float64, device=d)
         self.total_targets = sum(len(b.target_vertices) for b in plan.batches)
         self.current = None
@@ -299,10 +304,16 @@ class CobatchTrainer(FullGraphTrainer):
         self.send_rows = geo.send_rows
         self.exchange = RowExchange(np.arange(self.world + 1, dtype=np.int64) * geo.block,
                                     self.rank, self.world, self.pg)
-        # LOAD: input rows of this rank's block from the resident store
-        call("gdx_gather_split_rows", self.Xall.hi.data_ptr(), self.Xall.lo.data_ptr(), self.Xall.ld,
-             geo.l2g.data_ptr(), geo.nloc, self.F, self.Xsp.hi.data_ptr(), self.Xsp.lo.data_ptr(),
-             self.Xsp.ld, stream_handle())
+        # LOAD: input rows of this rank's block from the resident store (gdx_gather_split_rows),
+        # or, with GDX_FUSED_LOAD=1, read by the layer-0 forward and dW GEMMs themselves
+        # (TMA gather4 through geo.l2g)
+        if self._fused_load and geo.nloc:
+            self._xg = geo.l2g[:geo.nloc]
+        else:
+            self._xg = None
+            call("gdx_gather_split_rows", self.Xall.hi.data_ptr(), self.Xall.lo.data_ptr(), self.Xall.ld,
+                 geo.l2g.data_ptr(), geo.nloc, self.F, self.Xsp.hi.data_ptr(), self.Xsp.lo.data_ptr(),
+                 self.Xsp.ld, stream_handle())
         if geo.nloc:   # labels of the batch rows: 4-byte rows moved bit for bit
             call("gdx_gather_rows", self.labels_all.data_ptr(), 1, geo.l2g.data_ptr(), geo.nloc, 1,
                  self.labels.data_ptr(), 1, stream_handle())

@@ -171,7 +171,30 @@ struct Epi {
     int64_t peer_delta[7];
     int stage_stores;       // row-contiguous (smem-transposed) fp32 stores
     int tma_store;          // ... leaving smem through TMA bulk tensor stores (map_c0 / map_c1)
+    const uint32_t* a_rows; // row gather of a K-major A (m index) / an MN-major B (k index):
+    const uint32_t* b_rows; // TMA gather4, 4 source rows per instruction
+    uint32_t k;
 };
+
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c_inner,
+                                            const uint4& rows) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c_inner), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
+// four consecutive entries of a row index (out of range -> 0xFFFFFFFF: TMA zero-fills)
+__device__ __forceinline__ uint4 gather_rows4(const uint32_t* idx, uint32_t r0, uint32_t count) {
+    uint4 v;
+    v.x = r0 < count ? __ldg(idx + r0) : 0xFFFFFFFFu;
+    v.y = r0 + 1 < count ? __ldg(idx + r0 + 1) : 0xFFFFFFFFu;
+    v.z = r0 + 2 < count ? __ldg(idx + r0 + 2) : 0xFFFFFFFFu;
+    v.w = r0 + 3 < count ? __ldg(idx + r0 + 3) : 0xFFFFFFFFu;
+    return v;
+}
 
 // Store transpose buffers, 4 KB per epilogue warp (32 KB at EW = 8):
 //  * TMA stores: two 32 rows x 16 fp32 boxes (2 KB each, 64-byte rows in the SWIZZLE_64B
@@ -318,7 +341,55 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
         mt = mn / ep.n_tiles;
     };
 
-    if (warp == 0) {
+    const bool gather_a = !A_MN && ep.a_rows != nullptr;
+    const bool gather_b = B_MN && ep.b_rows != nullptr;
+    if (warp == 0 && (gather_a || gather_b)) {
+        // ---------------- TMA producer, gathered operand(s): the whole warp ----------------
+        // Lane l gathers A rows 4l..4l+3 of the tile (K-major A: 32 x gather4 = 128 rows)
+        // and B k-rows 4(l & 15).. of 64-wide column block l >> 4 (MN-major B), so one
+        // k block's gathers go out from 32 lanes at once. Lane 0 waits/arms the barrier.
+        uint32_t it = 0;
+        for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+            uint32_t mt, nt, z;
+            tile_coords(t, mt, nt, z);
+            const uint32_t kb0 = z * per, kb1 = min(ep.kblocks, kb0 + per);
+            uint4 ia = make_uint4(0, 0, 0, 0);
+            if (gather_a) ia = gather_rows4(ep.a_rows, mt * BM + 4 * lane, ep.m);
+            for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
+                const int s = it % STAGES;
+                uint8_t* st = smem + s * S::kStage;
+                const int32_t kc = static_cast<int32_t>(kb * BK);
+                uint4 ib = make_uint4(0, 0, 0, 0);
+                if (gather_b) ib = gather_rows4(ep.b_rows, kb * BK + 4 * (lane & 15), ep.k);
+                if (lane == 0) {
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    mbar_expect_tx(&full[s], S::kStage);
+                }
+                __syncwarp();
+                if (gather_a) {
+                    tma_gather4(st + lane * 512, &map_ahi, &full[s], kc, ia);
+                    tma_gather4(st + S::kA + lane * 512, &map_alo, &full[s], kc, ia);
+                } else if (lane == 0) {
+                    load_operand<BM, A_MN>(st, &map_ahi, &full[s], static_cast<int32_t>(mt * BM), kc);
+                    load_operand<BM, A_MN>(st + S::kA, &map_alo, &full[s], static_cast<int32_t>(mt * BM), kc);
+                }
+                if (gather_b) {
+#pragma unroll
+                    for (int blk = lane >> 4; blk < BN / 64; blk += 2) {
+                        const uint32_t off = blk * (64 * BK * 2) + (lane & 15) * 512;
+                        const int32_t nc = static_cast<int32_t>(nt * BN + 64 * blk);
+                        tma_gather4(st + 2 * S::kA + off, &map_bhi, &full[s], nc, ib);
+                        tma_gather4(st + 2 * S::kA + S::kB + off, &map_blo, &full[s], nc, ib);
+                    }
+                } else if (lane == 0) {
+                    load_operand<BN, B_MN>(st + 2 * S::kA, &map_bhi, &full[s], static_cast<int32_t>(nt * BN), kc);
+                    load_operand<BN, B_MN>(st + 2 * S::kA + S::kB, &map_blo, &full[s],
+                                           static_cast<int32_t>(nt * BN), kc);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer ----------------
             uint32_t it = 0, tl = 0;
@@ -675,9 +746,11 @@ __global__ void gemm_simt_kernel(const uint16_t* a_hi, const uint16_t* a_lo, uin
     const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= ep.m || col >= ep.n) return;
     float acc = 0.f;
+    const uint64_t arow = ep.a_rows ? ep.a_rows[row] : row;  // gathered K-major A
     for (uint32_t i = 0; i < k; ++i) {
-        const uint64_t ia = a_mn ? static_cast<uint64_t>(i) * lda + row : static_cast<uint64_t>(row) * lda + i;
-        const uint64_t ib = b_mn ? static_cast<uint64_t>(i) * ldb + col : static_cast<uint64_t>(col) * ldb + i;
+        const uint64_t ki = ep.b_rows ? ep.b_rows[i] : i;        // gathered MN-major B
+        const uint64_t ia = a_mn ? static_cast<uint64_t>(i) * lda + row : arow * lda + i;
+        const uint64_t ib = b_mn ? ki * ldb + col : static_cast<uint64_t>(col) * ldb + i;
         const float a = bf2f(a_hi[ia]) + bf2f(a_lo[ia]);
         const float b = bf2f(b_hi[ib]) + bf2f(b_lo[ib]);
         acc = fmaf(a, b, acc);
@@ -781,8 +854,20 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EW, bool MT = false>
 int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
     int rc;
-    if ((rc = operand_maps(&ma_hi, &ma_lo, g->a_hi, g->a_lo, g->m, g->k, g->lda, A_MN, BM))) return rc;
-    if ((rc = operand_maps(&mb_hi, &mb_lo, g->b_hi, g->b_lo, g->n, g->k, g->ldb, B_MN, BN))) return rc;
+    // gathered operands: maps over the whole source (k inner for A, n inner for B), one
+    // row per box -- the tile::gather4 form (tools/probe/gather4_probe.cu)
+    if (g->a_rows) {
+        if ((rc = make_map(&ma_hi, g->a_hi, g->k, g->a_src_rows, g->lda, 1))) return rc;
+        if ((rc = make_map(&ma_lo, g->a_lo, g->k, g->a_src_rows, g->lda, 1))) return rc;
+    } else if ((rc = operand_maps(&ma_hi, &ma_lo, g->a_hi, g->a_lo, g->m, g->k, g->lda, A_MN, BM))) {
+        return rc;
+    }
+    if (g->b_rows) {
+        if ((rc = make_map(&mb_hi, g->b_hi, g->n, g->b_src_rows, g->ldb, 1))) return rc;
+        if ((rc = make_map(&mb_lo, g->b_lo, g->n, g->b_src_rows, g->ldb, 1))) return rc;
+    } else if ((rc = operand_maps(&mb_hi, &mb_lo, g->b_hi, g->b_lo, g->n, g->k, g->ldb, B_MN, BN))) {
+        return rc;
+    }
     // TMA-store epilogue for the staged fp32 outputs (16-byte aligned bases, pitch % 4)
     CUtensorMap mc0{}, mc1{}, mmask{}, mshi{}, mslo{};
     Epi e = ep;
@@ -852,7 +937,7 @@ bool mask_tma_ok(const gdx_gemm_args* g, const Epi& ep) {
         return !(e && e[0] == '0');
     }();
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    return on && g->mask && g->n == 64 && g->k > 0 && !g->a_mn_major && g->b_mn_major && ep.split_k <= 1 &&
+    return on && g->mask && !g->a_rows && !g->b_rows && g->n == 64 && g->k > 0 && !g->a_mn_major && g->b_mn_major && ep.split_k <= 1 &&
            g->npeers == 0 && ep.split >= g->n && !g->c1 && (!g->c0 || (al(g->c0) && g->ldc0 % 4 == 0)) &&
            al(g->mask) && g->ld_mask % 4 == 0 &&
            (!g->out_hi || (al(g->out_hi) && al(g->out_lo) && g->ld_split % 8 == 0));
@@ -872,6 +957,10 @@ int validate(const gdx_gemm_args* g) {
     GDX_REQUIRE(!g->mask || g->ld_mask >= g->n, GDX_INPUT, "gdx_gemm_tn: ld_mask < n");
     GDX_REQUIRE(g->npeers <= 7, GDX_INPUT, "gdx_gemm_tn: at most 7 peers");
     GDX_REQUIRE(g->npeers == 0 || g->split_k <= 1, GDX_INPUT, "gdx_gemm_tn: peers with split_k");
+    GDX_REQUIRE(!g->a_rows || (!g->a_mn_major && g->a_src_rows > 0 && g->a_src_rows < (1ull << 31)), GDX_INPUT,
+                "gdx_gemm_tn: a_rows gathers a K-major A from a_src_rows (< 2^31) source rows");
+    GDX_REQUIRE(!g->b_rows || (g->b_mn_major && g->b_src_rows > 0 && g->b_src_rows < (1ull << 31)), GDX_INPUT,
+                "gdx_gemm_tn: b_rows gathers an MN-major B from b_src_rows (< 2^31) source rows");
     return GDX_OK;
 }
 
@@ -891,7 +980,7 @@ Epi make_epi(const gdx_gemm_args* g, int bn) {
            g->mask, g->ld_mask, g->split_unscaled, g->npeers, g->peer_target, {},
            // measured (tools/gemm_bench.py): the transposed stores win on long
            // write-bound GEMMs (6 M rows: 1.2-1.25x) and lose on short ones (233 K rows)
-           g->m >= stage_min_rows() ? 1 : 0, 0};
+           g->m >= stage_min_rows() ? 1 : 0, 0, g->a_rows, g->b_rows, g->k};
     for (int r = 0; r < 7; ++r) ep.peer_delta[r] = g->peer_delta[r];
     return ep;
 }

@@ -161,11 +161,18 @@ class RowBins:
 
 def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None, relu=False,
             out_split: Split | None = None, split_k: int = 1, m=None, simt=False, a_mn=False,
-            b_mn=False, mask=None, split_unscaled=False, peers=None, stream=None):
+            b_mn=False, mask=None, split_unscaled=False, peers=None, stream=None, a_rows=None,
+            b_rows=None):
     """K2: C(m, n) = sum_k A(m, k) B(n, k).  A is stored [m][k] (K-major) or, with
-    a_mn, [k][m]; likewise B ([n][k] or [k][n]).  See gdx_gemm_tn."""
+    a_mn, [k][m]; likewise B ([n][k] or [k][n]).  a_rows / b_rows (int32 device
+    tensors): A / B are the SOURCE matrices and the operand's rows (m for a K-major A,
+    k for an MN-major B) are gathered through the index.  See gdx_gemm_tn."""
     mA, kA = (A.cols, A.rows) if a_mn else (A.rows, A.cols)
     nB, kB = (B.cols, B.rows) if b_mn else (B.rows, B.cols)
+    if a_rows is not None:
+        mA = a_rows.numel()
+    if b_rows is not None:
+        kB = b_rows.numel()
     assert kA == kB, (kA, kB)
     g = GemmArgs()
     g.a_hi, g.a_lo, g.lda = A.hi.data_ptr(), A.lo.data_ptr(), A.ld
@@ -190,6 +197,10 @@ def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None,
     if mask is not None:
         g.mask, g.ld_mask = mask.data_ptr(), mask.stride(0)
     g.split_unscaled = int(split_unscaled)
+    if a_rows is not None:
+        g.a_rows, g.a_src_rows = a_rows.data_ptr(), A.rows
+    if b_rows is not None:
+        g.b_rows, g.b_src_rows = b_rows.data_ptr(), B.rows
     if peers is not None:  # (target output, byte deltas): fused NVLink exchange
         target, deltas = peers
         g.npeers, g.peer_target = len(deltas), int(target)

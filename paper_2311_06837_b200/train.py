@@ -564,9 +564,16 @@ class FullGraphTrainer:
             dist.all_reduce(t, group=self.pg)
 
     # ---- one epoch ----
+    def _x_operand(self):
+        """Layer 0's input rows as a GEMM operand: the local split copy, or (cooperative
+        batches with the fused LOAD) the resident store plus the batch's row index, read
+        by the GEMMs through TMA gather4 -- (split, gather index or None)."""
+        xg = getattr(self, "_xg", None)
+        return (self.Xsp, None) if xg is None else (self.Xall, xg)
+
     def forward(self):
         cfg = self.cfg
-        A = self.Xsp
+        A, xg = self._x_operand()
         acts = []
         for l, L in enumerate(self.layers):
             relu = l + 1 < cfg.layers
@@ -584,12 +591,13 @@ class FullGraphTrainer:
                 continue
             own = L.Zfull[self.lo:self.hi]
             pe = self._peers(L.z_peers, 1 if cfg.kind == "sage" else 0)
+            gx = dict(a_rows=xg) if l == 0 and xg is not None else {}
             if cfg.kind == "sage":
-                gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w, m=m_in, peers=pe)
+                gemm_tn(A, L.Wsp, c0=L.S, c1=own, split=L.w, m=m_in, peers=pe, **gx)
             elif cfg.kind == "gcn":
-                gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s, m=m_in, peers=pe)
+                gemm_tn(A, L.Wsp, c0=own, row_scale=self.gcn_s, m=m_in, peers=pe, **gx)
             else:
-                gemm_tn(A, L.Wsp, c0=own, m=m_in, peers=pe)
+                gemm_tn(A, L.Wsp, c0=own, m=m_in, peers=pe, **gx)
             self._publish(own, L.z_peers, stored=pe is not None)
             nxt = self.layers[l + 1] if l + 1 < cfg.layers else None
             if getattr(nxt, "agg_first", False):   # output rows feed an aggregate-first layer
@@ -683,13 +691,17 @@ class FullGraphTrainer:
             # dW = G^T H_in, split-K over the local rows; both operands MN-major in place
             # (K = the rows that fed layer l; rows past them carry no gradient)
             A_in = self.Xsp if l == 0 else self.layers[l - 1].Hsp
+            Bop, gx = A_in.rows_view(r_in), {}
+            if l == 0:
+                xs, xg = self._x_operand()
+                if xg is not None:
+                    Bop, gx = xs, dict(b_rows=xg[:r_in])
             sk = _splitk_eff(L.split_k, r_in)
             ws = self._wstream()
             if ws is not None:  # overlap with the next layer's (L2-bound) aggregation
                 ws.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(ws) if ws is not None else _nullctx():
-                gemm_tn(L.G.rows_view(r_in), A_in.rows_view(r_in), c0=L.ws, split_k=sk, a_mn=True,
-                        b_mn=True)
+                gemm_tn(L.G.rows_view(r_in), Bop, c0=L.ws, split_k=sk, a_mn=True, b_mn=True, **gx)
                 self._sgd_or_reduce(L, sk, L.upd_cols)
         if getattr(self, "_ws", None) is not None:
             torch.cuda.current_stream().wait_stream(self._ws)

@@ -159,3 +159,26 @@ def test_cobatch_graph_replay_matches_eager(cuda, kind, out):
     wa = np.concatenate([x.ravel() for x in a.get_weights()])
     wb = np.concatenate([x.ravel() for x in b.get_weights()])
     np.testing.assert_allclose(wb, wa, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("kind", ["sage", "gcn"])
+def test_cobatch_fused_load_matches_gather_pass(cuda, kind, monkeypatch):
+    """GDX_FUSED_LOAD=1 (layer-0 GEMMs read the batch's rows from the resident store
+    through TMA gather4) trains bit for bit like the separate LOAD gather pass."""
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.cobatch import CobatchTrainer
+    from paper_2311_06837_b200.train import ModelConfig, init_weights
+
+    dims = [72, 32, 32, 9]
+    g, hp, plan = _plan(3000, 10.0, 23, 2, 1, 3, 3, G.SamplingConfig(1, 15, 3), dims)
+    cfg = ModelConfig(kind, dims, lr=0.5)
+    w0 = init_weights(cfg, 3)
+    res = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("GDX_FUSED_LOAD", fused)
+        tr = CobatchTrainer(g, cfg, plan, hp.server, hp.gpu, 0, weights=w0)
+        assert tr._fused_load == (fused == "1")
+        losses = [tr.train_epoch() for _ in range(3)]
+        res.append((losses, np.concatenate([x.ravel() for x in tr.get_weights()])))
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1])

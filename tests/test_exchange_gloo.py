@@ -122,7 +122,8 @@ def test_kernel_selection_helpers():
     from paper_2311_06837_b200.train import AGG_ROWS, AGG_ROWS2, _splitk_eff, agg_variant
     assert agg_variant(64, 114_624_474, 232_965) == 0          # Reddit 64-wide: warp per row
     assert agg_variant(48, 114_624_474, 232_965) == AGG_ROWS   # 48-wide rows
-    assert agg_variant(64, 15_600_000, 6_000_000) == AGG_ROWS2  # cobatch: 2.6 edges per row
+    assert agg_variant(64, 15_600_000, 6_000_000) == AGG_ROWS   # cobatch: 2.6 edges per row (predicated tail)
+    assert agg_variant(64, 42_000_000, 6_000_000) == AGG_ROWS2  # degree 7
     assert agg_variant(64, 72_000_000, 6_000_000) == AGG_ROWS2  # degree 12
     for sk, k in [(96, 232965), (296, 100), (7, 64), (5, 0), (300, 6_000_000)]:
         e = _splitk_eff(sk, k)

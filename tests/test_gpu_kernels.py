@@ -253,6 +253,67 @@ def test_gemm_staged_split_outputs(gdx, cuda, relu, split):
     close(sp.to_float()[ri].double().cpu().numpy(), ref)
 
 
+def _gathered_split(gdx, S, idx, cuda):
+    """rows idx of split S as a fresh Split (what gdx_gather_split_rows produces)."""
+    import torch
+    out = gdx.Split(idx.numel(), S.cols, cuda)
+    ii = idx.long()
+    out.hi.view(-1, out.ld)[:idx.numel()] = S.hi.view(-1, S.ld)[ii][:, :out.ld]
+    out.lo.view(-1, out.ld)[:idx.numel()] = S.lo.view(-1, S.ld)[ii][:, :out.ld]
+    return out
+
+
+@pytest.mark.parametrize("m,k,n", [(1000, 128, 128), (517, 100, 64), (300, 64, 256)])
+def test_gemm_gathered_a_rows(gdx, cuda, m, k, n):
+    """TMA gather4 of a K-major A (the cooperative batch's LOAD fused into its forward
+    GEMM): bit-identical to gathering the rows first, c0/c1 split outputs included."""
+    import torch
+    rng = np.random.default_rng(m + k)
+    src_rows = 5000
+    A = _split(gdx, rng.uniform(-1, 1, (src_rows, k)), cuda)
+    B = _split(gdx, rng.uniform(-1, 1, (n, k)), cuda)
+    idx = torch.from_numpy(rng.integers(0, src_rows, m).astype(np.int32)).to(cuda)
+    split = n // 2
+    outs = []
+    for gathered in (True, False):
+        c0, c1 = gdx.dense(m, split, cuda), gdx.dense(m, n - split, cuda)
+        if gathered:
+            gdx.gemm_tn(A, B, c0=c0, c1=c1, split=split, a_rows=idx)
+        else:
+            gdx.gemm_tn(_gathered_split(gdx, A, idx, cuda), B, c0=c0, c1=c1, split=split)
+        outs.append((c0.clone(), c1.clone()))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    c = gdx.dense(m, n, cuda)
+    gdx.gemm_tn(A, B, c0=c, a_rows=idx, simt=True)   # the SIMT reference gathers too
+    close(torch.cat(outs[0], 1).double().cpu().numpy(), c[:, :n].double().cpu().numpy())
+
+
+@pytest.mark.parametrize("kk,n,sk", [(1000, 128, 4), (4099, 64, 8), (200, 256, 1)])
+def test_gemm_gathered_b_rows(gdx, cuda, kk, n, sk):
+    """TMA gather4 of an MN-major B over k (the cooperative batch's dW GEMM reading its
+    input rows from the resident store): bit-identical to gathering first."""
+    import torch
+    rng = np.random.default_rng(kk)
+    src_rows, m = 9000, 64
+    G = _split(gdx, rng.uniform(-1, 1, (kk, m)), cuda)      # [k][m]: MN-major A
+    X = _split(gdx, rng.uniform(-1, 1, (src_rows, n)), cuda)  # source [rows][n]
+    idx = torch.from_numpy(rng.choice(src_rows, kk, replace=False).astype(np.int32)).to(cuda)
+    outs = []
+    for gathered in (True, False):
+        ws = torch.zeros((sk * m, gdx.pad4(n)), dtype=torch.float32, device=cuda)
+        if gathered:
+            gdx.gemm_tn(G, X, c0=ws, split_k=sk, a_mn=True, b_mn=True, b_rows=idx)
+        else:
+            gdx.gemm_tn(G, _gathered_split(gdx, X, idx, cuda), c0=ws, split_k=sk, a_mn=True, b_mn=True)
+        outs.append(ws.clone())
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    tot = outs[0].view(sk, m, -1).sum(0)[:, :n].double().cpu().numpy()
+    xg = X.to_float()[idx.long()].double().cpu().numpy()
+    close(tot, G.to_float().double().cpu().numpy().T @ xg)
+
+
 @pytest.mark.parametrize("width", [64, 30])
 def test_grad_prepare(gdx, cuda, width):
     """g = dH * (H > 0) -> split(g) and gs = g * scale (vector and scalar forms)."""
