@@ -36,11 +36,11 @@ MODEL = "sage"
 # BASELINE.json configs beyond the headline (configs[1]); selected with --config
 CONFIGS = {
     "reddit-sage": dict(n=232965, degree=491.99, seed=11, kind="sage", dims=[602, 64, 64, 41],
-                        mode="full", lr=0.1,
+                        mode="full", lr=0.1, packed24=True,
                         workload="reddit-shape full-graph 3-layer GraphSAGE-mean training epoch "
                                  "(BASELINE configs[1])"),
     "reddit-gcn56-eas": dict(n=232965, degree=491.99, seed=11, kind="gcn", dims=[602] + [64] * 55 + [41],
-                             mode="eas", eas=(1, 15, 3), servers=8, lr=1.0, init="he",
+                             mode="eas", eas=(1, 15, 3), servers=8, lr=1.0, init="he", packed24=True,
                              workload="reddit-shape 56-layer normalised GCN, expansion-aware sampling "
                                       "EAS(m=1,k=15,seed=3) on an 8-server random partition "
                                       "(N_s=8 emulated servers, SURVEY §8d config 3); GPU r trains "
@@ -605,7 +605,12 @@ def main():
         sub = G.extract_sampled(g, part, rank % servers, G.SamplingConfig(m, k, sseed))
     # the C-ABI trainer (csrc/trainer.cu): the whole epoch runs in libgdx's C++
     t0 = time.perf_counter()
-    tr = NativeTrainer(g, cfg, rank=rank, world=world, pg=pg, subgraph=sub, use_graph=not args.eager)
+    # packed-24 gathered rows where the gathered matrix is L2-resident (Reddit shapes);
+    # GDX_PACKED24=0/1 overrides (A/B)
+    p24 = os.environ.get("GDX_PACKED24")
+    packed24 = bool(C.get("packed24")) if p24 is None else p24 == "1"
+    tr = NativeTrainer(g, cfg, rank=rank, world=world, pg=pg, subgraph=sub, use_graph=not args.eager,
+                       packed24=packed24)
     t_setup = time.perf_counter() - t0
     stream = tr.stream()
 
@@ -765,6 +770,9 @@ def main():
             "scaling": "strong" if C["mode"] == "full" else "weak",
             "vs_baseline": None,
             "dtype": "f32 (tcgen05 GEMMs: bf16x3 split, fp32 accumulate)",
+            "gathered_rows": ("packed-24 (fp32 rounded to 24 bits, relative 2^-16 = the split GEMM "
+                              "operands' precision) for the 64-wide Z / dZ rows; fp32 accumulation"
+                              if packed24 else "fp32"),
             "data": DATA[args.config],
             "config": config_block(args, C, world, exchange_label(tr, world)),
             "epoch_ms": round(ms, 3),

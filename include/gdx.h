@@ -118,6 +118,10 @@ typedef struct gdx_aggregate_args {
     uint16_t* out24_hi;
     uint8_t* out24_lo;
     uint64_t ld_out24;
+    /* pitch of the packed-24 source's low plane in bytes (0: ld_src) -- e.g. one
+     * interleaved 3F-byte row per vertex (high plane then low plane), so a block of
+     * rows is one contiguous range (the trainer's exchanged buffers) */
+    uint64_t ld_src_lo8;
 } gdx_aggregate_args;
 /* Degree-binned load balancing for skewed graphs (replaces the reference's uniform
  * per-vertex loop, reference_gnn.cpp:76-83, for hub-heavy inputs): rows with more
@@ -209,6 +213,11 @@ typedef struct gdx_gemm_args {
      * gdx_gather_split_rows followed by the plain GEMM. */
     const uint32_t* a_rows; uint64_t a_src_rows;
     const uint32_t* b_rows; uint64_t b_src_rows;
+    /* Packed-24 output (nullable; the aggregation's packed-24 source format): the columns
+     * of output p24_target (0: c0's [0, split), 1: c1's [split, n)) are stored as the
+     * high-16 plane p24_hi (pitch ld_p24_hi u16) + low-8 plane p24_lo (pitch ld_p24_lo
+     * bytes) instead of fp32; that output's fp32 pointer must be null. */
+    uint16_t* p24_hi; uint8_t* p24_lo; uint64_t ld_p24_hi, ld_p24_lo; int p24_target;
 } gdx_gemm_args;
 int gdx_gemm_tn(const gdx_gemm_args* g, gdx_stream stream);
 /* Reference-precision SIMT fallback of the same contract, for tests only. */
@@ -432,6 +441,10 @@ typedef struct gdx_trainer_config {
                                * (max(4096, 32 x mean degree)), 0xFFFFFFFF: never */
     int fused_exchange;       /* world > 1: 1 = gdx_aggregate_exchange (one kernel per layer
                                * exchange), 0 = push kernel + two passes + wait kernel */
+    int packed24;             /* 1: the gathered Z / dZ rows of 64k-wide transform-first layers
+                               * are stored packed-24 (fp32 rounded to 24 bits, relative 2^-16:
+                               * the GEMM operands' precision) -- 25% fewer gathered bytes on
+                               * L2-resident graphs; off with fused_exchange or heavy rows */
 } gdx_trainer_config;
 typedef struct gdx_trainer_graph {
     uint32_t num_vertices;          /* V of the whole graph */

@@ -28,7 +28,7 @@ class AggregateArgs(C.Structure):
         ("src", vp), ("ld_src", u64), ("self_coef", C.c_float), ("self_base", u64),
         ("post_scale", vp), ("add", vp), ("ld_add", u64), ("relu", C.c_int),
         ("out", vp), ("ld_out", u64), ("out_hi", vp), ("out_lo", vp), ("ld_split", u64),
-        ("src_lo8", vp), ("out24_hi", vp), ("out24_lo", vp), ("ld_out24", u64),
+        ("src_lo8", vp), ("out24_hi", vp), ("out24_lo", vp), ("ld_out24", u64), ("ld_src_lo8", u64),
     ]
 
 
@@ -49,6 +49,7 @@ class GemmArgs(C.Structure):
         ("split_unscaled", C.c_int), ("npeers", u32), ("peer_target", C.c_int),
         ("peer_delta", C.c_int64 * 7),
         ("a_rows", vp), ("a_src_rows", u64), ("b_rows", vp), ("b_src_rows", u64),
+        ("p24_hi", vp), ("p24_lo", vp), ("ld_p24_hi", u64), ("ld_p24_lo", u64), ("p24_target", C.c_int),
     ]
 
 

@@ -104,6 +104,7 @@ struct AggParams {
     uint16_t* out24_hi;       // optional packed-24 copy of the output
     uint8_t* out24_lo;
     uint64_t ld_out24;
+    uint64_t ld_lo8;          // low-plane pitch of a packed-24 source (u8 elements)
 };
 
 constexpr int pow2_floor(int x) { return x >= 32 ? 32 : x >= 16 ? 16 : x >= 8 ? 8 : x >= 4 ? 4 : x >= 2 ? 2 : 1; }
@@ -503,16 +504,8 @@ __global__ void __launch_bounds__(256) aggregate_scalar(const AggParams p, uint3
 // operands that produce and consume it) in two planes: the high 16 bits (u16) and
 // the next 8 bits (u8).  A 64-wide row is then 128 + 64 bytes (6 sectors) instead
 // of 256 (8 sectors): the L2-bound gather moves 25% fewer bytes.  Decoding is three
-// byte permutes per two values; accumulation stays fp32.
-__device__ __forceinline__ void pack24(float x, uint16_t& hi, uint8_t& lo) {
-    uint32_t u = __float_as_uint(x);
-    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x7fu + ((u >> 8) & 1u)) & 0xffffff00u;  // RNE at bit 8
-    hi = static_cast<uint16_t>(u >> 16);
-    lo = static_cast<uint8_t>(u >> 8);
-}
-__device__ __forceinline__ float unpack24(uint16_t hi, uint8_t lo) {
-    return __uint_as_float((static_cast<uint32_t>(hi) << 16) | (static_cast<uint32_t>(lo) << 8));
-}
+// byte permutes per two values; accumulation stays fp32. pack24 / unpack24 are in
+// gdx_common.cuh (the GEMM epilogue writes the format too).
 
 // 8 values from one 16-byte high-plane vector and one 8-byte low-plane vector
 __device__ __forceinline__ void decode8(const uint4 h, const uint2 l, float4& a, float4& b) {
@@ -560,7 +553,7 @@ __device__ __forceinline__ void epilogue8(const AggParams& p, uint32_t row, uint
     if (p.self_coef != 0.f) {
         const uint64_t o = (p.self_base + row) * p.ld_src + c0;
         const uint4 h = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.src) + o));
-        const uint2 l = __ldg(reinterpret_cast<const uint2*>(p.src_lo8 + o));
+        const uint2 l = __ldg(reinterpret_cast<const uint2*>(p.src_lo8 + (p.self_base + row) * p.ld_lo8 + c0));
         float4 a, b;
         decode8(h, l, a, b);
         v[0] += p.self_coef * a.x; v[1] += p.self_coef * a.y; v[2] += p.self_coef * a.z; v[3] += p.self_coef * a.w;
@@ -618,7 +611,7 @@ __global__ void __launch_bounds__(256, MINB) aggregate_p24(const AggParams p) {
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
     const uint64_t hbase = reinterpret_cast<uint64_t>(p.src) + 16 * lin;
     const uint64_t lbase = reinterpret_cast<uint64_t>(p.src_lo8) + 8 * lin;
-    const uint32_t ldh = static_cast<uint32_t>(p.ld_src * 2), ldl = static_cast<uint32_t>(p.ld_src);
+    const uint32_t ldh = static_cast<uint32_t>(p.ld_src * 2), ldl = static_cast<uint32_t>(p.ld_lo8);
     const uint32_t warps_total = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < p.rows; it += warps_total) {
         const uint32_t row = p.row_list ? p.row_list[it] : it;
@@ -702,7 +695,7 @@ __global__ void __launch_bounds__(256, MINB) aggregate_rows_p24(const AggParams 
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
     const uint64_t hbase = reinterpret_cast<uint64_t>(p.src) + 16 * lin;
     const uint64_t lbase = reinterpret_cast<uint64_t>(p.src_lo8) + 8 * lin;
-    const uint32_t ldh = static_cast<uint32_t>(p.ld_src * 2), ldl = static_cast<uint32_t>(p.ld_src);
+    const uint32_t ldh = static_cast<uint32_t>(p.ld_src * 2), ldl = static_cast<uint32_t>(p.ld_lo8);
     const uint64_t groups = static_cast<uint64_t>((gridDim.x * blockDim.x) >> 5) * EPW;
     for (uint64_t r = static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * EPW + sub; r < p.rows;
          r += groups) {
@@ -1125,7 +1118,8 @@ int aggregate_impl(const gdx_aggregate_args* a, int variant, gdx_stream stream) 
                 a->rows, a->width / 4, a->src, a->ld_src,
                 static_cast<uint32_t>(a->ld_src * 4), a->self_coef, a->self_base, a->post_scale,
                 a->add, a->ld_add, a->relu, a->out, a->ld_out, a->out_hi, a->out_lo, a->ld_split,
-                nullptr, a->src_lo8, a->out24_hi, a->out24_lo, a->ld_out24};
+                nullptr, a->src_lo8, a->out24_hi, a->out24_lo, a->ld_out24,
+                a->ld_src_lo8 ? a->ld_src_lo8 : a->ld_src};
     if (a->src_lo8 || a->out24_hi) {
         // packed-24 rows: widths in whole 8-value groups (8..256, 48 included), 16-byte rows
         GDX_REQUIRE(!a->out24_hi == !a->out24_lo, GDX_INPUT, "gdx_aggregate: out24_hi/out24_lo must pair");
@@ -1133,6 +1127,7 @@ int aggregate_impl(const gdx_aggregate_args* a, int variant, gdx_stream stream) 
                         (!a->src_lo8 || (reinterpret_cast<uintptr_t>(a->src_lo8) & 7) == 0),
                     GDX_INPUT, "gdx_aggregate: packed-24 rows need width and pitch multiples of 8");
         GDX_REQUIRE(a->src_lo8, GDX_INPUT, "gdx_aggregate: a packed-24 output needs a packed-24 source");
+        GDX_REQUIRE(a->ld_src_lo8 % 8 == 0, GDX_INPUT, "gdx_aggregate: ld_src_lo8 must be a multiple of 8");
         GDX_REQUIRE(!a->out24_hi || (a->ld_out24 % 8 == 0 && aligned16(a->out24_hi) &&
                                      (reinterpret_cast<uintptr_t>(a->out24_lo) & 7) == 0),
                     GDX_INPUT, "gdx_aggregate: packed-24 output pitch must be a multiple of 8");

@@ -81,4 +81,33 @@ __device__ __forceinline__ void split_bf16(float x, uint16_t& hi, uint16_t& lo) 
     lo = f2bf_rn(x - bf2f(hi));
 }
 
+// ---- packed-24 rows (aggregate.cu): fp32 rounded to nearest-even at bit 8, stored as
+// the high 16 bits (u16 plane) and the next 8 bits (u8 plane) --------------------------
+__device__ __forceinline__ void pack24(float x, uint16_t& hi, uint8_t& lo) {
+    uint32_t u = __float_as_uint(x);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x7fu + ((u >> 8) & 1u)) & 0xffffff00u;  // RNE at bit 8
+    hi = static_cast<uint16_t>(u >> 16);
+    lo = static_cast<uint8_t>(u >> 8);
+}
+__device__ __forceinline__ float unpack24(uint16_t hi, uint8_t lo) {
+    return __uint_as_float((static_cast<uint32_t>(hi) << 16) | (static_cast<uint32_t>(lo) << 8));
+}
+// 16 values -> 32 bytes of high plane (two 16-byte words) + 16 bytes of low plane
+__device__ __forceinline__ void pack24x16(const float* v, uint4& h0, uint4& h1, uint4& l) {
+    uint32_t hw[8], lw[4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        uint16_t a, b;
+        uint8_t la, lb;
+        pack24(v[2 * j], a, la);
+        pack24(v[2 * j + 1], b, lb);
+        hw[j] = static_cast<uint32_t>(a) | (static_cast<uint32_t>(b) << 16);
+        if (j % 2 == 0) lw[j / 2] = static_cast<uint32_t>(la) | (static_cast<uint32_t>(lb) << 8);
+        else lw[j / 2] |= (static_cast<uint32_t>(la) << 16) | (static_cast<uint32_t>(lb) << 24);
+    }
+    h0 = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    h1 = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+    l = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
 }  // namespace gdx

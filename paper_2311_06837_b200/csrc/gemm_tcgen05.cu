@@ -174,6 +174,10 @@ struct Epi {
     const uint32_t* a_rows; // row gather of a K-major A (m index) / an MN-major B (k index):
     const uint32_t* b_rows; // TMA gather4, 4 source rows per instruction
     uint32_t k;
+    uint16_t* p24_hi;       // packed-24 form of output p24_target (its fp32 pointer is null)
+    uint8_t* p24_lo;
+    uint64_t ld_p24_hi, ld_p24_lo;
+    int p24_target;
 };
 
 __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c_inner,
@@ -271,7 +275,8 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                 const __grid_constant__ CUtensorMap map_c0, const __grid_constant__ CUtensorMap map_c1,
                 const __grid_constant__ CUtensorMap map_mask, const __grid_constant__ CUtensorMap map_shi,
-                const __grid_constant__ CUtensorMap map_slo, const Epi ep) {
+                const __grid_constant__ CUtensorMap map_slo, const __grid_constant__ CUtensorMap map_phi,
+                const __grid_constant__ CUtensorMap map_plo, const Epi ep) {
     static_assert(!MT || (BN == 64 && EW == 8), "mask-TMA variant: BN 64, 8 epilogue warps");
     using S = Smem<BN, STAGES, EW, MT>;
     constexpr int kEpiWarps = EW;
@@ -533,9 +538,21 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
                             *reinterpret_cast<uint4*>(buf + 3072 + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
                         }
                     }
+                    if (ep.p24_hi) {  // packed-24 c0: hi 32 x 32 B (SWIZZLE_32B) at 0, lo 32 x 16 B at 1 KB
+                        float o[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) o[j] = ep.relu ? fmaxf(vv[j] * rs, 0.f) : vv[j] * rs;
+                        uint4 h0, h1, l0;
+                        pack24x16(o, h0, h1, l0);
+                        const uint32_t s32 = (lane >> 2) & 1;
+                        *reinterpret_cast<uint4*>(buf + lane * 32 + (s32 << 4)) = h0;
+                        *reinterpret_cast<uint4*>(buf + lane * 32 + ((1 ^ s32) << 4)) = h1;
+                        *reinterpret_cast<uint4*>(buf + 1024 + lane * 16) = l0;
+                    }
                     const uint32_t sw = (lane >> 1) & 3;  // SWIZZLE_64B
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
+                        if (ep.p24_hi) break;
                         float4 o;
                         o.x = vv[4 * j] * rs;
                         o.y = vv[4 * j + 1] * rs;
@@ -552,6 +569,10 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
                     if (lane == 0) {
                         const int32_t r0 = static_cast<int32_t>(mt * BM + lane_base);
                         if (ep.c0) tma_store_2d_nc(&map_c0, buf, col0, r0);
+                        if (ep.p24_hi) {
+                            tma_store_2d_nc(&map_phi, buf, col0, r0);
+                            tma_store_2d_nc(&map_plo, buf + 1024, col0, r0);
+                        }
                         if (ep.out_hi) {
                             tma_store_2d_nc(&map_shi, buf + 2048, col0, r0);
                             tma_store_2d_nc(&map_slo, buf + 3072, col0, r0);
@@ -689,6 +710,20 @@ __global__ void __launch_bounds__(kThreadsFor(EW), 1)
                         continue;
                     }
                     if (!row_ok) continue;
+                    if (ep.p24_hi && col0 + 16 <= ep.n &&
+                        (ep.p24_target == 0 ? col0 + 16 <= ep.split : col0 >= ep.split)) {
+                        const uint32_t pc = ep.p24_target == 0 ? col0 : col0 - ep.split;
+                        uint4 h0, h1, l0;
+                        pack24x16(vv, h0, h1, l0);
+                        uint4* hp = reinterpret_cast<uint4*>(ep.p24_hi + static_cast<uint64_t>(row) * ep.ld_p24_hi + pc);
+                        hp[0] = h0;
+                        hp[1] = h1;
+                        *reinterpret_cast<uint4*>(ep.p24_lo + static_cast<uint64_t>(row) * ep.ld_p24_lo + pc) = l0;
+                        if (ep.out_hi && !ep.split_unscaled)
+                            store_split16(vv, ep.out_hi + static_cast<uint64_t>(row) * ep.ld_split + col0,
+                                          ep.out_lo + static_cast<uint64_t>(row) * ep.ld_split + col0, col0, ep.n);
+                        continue;
+                    }
                     // a 16-column group entirely on one side of the split: 4 x 16 B stores
                     float* base = nullptr;
                     bool xchg = false;
@@ -809,10 +844,10 @@ int make_map(CUtensorMap* map, const uint16_t* base, uint64_t inner, uint64_t ou
 // fp32 output map for the TMA-store epilogue: (cols inner, rows outer), box {16, 32},
 // 64-byte rows swizzled as the epilogue writes them.
 int make_out_map(CUtensorMap* map, void* base, uint64_t cols, uint64_t rows, uint64_t ld,
-                 bool u16 = false, uint32_t box_cols = 16, uint32_t box_rows = 32) {
+                 bool u16 = false, uint32_t box_cols = 16, uint32_t box_rows = 32, bool u8 = false) {
     auto fn = encode_fn();
     GDX_REQUIRE(fn != nullptr, GDX_INTERNAL, "cuTensorMapEncodeTiled unavailable");
-    const uint32_t esz = u16 ? 2 : 4;
+    const uint32_t esz = u8 ? 1 : u16 ? 2 : 4;
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {ld * esz};
     cuuint32_t box[2] = {box_cols, box_rows};
@@ -820,8 +855,10 @@ int make_out_map(CUtensorMap* map, void* base, uint64_t cols, uint64_t rows, uin
     const uint32_t row_bytes = box_cols * esz;
     const CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                   : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                    : CU_TENSOR_MAP_SWIZZLE_32B;
-    CUresult r = fn(map, u16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
+                                  : row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                    : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = fn(map, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : u16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     GDX_REQUIRE(r == CUDA_SUCCESS, GDX_INTERNAL,
@@ -869,7 +906,7 @@ int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
         return rc;
     }
     // TMA-store epilogue for the staged fp32 outputs (16-byte aligned bases, pitch % 4)
-    CUtensorMap mc0{}, mc1{}, mmask{}, mshi{}, mslo{};
+    CUtensorMap mc0{}, mc1{}, mmask{}, mshi{}, mslo{}, mphi{}, mplo{};
     Epi e = ep;
     e.tma_store = 0;
     if constexpr (MT) {  // gdx_gemm_tn checked the shapes and alignments (mask_tma_ok)
@@ -880,8 +917,12 @@ int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
             if ((rc = make_out_map(&mshi, ep.out_hi, ep.n, ep.m, ep.ld_split, true))) return rc;
             if ((rc = make_out_map(&mslo, ep.out_lo, ep.n, ep.m, ep.ld_split, true))) return rc;
         }
+        if (ep.p24_hi) {
+            if ((rc = make_out_map(&mphi, ep.p24_hi, ep.n, ep.m, ep.ld_p24_hi, true))) return rc;
+            if ((rc = make_out_map(&mplo, ep.p24_lo, ep.n, ep.m, ep.ld_p24_lo, false, 16, 32, true))) return rc;
+        }
         e.tma_store = ep.c0 != nullptr;
-    } else if (kStgBytesFor(EW) && ep.stage_stores && ep.split_k <= 1 && tma_store_enabled()) {
+    } else if (kStgBytesFor(EW) && ep.stage_stores && ep.split_k <= 1 && tma_store_enabled() && !ep.p24_hi) {
         const bool ok0 = !ep.c0 || (ep.split >= 16 && ep.ldc0 % 4 == 0 &&
                                     (reinterpret_cast<uintptr_t>(ep.c0) & 15) == 0);
         const bool ok1 = !ep.c1 || ep.split >= ep.n ||
@@ -899,7 +940,7 @@ int launch_tc(const gdx_gemm_args* g, const Epi& ep, cudaStream_t s) {
     const uint64_t sms = static_cast<uint64_t>(device_sms());
     const uint64_t tiles = static_cast<uint64_t>(ep.m_tiles) * ep.n_tiles * ep.split_k;
     const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
-    kern<<<grid, kThreadsFor(EW), bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, mc0, mc1, mmask, mshi, mslo, e);
+    kern<<<grid, kThreadsFor(EW), bytes, s>>>(ma_hi, ma_lo, mb_hi, mb_lo, mc0, mc1, mmask, mshi, mslo, mphi, mplo, e);
     note_launch();
     return check_launch("gdx_gemm_tn");
 }
@@ -939,6 +980,7 @@ bool mask_tma_ok(const gdx_gemm_args* g, const Epi& ep) {
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     return on && g->mask && !g->a_rows && !g->b_rows && g->n == 64 && g->k > 0 && !g->a_mn_major && g->b_mn_major && ep.split_k <= 1 &&
            g->npeers == 0 && ep.split >= g->n && !g->c1 && (!g->c0 || (al(g->c0) && g->ldc0 % 4 == 0)) &&
+           (!g->p24_hi || g->p24_target == 0) &&
            al(g->mask) && g->ld_mask % 4 == 0 &&
            (!g->out_hi || (al(g->out_hi) && al(g->out_lo) && g->ld_split % 8 == 0));
 }
@@ -957,6 +999,15 @@ int validate(const gdx_gemm_args* g) {
     GDX_REQUIRE(!g->mask || g->ld_mask >= g->n, GDX_INPUT, "gdx_gemm_tn: ld_mask < n");
     GDX_REQUIRE(g->npeers <= 7, GDX_INPUT, "gdx_gemm_tn: at most 7 peers");
     GDX_REQUIRE(g->npeers == 0 || g->split_k <= 1, GDX_INPUT, "gdx_gemm_tn: peers with split_k");
+    if (g->p24_hi) {
+        const uint32_t lo = g->p24_target == 0 ? 0 : g->split, hi = g->p24_target == 0 ? g->split : g->n;
+        auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        GDX_REQUIRE(g->p24_lo && (g->p24_target == 0 ? !g->c0 : !g->c1), GDX_INPUT,
+                    "gdx_gemm_tn: a packed-24 output needs both planes and replaces its fp32 output");
+        GDX_REQUIRE(lo % 16 == 0 && (hi - lo) % 16 == 0 && g->ld_p24_hi % 8 == 0 && g->ld_p24_lo % 16 == 0 &&
+                        al(g->p24_hi) && al(g->p24_lo) && g->split_k <= 1 && g->npeers == 0,
+                    GDX_INPUT, "gdx_gemm_tn: packed-24 output columns, pitches and bases must be 16-aligned");
+    }
     GDX_REQUIRE(!g->a_rows || (!g->a_mn_major && g->a_src_rows > 0 && g->a_src_rows < (1ull << 31)), GDX_INPUT,
                 "gdx_gemm_tn: a_rows gathers a K-major A from a_src_rows (< 2^31) source rows");
     GDX_REQUIRE(!g->b_rows || (g->b_mn_major && g->b_src_rows > 0 && g->b_src_rows < (1ull << 31)), GDX_INPUT,
@@ -980,7 +1031,8 @@ Epi make_epi(const gdx_gemm_args* g, int bn) {
            g->mask, g->ld_mask, g->split_unscaled, g->npeers, g->peer_target, {},
            // measured (tools/gemm_bench.py): the transposed stores win on long
            // write-bound GEMMs (6 M rows: 1.2-1.25x) and lose on short ones (233 K rows)
-           g->m >= stage_min_rows() ? 1 : 0, 0, g->a_rows, g->b_rows, g->k};
+           g->m >= stage_min_rows() && !g->p24_hi ? 1 : 0, 0, g->a_rows, g->b_rows, g->k,
+           g->p24_hi, g->p24_lo, g->ld_p24_hi, g->ld_p24_lo, g->p24_target};
     for (int r = 0; r < 7; ++r) ep.peer_delta[r] = g->peer_delta[r];
     return ep;
 }

@@ -46,7 +46,19 @@ __global__ void zero_f64(double* p) { *p = 0.0; }
 struct Mat {  // fp32 rows x cols, row pitch ld (elements)
     float* p = nullptr;
     uint64_t ld = 0;
+    // p24: the rows are packed-24 instead (cfg.packed24), interleaved so that a block of
+    // rows is one contiguous range: row r at byte 3 ld r, high plane (ld u16) then low
+    // plane (ld u8)
+    int p24 = 0;
     float* row(uint64_t r) const { return p + r * ld; }
+    uint64_t row_bytes() const { return p24 ? 3 * ld : 4 * ld; }
+    Mat rows_from(uint64_t r) const {  // view starting at row r
+        Mat v = *this;
+        v.p = reinterpret_cast<float*>(reinterpret_cast<char*>(p) + r * row_bytes());
+        return v;
+    }
+    uint16_t* hi24() const { return reinterpret_cast<uint16_t*>(p); }
+    uint8_t* lo24() const { return reinterpret_cast<uint8_t*>(p) + 2 * ld; }
 };
 struct Spl {  // split-bf16 operand
     uint16_t* hi = nullptr;
@@ -245,6 +257,15 @@ int gemm(gdx_trainer* t, const Spl& A, const Spl& B, bool a_mn, bool b_mn, uint3
     g.m = m; g.n = nB; g.k = kA;
     g.c0 = c0.p; g.ldc0 = c0.ld;
     g.c1 = c1.p; g.ldc1 = c1.ld;
+    for (int which = 0; which < 2; ++which) {  // a packed-24 output replaces its fp32 form
+        const Mat& c = which ? c1 : c0;
+        if (!c.p24) continue;
+        if (which) g.c1 = nullptr;
+        else g.c0 = nullptr;
+        g.p24_hi = c.hi24(); g.p24_lo = c.lo24();
+        g.ld_p24_hi = 3 * c.ld / 2; g.ld_p24_lo = 3 * c.ld;
+        g.p24_target = which;
+    }
     g.split = split ? split : nB;
     g.row_scale = row_scale;
     g.relu = relu;
@@ -276,6 +297,12 @@ int aggregate(gdx_trainer* t, const Mat& src, uint32_t width, uint32_t rows, con
     a.rows = rows;
     a.width = width;
     a.src = src.p; a.ld_src = src.ld;
+    if (src.p24) {  // packed-24 rows: u16 high plane + u8 low plane, both at the 3 ld-byte pitch
+        a.src = reinterpret_cast<const float*>(src.hi24());
+        a.ld_src = 3 * src.ld / 2;
+        a.src_lo8 = src.lo24();
+        a.ld_src_lo8 = 3 * src.ld;
+    }
     a.self_coef = e.self_coef;
     a.self_base = t->lo;
     a.post_scale = e.post_scale;
@@ -295,7 +322,9 @@ int aggregate(gdx_trainer* t, const Mat& src, uint32_t width, uint32_t rows, con
         TR_CUDA(cudaEventRecord(e1, t->stream));
         t->prof_events.push_back({e0, e1});
         // 4 nnz + 8 (rows+1) + 4 F nnz + 4 F rows per launch
-        t->prof_bytes.push_back(4.0 * nnz_pass + 8.0 * (rows + 1.0) + 4.0 * width * nnz_pass + 4.0 * width * rows);
+        // (a packed-24 source moves 3 bytes per gathered value instead of 4)
+        const double eb = src.p24 ? 3.0 : 4.0;
+        t->prof_bytes.push_back(4.0 * nnz_pass + 8.0 * (rows + 1.0) + eb * width * nnz_pass + 4.0 * width * rows);
     }
     return GDX_OK;
 }
@@ -419,14 +448,13 @@ int forward(gdx_trainer* t) {
                        nullptr, false));
             continue;
         }
-        Mat own = Ly.Zfull;
-        own.p = own.row(t->lo);
+        Mat own = Ly.Zfull.rows_from(t->lo);
         if (kind == GDX_MODEL_SAGE)
             TR_OK(gemm(t, A, Ly.Wsp, false, false, m_in, Ly.S, own, Ly.w, nullptr, false, nullptr, 1, nullptr, false));
         else
             TR_OK(gemm(t, A, Ly.Wsp, false, false, m_in, own, Mat{}, 0, kind == GDX_MODEL_GCN ? t->gcn_s : nullptr,
                        false, nullptr, 1, nullptr, false));
-        TR_OK(publish(t, own.p, t->nloc * Ly.Zfull.ld * 4));
+        TR_OK(publish(t, own.p, t->nloc * Ly.Zfull.row_bytes()));
         AggEpi e;
         e.has_out = e.has_split = true;
         if (l + 1 < t->L && t->layers[l + 1].agg_first) {
@@ -462,8 +490,7 @@ struct GradTargets {
 GradTargets grad_targets(gdx_trainer* t, uint32_t l) {
     Layer& Ly = t->layers[l];
     GradTargets g;
-    g.own = Ly.dfull;
-    g.own.p = g.own.row(t->lo);
+    g.own = Ly.dfull.rows_from(t->lo);
     if (t->cfg.kind == GDX_MODEL_SAGE) {
         g.scale = t->inv_deg;
         g.split = &Ly.G;
@@ -501,11 +528,12 @@ int backward_agg_first(gdx_trainer* t, uint32_t l) {
     e.add = Ly.dself;
     TR_OK(exchange_aggregate(t, Ly.dAfull, Ly.w, t->rows_in[l], e));
     GradTargets gt = grad_targets(t, l - 1);
+    if (gt.own.p24) return err(GDX_INTERNAL, "grad_prepare: packed-24 gradient rows");
     const Mat a = act(t, l - 1);
     TR_OK(gdx_grad_prepare(Ly.dtmp.p, Ly.dtmp.ld, a.p, a.ld, t->rows_out[l - 1], Ly.w, gt.scale, nullptr, 0, gt.own.p,
                            gt.own.ld, gt.split ? gt.split->hi : nullptr, gt.split ? gt.split->lo : nullptr,
                            gt.split ? gt.split->ld : 0, reinterpret_cast<gdx_stream>(t->stream)));
-    return publish(t, gt.own.p, t->nloc * t->layers[l - 1].dfull.ld * 4);
+    return publish(t, gt.own.p, t->nloc * t->layers[l - 1].dfull.row_bytes());
 }
 
 int backward_and_step(gdx_trainer* t) {
@@ -533,7 +561,7 @@ int backward_and_step(gdx_trainer* t) {
             const Mat a = act(t, l - 1);
             TR_OK(gemm(t, Ly.G, Ly.Wsp, false, true, t->rows_out[l - 1], gt.own, Mat{}, 0, gt.scale, false,
                        gt.split, 1, &a, true));
-            TR_OK(publish(t, gt.own.p, t->nloc * t->layers[l - 1].dfull.ld * 4));
+            TR_OK(publish(t, gt.own.p, t->nloc * t->layers[l - 1].dfull.row_bytes()));
         }
         const Spl A_in = l == 0 ? t->Xsp : t->layers[l - 1].Hsp;
         const uint32_t sk = splitk_eff(Ly.split_k, r_in);
@@ -579,10 +607,11 @@ int epoch_body(gdx_trainer* t) {
                                      nullptr, nullptr, 0, last.Gl.hi, last.Gl.lo, last.Gl.ld, t->loss_acc, s));
     } else {
         GradTargets gt = grad_targets(t, t->L - 1);
+        if (gt.own.p24) return err(GDX_INTERNAL, "softmax: packed-24 gradient rows");
         TR_OK(gdx_softmax_xent_fused(last.Hout.p, last.Hout.ld, t->loss_rows, t->classes, t->labels, inv, nullptr, 0,
                                      gt.scale, gt.own.p, gt.own.ld, gt.split ? gt.split->hi : nullptr,
                                      gt.split ? gt.split->lo : nullptr, gt.split ? gt.split->ld : 0, t->loss_acc, s));
-        TR_OK(publish(t, gt.own.p, t->nloc * last.dfull.ld * 4));
+        TR_OK(publish(t, gt.own.p, t->nloc * last.dfull.row_bytes()));
     }
     return backward_and_step(t);
 }
@@ -687,6 +716,16 @@ int setup_model(gdx_trainer* t) {
             TR_OK(dspl(t, &Ly.Hsp, t->nloc, Ly.w));
             TR_OK(dspl(t, &Ly.G, t->nloc, Ly.nz));
         }
+    }
+    // packed-24 gathered rows (cfg.packed24) for 64k-wide transform-first layers: Z from
+    // the forward GEMM's epilogue, dZ from the dH GEMM's (not from the softmax or
+    // grad_prepare kernels, which write fp32)
+    const bool p24_ok = t->cfg.packed24 && !t->cfg.fused_exchange && (!t->bins || t->bins->n_heavy == 0);
+    for (uint32_t l = 0; l < t->L && p24_ok; ++l) {
+        Layer& Ly = t->layers[l];
+        if (Ly.agg_first || Ly.w % 64 != 0) continue;
+        Ly.Zfull.p24 = 1;
+        Ly.dfull.p24 = l + 1 < t->L && !t->layers[l + 1].agg_first;
     }
     if (!t->subgraph && t->world > 1) {
         uint32_t wmax = 0;

@@ -103,10 +103,12 @@ def dense(rows: int, cols: int, device, zero: bool = True) -> torch.Tensor:
 def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_split: Split | None = None,
               self_coef: float = 0.0, self_base: int = 0, post_scale=None, add=None, relu=False,
               row_end=None, row_begin=None, skip=None, partial=None, stream=None, variant: int = 0,
-              bins: "RowBins | None" = None):
+              bins: "RowBins | None" = None, src_lo8=None, ld_src_lo8: int = 0):
     """K1/K3 (see include/gdx.h gdx_aggregate).  row_begin/row_end override the CSR
     row bounds; skip = (seg_lo, seg_hi) excludes a per-row sub-range; partial adds
-    precomputed partial sums before the epilogue."""
+    precomputed partial sums before the epilogue.  src_lo8 (uint8 tensor or byte
+    address): src is the u16 high plane of packed-24 rows, this the low plane (pitch
+    ld_src_lo8 bytes, default the high plane's pitch in elements)."""
     a = AggregateArgs()
     a.row_ptr = g.row_ptr.data_ptr() if row_begin is None else row_begin.data_ptr()
     a.row_end = ptr(row_end) if row_begin is None else (row_end.data_ptr() if row_end is not None
@@ -120,6 +122,9 @@ def aggregate(g: DeviceCSR, src: torch.Tensor, width: int, *, out=None, out_spli
     a.width = width
     a.src = src.data_ptr()
     a.ld_src = src.stride(0) if src.dim() == 2 else width
+    if src_lo8 is not None:
+        a.src_lo8 = src_lo8 if isinstance(src_lo8, int) else src_lo8.data_ptr()
+        a.ld_src_lo8 = ld_src_lo8
     a.self_coef = self_coef
     a.self_base = self_base
     a.post_scale = ptr(post_scale)
@@ -162,7 +167,7 @@ class RowBins:
 def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None, relu=False,
             out_split: Split | None = None, split_k: int = 1, m=None, simt=False, a_mn=False,
             b_mn=False, mask=None, split_unscaled=False, peers=None, stream=None, a_rows=None,
-            b_rows=None):
+            b_rows=None, p24=None):
     """K2: C(m, n) = sum_k A(m, k) B(n, k).  A is stored [m][k] (K-major) or, with
     a_mn, [k][m]; likewise B ([n][k] or [k][n]).  a_rows / b_rows (int32 device
     tensors): A / B are the SOURCE matrices and the operand's rows (m for a K-major A,
@@ -197,6 +202,8 @@ def gemm_tn(A: Split, B: Split, *, c0=None, c1=None, split=None, row_scale=None,
     if mask is not None:
         g.mask, g.ld_mask = mask.data_ptr(), mask.stride(0)
     g.split_unscaled = int(split_unscaled)
+    if p24 is not None:   # (hi address, lo address, ld_hi u16, ld_lo bytes, target output)
+        g.p24_hi, g.p24_lo, g.ld_p24_hi, g.ld_p24_lo, g.p24_target = p24
     if a_rows is not None:
         g.a_rows, g.a_src_rows = a_rows.data_ptr(), A.rows
     if b_rows is not None:

@@ -28,7 +28,7 @@ class TrainerConfig(C.Structure):
                 ("lr", C.c_float), ("rank", C.c_uint32), ("world", C.c_uint32), ("device", C.c_int),
                 ("feature_seed", C.c_uint64), ("label_seed", C.c_uint64), ("use_graph", C.c_int),
                 ("no_agg_first", C.c_int), ("push_ctas", C.c_uint32), ("peer_timeout_s", C.c_double),
-                ("heavy_degree", C.c_uint32), ("fused_exchange", C.c_int)]
+                ("heavy_degree", C.c_uint32), ("fused_exchange", C.c_int), ("packed24", C.c_int)]
 
 
 class TrainerGraph(C.Structure):
@@ -95,7 +95,8 @@ class NativeTrainer:
     def __init__(self, g: Graph, cfg, *, rank: int = 0, world: int = 1, device: int | None = None,
                  weights=None, weight_seed: int = 3, subgraph=None, pg=None, use_graph: bool = True,
                  feature_seed: int = FEATURE_SEED, label_seed: int = LABEL_SEED, push_ctas: int = 0,
-                 no_agg_first: bool = False, heavy_degree: int = 0, fused_exchange: bool | None = None):
+                 no_agg_first: bool = False, heavy_degree: int = 0, fused_exchange: bool | None = None,
+                 packed24: bool = False):
         import torch
         L = _bind()
         if cfg.kind not in KIND:
@@ -106,7 +107,8 @@ class NativeTrainer:
         self._dims_c = (C.c_uint32 * len(self.dims))(*self.dims)
         c = TrainerConfig(KIND[cfg.kind], len(self.dims) - 1, self._dims_c, cfg.lr, rank, world, self.device,
                           feature_seed, label_seed, int(use_graph), int(no_agg_first), push_ctas, 0.0,
-                          heavy_degree, int(_fused_default() if fused_exchange is None else fused_exchange))
+                          heavy_degree, int(_fused_default() if fused_exchange is None else fused_exchange),
+                          int(packed24))
         gr = TrainerGraph()
         gr.num_vertices = g.num_vertices()
         self.subgraph_mode = subgraph is not None

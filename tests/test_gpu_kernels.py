@@ -314,6 +314,83 @@ def test_gemm_gathered_b_rows(gdx, cuda, kk, n, sk):
     close(tot, G.to_float().double().cpu().numpy().T @ xg)
 
 
+def _interleaved_p24(cuda, ref, m, n):
+    """packed-24 planes of fp32 `ref` [m, n] in the trainer's interleaved rows (3 n bytes
+    per row: high plane then low plane) via gdx_pack24 -- (buffer, hi addr, lo addr)."""
+    import torch
+    from paper_2311_06837_b200._lib import call
+    from paper_2311_06837_b200.device import stream_handle
+    hi = torch.zeros(m * n, dtype=torch.int16, device=cuda)
+    lo = torch.zeros(m * n, dtype=torch.uint8, device=cuda)
+    call("gdx_pack24", ref.data_ptr(), ref.stride(0), m, n, hi.data_ptr(), lo.data_ptr(), n, stream_handle())
+    buf = torch.zeros((m, 3 * n), dtype=torch.uint8, device=cuda)
+    buf[:, :2 * n] = hi.view(torch.uint8).view(m, 2 * n)
+    buf[:, 2 * n:] = lo.view(m, n)
+    return buf.view(-1)
+
+
+@pytest.mark.parametrize("case", ["sage-fwd", "gcn-fwd", "dh-mask"])
+def test_gemm_packed24_outputs(gdx, cuda, case):
+    """Packed-24 GEMM outputs (generic epilogue: SAGE forward's c1 / GCN forward's
+    row-scaled c0; TMA-store mask epilogue: the dH GEMM) are exactly the packed-24
+    rounding of the fp32 outputs, in the trainer's interleaved row layout."""
+    import torch
+    rng = np.random.default_rng(7)
+    m, k = 1000, 96
+    n = 128 if case == "sage-fwd" else 64
+    A = _split(gdx, rng.uniform(-1, 1, (m, k)), cuda)
+    kw, bmn = {}, case == "dh-mask"
+    B = _split(gdx, rng.uniform(-1, 1, (k, n)) if bmn else rng.uniform(-1, 1, (n, k)), cuda)
+    if case == "gcn-fwd":
+        kw["row_scale"] = torch.rand(m, device=cuda) + 0.5
+    if case == "dh-mask":
+        kw.update(mask=torch.randn(m, n, device=cuda), row_scale=torch.rand(m, device=cuda) + 0.5,
+                  out_split=gdx.Split(m, n, cuda), split_unscaled=True)
+    w24 = 64
+    buf = torch.zeros(m * 3 * w24, dtype=torch.uint8, device=cuda)
+    p24 = (buf.data_ptr(), buf.data_ptr() + 2 * w24, 3 * w24 // 2, 3 * w24)
+    ref = gdx.dense(m, n, cuda)
+    if case == "sage-fwd":
+        S = gdx.dense(m, 64, cuda)
+        gdx.gemm_tn(A, B, c0=S, split=64, p24=p24 + (1,))
+        gdx.gemm_tn(A, B, c0=ref, **kw)
+        want = ref[:, 64:128].contiguous()
+        torch.cuda.synchronize()
+        assert torch.equal(S, ref[:, :64])
+    else:
+        gdx.gemm_tn(A, B, b_mn=bmn, p24=p24 + (0,), **kw)
+        gdx.gemm_tn(A, B, c0=ref, b_mn=bmn, **kw)
+        want = ref[:, :64].contiguous()
+    exp = _interleaved_p24(cuda, want, m, w24)
+    torch.cuda.synchronize()
+    assert torch.equal(buf, exp)
+
+
+def test_aggregate_packed24_interleaved_rows(gdx, cuda):
+    """ld_src_lo8: a packed-24 source in interleaved rows aggregates exactly like the
+    same values in two separate planes."""
+    import torch
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200._lib import call
+    from paper_2311_06837_b200.device import stream_handle
+    n, w = 3000, 64
+    g = G.gen_random_graph(n, 30.0, 5)
+    dg = g.device(cuda)
+    x = torch.randn(n, w, device=cuda)
+    inter = _interleaved_p24(cuda, x, n, w)
+    hi = torch.zeros(n * w, dtype=torch.int16, device=cuda)
+    lo = torch.zeros(n * w, dtype=torch.uint8, device=cuda)
+    call("gdx_pack24", x.data_ptr(), w, n, w, hi.data_ptr(), lo.data_ptr(), w, stream_handle())
+    outs = []
+    for src, lo8, ldl in ((hi.view(n, w), lo, 0), (torch.as_strided(inter.view(torch.int16), (n, w), (3 * w // 2, 1)),
+                                                    inter.data_ptr() + 2 * w, 3 * w)):
+        out = gdx.dense(n, w, cuda)
+        gdx.aggregate(dg, src, w, out=out, self_coef=1.0, src_lo8=lo8, ld_src_lo8=ldl)
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("width", [64, 30])
 def test_grad_prepare(gdx, cuda, width):
     """g = dH * (H > 0) -> split(g) and gs = g * scale (vector and scalar forms)."""
