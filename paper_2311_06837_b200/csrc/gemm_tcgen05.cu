@@ -993,7 +993,7 @@ int validate(const gdx_gemm_args* g) {
     GDX_REQUIRE(g->lda % 8 == 0 && g->ldb % 8 == 0, GDX_INPUT,
                 "gdx_gemm_tn: leading dims must be multiples of 8 elements (16 B TMA pitch)");
     GDX_REQUIRE(g->split <= g->n, GDX_INPUT, "gdx_gemm_tn: split > n");
-    GDX_REQUIRE(g->c0 || g->c1 || g->out_hi, GDX_INPUT, "gdx_gemm_tn: no output");
+    GDX_REQUIRE(g->c0 || g->c1 || g->out_hi || g->p24_hi, GDX_INPUT, "gdx_gemm_tn: no output");
     GDX_REQUIRE(!g->out_hi == !g->out_lo, GDX_INPUT, "gdx_gemm_tn: out_hi/out_lo must pair");
     GDX_REQUIRE(g->split_k <= 1 || g->c0, GDX_INPUT, "gdx_gemm_tn: split_k needs c0 workspace");
     GDX_REQUIRE(!g->mask || g->ld_mask >= g->n, GDX_INPUT, "gdx_gemm_tn: ld_mask < n");

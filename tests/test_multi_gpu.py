@@ -24,7 +24,7 @@ def test_row_partitioned_training_matches_oracle():
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
                         "--master-port", "29531", os.path.join(ROOT, "tools", "dist_check.py"),
-                        "--modes", "sm,epilogue,nccl,native,native-eas,native-fused"],
+                        "--modes", "sm,epilogue,nccl,native,native-eas,native-fused,native-p24"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     line = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and line, r.stdout[-2000:] + r.stderr[-2000:]

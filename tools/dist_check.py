@@ -40,6 +40,7 @@ MODES = {
     "native": {"_NATIVE": "1"},                            # C-ABI trainer (csrc/trainer.cu): IPC buffers
     "native-fused": {"_NATIVE": "1", "GDX_FUSED_EXCHANGE": "1"},  # one kernel: push + aggregate + wait
     "native-eas": {"_NATIVE": "eas"},                      # C-ABI trainer, per-rank EAS subgraphs
+    "native-p24": {"_NATIVE": "1", "_P24": "1"},           # C-ABI trainer, packed-24 gathered rows
 }
 FULL_CASES = (("sage", 5001, 24.0, [96, 64, 64, 41], 5),
               ("gcn", 3001, 10.0, [32, 32, 8], 4),
@@ -147,7 +148,8 @@ def main():
                 g = G.gen_random_graph(n, deg, 5)
                 cfg = ModelConfig(kind, dims, lr=0.5)
                 w0 = init_weights(cfg, 3)
-                tr = Trainer(g, cfg, rank=rank, world=world, weights=w0, pg=dist.group.WORLD)
+                kw = {"packed24": True} if env.get("_P24") else {}
+                tr = Trainer(g, cfg, rank=rank, world=world, weights=w0, pg=dist.group.WORLD, **kw)
                 losses = [tr.train_epoch() for _ in range(epochs)]
                 same = weights_identical(tr, dev)
                 dist.barrier()   # no rank frees its IPC-shared buffers while a peer may touch them
