@@ -30,7 +30,8 @@ def main():
     if args.what in ("reddit", "products"):
         C = bench.CONFIGS["reddit-sage" if args.what == "reddit" else "products-gcn"]
         g = G.gen_random_graph(C["n"], C["degree"], C["seed"])
-        tr = NativeTrainer(g, ModelConfig(C["kind"], list(C["dims"]), lr=C["lr"]), use_graph=False)
+        tr = NativeTrainer(g, ModelConfig(C["kind"], list(C["dims"]), lr=C["lr"]), use_graph=False,
+                           packed24=bool(C.get("packed24")))
         for _ in range(args.epochs):
             tr.train_epoch(sync_loss=False)
         torch.cuda.synchronize()
