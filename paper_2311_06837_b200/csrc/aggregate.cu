@@ -783,6 +783,18 @@ int launch_p24(const AggParams& p, int variant, cudaStream_t s) {
         else if (minb >= 6) rows ? vec(aggregate_rows_p24<LPE, UN, 6>, EPW) : vec(aggregate_p24<LPE, UN, 6>, EPW); \
         else rows ? vec(aggregate_rows_p24<LPE, UN, 4>, EPW) : vec(aggregate_p24<LPE, UN, 4>, EPW); \
         return 0;
+    // tuning: GDX_P24_UN=2 for the 64-wide warp-per-row kernel (lower unroll, more
+    // resident warps at MINB 6/8)
+    static const int un2 = [] {
+        const char* e = std::getenv("GDX_P24_UN");
+        return e && std::atoi(e) == 2;
+    }();
+    if (c8 == 8 && un2 && !rows) {
+        if (minb >= 8) vec(aggregate_p24<8, 2, 8>, 4);
+        else if (minb >= 6) vec(aggregate_p24<8, 2, 6>, 4);
+        else vec(aggregate_p24<8, 2, 4>, 4);
+        return 0;
+    }
     switch (c8) {
         GDX_P24_CASE(1, 1, 4, 32)
         GDX_P24_CASE(2, 2, 4, 16)
