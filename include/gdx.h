@@ -169,6 +169,10 @@ int gdx_row_split(const uint64_t* row_ptr, const uint32_t* col, uint32_t rows, u
  * plain CSR rows only (falls back to GDX_AGG_ROWS with row_end / skip / row lists). */
 #define GDX_AGG_ROWS2 2
 #define GDX_AGG_FLAT 3
+/* GDX_AGG_P24_WIDE: 48-wide packed-24 rows whose planes are readable to 64 columns (pitch
+ * >= 64 in both planes, e.g. the trainer's 192-byte interleaved rows) gathered as whole
+ * 64-wide rows; columns 48..63 are read but never stored. */
+#define GDX_AGG_P24_WIDE 16
 int gdx_aggregate_variant(const gdx_aggregate_args* a, int variant, gdx_stream stream);
 
 /* ------------------------------------------------------------------------
@@ -318,6 +322,14 @@ int gdx_softmax_xent_fused(const float* logits, uint64_t ld, uint32_t rows, uint
                            const int32_t* labels, float inv_count, float* dlogits, uint64_t ld_d,
                            const float* row_scale, float* gs, uint64_t ld_gs, uint16_t* g_hi,
                            uint16_t* g_lo, uint64_t ld_g, double* loss_sum, gdx_stream stream);
+/* Same, with gs stored as packed-24 rows (u16 high plane, pitch ld_hi24 elements; u8 low
+ * plane, pitch ld_lo8 bytes; the trainer's interleaved layout) instead of fp32 -- the
+ * gathered source of the output layer's transposed aggregation.  classes <= 128. */
+int gdx_softmax_xent_fused_p24(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
+                               const int32_t* labels, float inv_count, const float* row_scale,
+                               uint16_t* gs_hi24, uint64_t ld_hi24, uint8_t* gs_lo8, uint64_t ld_lo8,
+                               uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g, double* loss_sum,
+                               gdx_stream stream);
 /* Same, with gs also stored into npeers peer buffers (gs + gs_peer_delta[r] bytes). */
 int gdx_softmax_xent_fused_peers(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
                                  const int32_t* labels, float inv_count, const float* row_scale,
@@ -441,7 +453,7 @@ typedef struct gdx_trainer_config {
                                * (max(4096, 32 x mean degree)), 0xFFFFFFFF: never */
     int fused_exchange;       /* world > 1: 1 = gdx_aggregate_exchange (one kernel per layer
                                * exchange), 0 = push kernel + two passes + wait kernel */
-    int packed24;             /* 1: the gathered Z / dZ rows of 64k-wide transform-first layers
+    int packed24;             /* 1: the gathered Z / dZ rows of 64k- and 64k+48-wide transform-first layers
                                * are stored packed-24 (fp32 rounded to 24 bits, relative 2^-16:
                                * the GEMM operands' precision) -- 25% fewer gathered bytes on
                                * L2-resident graphs; off with fused_exchange or heavy rows */

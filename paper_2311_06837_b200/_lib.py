@@ -101,6 +101,8 @@ _SIGS = {
     "gdx_peer_wait": (C.c_int, [vp, vp, u32, u32, u64, vp]),
     "gdx_softmax_xent_fused": (C.c_int, [vp, u64, u32, u32, vp, C.c_float, vp, u64, vp, vp, u64, vp, vp,
                                          u64, vp, vp]),
+    "gdx_softmax_xent_fused_p24": (C.c_int, [vp, u64, u32, u32, vp, C.c_float, vp, vp, u64, vp, u64, vp, vp,
+                                             u64, vp, vp]),
     "gdx_degree_scale": (C.c_int, [vp, u32, C.c_int, vp, vp]),
     "gdx_probe_bandwidth": (C.c_int, [vp, u64, u32, C.c_int, vp, vp]),
     "gdx_sampled_growth": (C.c_int, [vp, vp, u32, vp, vp, u32, u32, u64, vp, vp, vp]),

@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(256, MINB) aggregate_p24(const AggParams p) {
             a1.z += __shfl_down_sync(0xffffffffu, a1.z, k * LPE);
             a1.w += __shfl_down_sync(0xffffffffu, a1.w, k * LPE);
         }
-        if (sub == 0) epilogue8(p, row, lin, a0, a1);
+        if (sub == 0 && 2 * lin < static_cast<int>(p.c4)) epilogue8(p, row, lin, a0, a1);
     }
 }
 
@@ -738,7 +738,7 @@ __global__ void __launch_bounds__(256, MINB) aggregate_rows_p24(const AggParams 
                 add4(a1, x1);
             }
         }
-        epilogue8(p, row, lin, a0, a1);
+        if (2 * lin < static_cast<int>(p.c4)) epilogue8(p, row, lin, a0, a1);
     }
 }
 
@@ -789,6 +789,16 @@ int launch_p24(const AggParams& p, int variant, cudaStream_t s) {
         const char* e = std::getenv("GDX_P24_UN");
         return e && std::atoi(e) == 2;
     }();
+    // GDX_AGG_P24_WIDE: 48-wide rows on a >= 64-column pitch gathered as whole 64-wide
+    // rows by the 8-lane kernels (16 lanes per 4 rows instead of 6-lane groups that leave
+    // a quarter of the warp idle); columns >= width are summed but never stored.
+    // Measured (Reddit, tools/agg24_bench.py): 6-lane row groups 1.38 ms, 6-lane warp per
+    // row 1.66 ms.
+    if (variant == GDX_AGG_P24_WIDE && c8 == 6) {
+        if (minb >= 6) vec(aggregate_p24<8, 4, 6>, 4);
+        else vec(aggregate_p24<8, 4, 4>, 4);
+        return 0;
+    }
     if (c8 == 8 && un2 && !rows) {
         if (minb >= 8) vec(aggregate_p24<8, 2, 8>, 4);
         else if (minb >= 6) vec(aggregate_p24<8, 2, 6>, 4);
@@ -1147,6 +1157,9 @@ int aggregate_impl(const gdx_aggregate_args* a, int variant, gdx_stream stream) 
                         (!a->partial || (a->ld_partial % 4 == 0 && aligned16(a->partial))) &&
                         (!a->out || (a->ld_out % 4 == 0 && aligned16(a->out))),
                     GDX_INPUT, "gdx_aggregate: packed-24 epilogue operands must be 16-byte rows");
+        GDX_REQUIRE(variant != GDX_AGG_P24_WIDE ||
+                        (a->src_lo8 && a->width == 48 && a->ld_src >= 64 && p.ld_lo8 >= 64),
+                    GDX_INPUT, "gdx_aggregate: GDX_AGG_P24_WIDE needs 48-wide packed-24 rows on a 64-column pitch");
         GDX_REQUIRE(launch_p24(p, variant, as_cuda(stream)) == 0, GDX_INPUT,
                     "gdx_aggregate: packed-24 width must be 8, 16, 32, 48, 64, 96, 128 or 256");
         note_launch();

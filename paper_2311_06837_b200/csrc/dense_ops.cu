@@ -359,7 +359,9 @@ __global__ void __launch_bounds__(256) softmax_xent_vec(const float* __restrict_
                                                         const int32_t* __restrict__ labels, float inv_count,
                                                         const float* __restrict__ row_scale, float* gs,
                                                         uint64_t ld_gs, uint16_t* g_hi, uint16_t* g_lo,
-                                                        uint64_t ld_g, uint32_t out_cols, double* loss_sum) {
+                                                        uint64_t ld_g, uint32_t out_cols, double* loss_sum,
+                                                        uint16_t* gs24_hi, uint8_t* gs24_lo, uint64_t ld24_hi,
+                                                        uint64_t ld24_lo) {
     constexpr int RPW = 32 / GL;
     const int lane = threadIdx.x & 31;
     const int sub = lane / GL, gl = lane - sub * GL;
@@ -400,6 +402,16 @@ __global__ void __launch_bounds__(256) softmax_xent_vec(const float* __restrict_
         if (c0 < out_cols) {
             if (gs)
                 *reinterpret_cast<float4*>(gs + r * ld_gs + c0) = make_float4(g[0] * rs, g[1] * rs, g[2] * rs, g[3] * rs);
+            if (gs24_hi) {  // gs as packed-24 rows (interleaved planes, trainer.cu Mat::p24)
+                ushort4 hh;
+                uchar4 ll;
+                pack24(g[0] * rs, hh.x, ll.x);
+                pack24(g[1] * rs, hh.y, ll.y);
+                pack24(g[2] * rs, hh.z, ll.z);
+                pack24(g[3] * rs, hh.w, ll.w);
+                *reinterpret_cast<ushort4*>(gs24_hi + r * ld24_hi + c0) = hh;
+                *reinterpret_cast<uchar4*>(gs24_lo + r * ld24_lo + c0) = ll;
+            }
             if (g_hi) {
                 ushort4 hh, ll;
                 split_bf16(g[0], hh.x, ll.x);
@@ -423,13 +435,17 @@ __global__ void __launch_bounds__(256) softmax_xent_vec(const float* __restrict_
 bool softmax_vec_launch(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes, const int32_t* labels,
                         float inv_count, float* dlogits, const float* row_scale, float* gs, uint64_t ld_gs,
                         uint16_t* g_hi, uint16_t* g_lo, uint64_t ld_g, double* loss_sum, uint32_t npeers,
-                        cudaStream_t st) {
+                        cudaStream_t st, uint16_t* gs24_hi = nullptr, uint8_t* gs24_lo = nullptr,
+                        uint64_t ld24_hi = 0, uint64_t ld24_lo = 0) {
     auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
     auto a8 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 7) == 0; };
     if (dlogits || npeers || classes > 128 || ld % 4 || !a16(logits)) return false;
     const uint32_t cols = (classes + 3) / 4 * 4;  // whole float4 groups written
     if (gs && (ld_gs % 4 || !a16(gs) || ld_gs < cols)) return false;
     if (g_hi && (ld_g % 4 || !a8(g_hi) || !a8(g_lo) || ld_g < cols)) return false;
+    if (gs24_hi && (ld24_hi % 4 || ld24_lo % 4 || !a8(gs24_hi) || (reinterpret_cast<uintptr_t>(gs24_lo) & 3) ||
+                    ld24_hi < cols || ld24_lo < cols))
+        return false;
     const uint64_t rpb = classes <= 64 ? 16 : 8;  // rows per 256-thread block and step
     // grid-stride with a bounded grid: the loss is one fp64 atomic per warp, and
     // ~10^6 atomics on one address would serialise
@@ -437,10 +453,12 @@ bool softmax_vec_launch(const float* logits, uint64_t ld, uint32_t rows, uint32_
     if (blocks > static_cast<uint64_t>(device_sms()) * 8) blocks = static_cast<uint64_t>(device_sms()) * 8;
     if (classes <= 64)
         softmax_xent_vec<16><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-            logits, ld, rows, classes, labels, inv_count, row_scale, gs, ld_gs, g_hi, g_lo, ld_g, cols, loss_sum);
+            logits, ld, rows, classes, labels, inv_count, row_scale, gs, ld_gs, g_hi, g_lo, ld_g, cols, loss_sum,
+            gs24_hi, gs24_lo, ld24_hi, ld24_lo);
     else
         softmax_xent_vec<32><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-            logits, ld, rows, classes, labels, inv_count, row_scale, gs, ld_gs, g_hi, g_lo, ld_g, cols, loss_sum);
+            logits, ld, rows, classes, labels, inv_count, row_scale, gs, ld_gs, g_hi, g_lo, ld_g, cols, loss_sum,
+            gs24_hi, gs24_lo, ld24_hi, ld24_lo);
     return true;
 }
 
@@ -476,6 +494,25 @@ extern "C" int gdx_softmax_xent_fused(const float* logits, uint64_t ld, uint32_t
     }
     note_launch();
     return check_launch("gdx_softmax_xent_fused");
+}
+
+extern "C" int gdx_softmax_xent_fused_p24(const float* logits, uint64_t ld, uint32_t rows, uint32_t classes,
+                                          const int32_t* labels, float inv_count, const float* row_scale,
+                                          uint16_t* gs_hi24, uint64_t ld_hi24, uint8_t* gs_lo8, uint64_t ld_lo8,
+                                          uint16_t* g_hi,
+                                          uint16_t* g_lo, uint64_t ld_g, double* loss_sum, gdx_stream stream) {
+    GDX_REQUIRE(logits && labels && loss_sum && gs_hi24 && gs_lo8, GDX_INPUT,
+                "gdx_softmax_xent_fused_p24: null pointer");
+    GDX_REQUIRE(!g_hi == !g_lo, GDX_INPUT, "gdx_softmax_xent_fused_p24: g_hi/g_lo must pair");
+    GDX_REQUIRE(classes >= 1, GDX_INPUT, "gdx_softmax_xent_fused_p24: classes must be >= 1");
+    if (!rows) return GDX_OK;
+    GDX_REQUIRE(softmax_vec_launch(logits, ld, rows, classes, labels, inv_count, nullptr, row_scale, nullptr, 0, g_hi,
+                                   g_lo, ld_g, loss_sum, 0, as_cuda(stream), gs_hi24, gs_lo8, ld_hi24, ld_lo8),
+                GDX_INPUT,
+                "gdx_softmax_xent_fused_p24: needs classes <= 128, 16-byte logits rows and packed-24 pitches "
+                "(multiples of 4, >= classes rounded to 4)");
+    note_launch();
+    return check_launch("gdx_softmax_xent_fused_p24");
 }
 
 extern "C" int gdx_softmax_xent_fused_peers(const float* logits, uint64_t ld, uint32_t rows,

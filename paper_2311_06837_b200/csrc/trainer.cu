@@ -219,6 +219,13 @@ int agg_variant(uint32_t width, uint64_t nnz, uint64_t rows) {
     if (rows && deg < 20.0) return GDX_AGG_ROWS2;
     return pad4(width) == 48 ? GDX_AGG_ROWS : 0;
 }
+bool p24_wide() {  // GDX_P24_WIDE=0: 48-wide packed-24 rows through the 6-lane row groups
+    static const bool on = [] {
+        const char* e = std::getenv("GDX_P24_WIDE");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
 uint32_t splitk_eff(uint32_t split_k, uint64_t k) {
     const uint64_t kb = (k + 63) / 64;
     if (kb <= 1) return 1;
@@ -316,7 +323,12 @@ int aggregate(gdx_trainer* t, const Mat& src, uint32_t width, uint32_t rows, con
         TR_CUDA(cudaEventCreate(&e1));
         TR_CUDA(cudaEventRecord(e0, t->stream));
     }
-    TR_OK(gdx_aggregate_balanced(&a, agg_variant(width, t->nnz, t->nloc), t->bins,
+    int variant = agg_variant(width, t->nnz, t->nloc);
+    // 48-wide packed-24 rows live on a 64-column pitch: gathered whole by the 8-lane kernel
+    if (src.p24 && width == 48 && src.ld >= 64 && variant == GDX_AGG_ROWS && t->nloc &&
+        static_cast<double>(t->nnz) / static_cast<double>(t->nloc) >= 20.0 && p24_wide())
+        variant = GDX_AGG_P24_WIDE;
+    TR_OK(gdx_aggregate_balanced(&a, variant, t->bins,
                                  reinterpret_cast<gdx_stream>(t->stream)));
     if (t->profile) {
         TR_CUDA(cudaEventRecord(e1, t->stream));
@@ -607,10 +619,16 @@ int epoch_body(gdx_trainer* t) {
                                      nullptr, nullptr, 0, last.Gl.hi, last.Gl.lo, last.Gl.ld, t->loss_acc, s));
     } else {
         GradTargets gt = grad_targets(t, t->L - 1);
-        if (gt.own.p24) return err(GDX_INTERNAL, "softmax: packed-24 gradient rows");
-        TR_OK(gdx_softmax_xent_fused(last.Hout.p, last.Hout.ld, t->loss_rows, t->classes, t->labels, inv, nullptr, 0,
-                                     gt.scale, gt.own.p, gt.own.ld, gt.split ? gt.split->hi : nullptr,
-                                     gt.split ? gt.split->lo : nullptr, gt.split ? gt.split->ld : 0, t->loss_acc, s));
+        if (gt.own.p24)
+            TR_OK(gdx_softmax_xent_fused_p24(last.Hout.p, last.Hout.ld, t->loss_rows, t->classes, t->labels, inv,
+                                             gt.scale, gt.own.hi24(), 3 * gt.own.ld / 2, gt.own.lo24(), 3 * gt.own.ld,
+                                             gt.split ? gt.split->hi : nullptr, gt.split ? gt.split->lo : nullptr,
+                                             gt.split ? gt.split->ld : 0, t->loss_acc, s));
+        else
+            TR_OK(gdx_softmax_xent_fused(last.Hout.p, last.Hout.ld, t->loss_rows, t->classes, t->labels, inv,
+                                         nullptr, 0, gt.scale, gt.own.p, gt.own.ld,
+                                         gt.split ? gt.split->hi : nullptr, gt.split ? gt.split->lo : nullptr,
+                                         gt.split ? gt.split->ld : 0, t->loss_acc, s));
         TR_OK(publish(t, gt.own.p, t->nloc * last.dfull.row_bytes()));
     }
     return backward_and_step(t);
@@ -720,12 +738,25 @@ int setup_model(gdx_trainer* t) {
     // packed-24 gathered rows (cfg.packed24) for 64k-wide transform-first layers: Z from
     // the forward GEMM's epilogue, dZ from the dH GEMM's (not from the softmax or
     // grad_prepare kernels, which write fp32)
+    // grad_prepare kernels, which write fp32).  A 64k+48-wide layer (the 41-class output
+    // layer) keeps a 64k+64 plane pitch -- the same bytes as its fp32 rows -- so a gathered
+    // row is 3 + 2 aligned sectors instead of 6 (GDX_P24_48=0 keeps those layers fp32);
+    // its dZ comes out of the softmax kernel (gdx_softmax_xent_fused_p24).
     const bool p24_ok = t->cfg.packed24 && !t->cfg.fused_exchange && (!t->bins || t->bins->n_heavy == 0);
+    static const bool p24_48 = [] {
+        const char* e = std::getenv("GDX_P24_48");
+        return !e || std::atoi(e) != 0;
+    }();
     for (uint32_t l = 0; l < t->L && p24_ok; ++l) {
         Layer& Ly = t->layers[l];
-        if (Ly.agg_first || Ly.w % 64 != 0) continue;
+        const bool w48 = Ly.w % 64 == 48 && p24_48;
+        if (Ly.agg_first || (Ly.w % 64 != 0 && !w48)) continue;
+        const uint64_t ld24 = w48 ? Ly.w + 16 : Ly.Zfull.ld;
         Ly.Zfull.p24 = 1;
-        Ly.dfull.p24 = l + 1 < t->L && !t->layers[l + 1].agg_first;
+        Ly.Zfull.ld = ld24;
+        const bool last = l + 1 == t->L;
+        Ly.dfull.p24 = last ? t->classes <= 128 && t->classes <= Ly.w : !t->layers[l + 1].agg_first;
+        if (Ly.dfull.p24) Ly.dfull.ld = ld24;
     }
     if (!t->subgraph && t->world > 1) {
         uint32_t wmax = 0;

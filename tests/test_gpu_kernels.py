@@ -464,3 +464,40 @@ def test_softmax_xent_fused(gdx, cuda, classes, ld):
     close(sp.to_float()[:, :classes].double().cpu().numpy(), g)
     close(gs[:, :classes].double().cpu().numpy(), g * sc[:, None])
     assert float(gs[:, classes:].abs().max().item() if ld > classes else 0.0) == 0.0
+
+
+@pytest.mark.parametrize("classes,ld", [(41, 64), (47, 64), (8, 8), (64, 64), (100, 128)])
+def test_softmax_xent_fused_p24(gdx, cuda, classes, ld):
+    """Packed-24 gs (the trainer's interleaved rows: u16 high plane then u8 low plane,
+    3 ld bytes per row) is the fp32 gs of gdx_softmax_xent_fused rounded by gdx_pack24:
+    bit-exact; the split copy and the loss are unchanged."""
+    import torch
+    from paper_2311_06837_b200._lib import call
+    rng = np.random.default_rng(classes + 1000)
+    n = 2999
+    z = rng.normal(0, 2, (n, classes)).astype(np.float32)
+    y = rng.integers(0, classes, n).astype(np.int32)
+    sc = rng.uniform(0.5, 2, n).astype(np.float32)
+    Z = torch.zeros(n, (classes + 3) // 4 * 4, device=cuda)
+    Z[:, :classes] = torch.from_numpy(z).to(cuda)
+    Y, S = torch.from_numpy(y).to(cuda), torch.from_numpy(sc).to(cuda)
+    gs = torch.zeros(n, ld, device=cuda)
+    sp, sp24 = gdx.Split(n, ld, cuda), gdx.Split(n, ld, cuda)
+    loss, loss24 = (torch.zeros(1, dtype=torch.float64, device=cuda) for _ in range(2))
+    call("gdx_softmax_xent_fused", Z.data_ptr(), Z.shape[1], n, classes, Y.data_ptr(), 1.0 / n, None, 0,
+         S.data_ptr(), gs.data_ptr(), ld, sp.hi.data_ptr(), sp.lo.data_ptr(), sp.ld, loss.data_ptr(),
+         gdx.stream_handle())
+    rows = torch.zeros(n, 3 * ld, dtype=torch.uint8, device=cuda)  # interleaved packed-24 rows
+    base = rows.data_ptr()
+    call("gdx_softmax_xent_fused_p24", Z.data_ptr(), Z.shape[1], n, classes, Y.data_ptr(), 1.0 / n, S.data_ptr(),
+         base, 3 * ld // 2, base + 2 * ld, 3 * ld, sp24.hi.data_ptr(), sp24.lo.data_ptr(), sp24.ld,
+         loss24.data_ptr(), gdx.stream_handle())
+    hi = torch.empty(n, ld, dtype=torch.int16, device=cuda)
+    lo = torch.empty(n, ld, dtype=torch.uint8, device=cuda)
+    call("gdx_pack24", gs.data_ptr(), ld, n, ld, hi.data_ptr(), lo.data_ptr(), ld, gdx.stream_handle())
+    torch.cuda.synchronize()
+    got = rows.cpu().numpy()
+    assert np.array_equal(got[:, :2 * ld].view(np.int16), hi.cpu().numpy())
+    assert np.array_equal(got[:, 2 * ld:], lo.cpu().numpy())
+    assert torch.equal(sp.hi, sp24.hi) and torch.equal(sp.lo, sp24.lo)
+    assert float(loss.item()) == pytest.approx(float(loss24.item()), rel=1e-12)

@@ -149,10 +149,12 @@ def test_cxx_host_program_runs_the_epoch(cuda):
     assert abs(got[0] - lo) <= 1e-3
 
 
-@pytest.mark.parametrize("kind,dims", [("sage", [128, 64, 64, 41]), ("gcn", [48, 64, 64, 10])])
+@pytest.mark.parametrize("kind,dims", [("sage", [128, 64, 64, 41]), ("gcn", [48, 64, 64, 10]),
+                                       ("gcn", [48, 64, 64, 47])])
 def test_native_packed24_matches_oracle_and_fp32(cuda, kind, dims):
-    """cfg.packed24: the 64-wide gathered Z / dZ rows stored packed-24 (written by the
-    forward GEMM and the fused dH GEMM epilogues, read by the packed-24 aggregation).
+    """cfg.packed24: the 64- and 48-wide gathered Z / dZ rows stored packed-24 (written by
+    the forward GEMM and the fused dH GEMM epilogues and, for the output layer's dZ, the
+    softmax kernel; read by the packed-24 aggregation).
     Losses stay within the oracle tolerance and within 24-bit rounding of the fp32 rows."""
     import paper_2311_06837_b200 as G
     from paper_2311_06837_b200.native import NativeTrainer

@@ -64,6 +64,27 @@ def main():
                 return float(np.median([a.elapsed_time(b) for a, b in ev]))
 
             t32, t24 = timed(run32), timed(run24)
+            extra = {}
+            if w == 48:  # 48 values on a 64-element plane pitch: 3 + 2 aligned sectors per row
+                hi64 = torch.zeros((n, 64), dtype=torch.int16, device=d)
+                lo64 = torch.zeros((n, 64), dtype=torch.uint8, device=d)
+                hi64[:, :w] = hi
+                lo64[:, :w] = lo
+                out64 = dense(n, w, d)
+                for v in (0, 1, 16):
+                    def run64(v=v):
+                        a = AggregateArgs()
+                        a.row_ptr, a.col, a.rows, a.width = dg.row_ptr.data_ptr(), dg.col.data_ptr(), n, w
+                        a.src, a.ld_src, a.src_lo8 = hi64.data_ptr(), 64, lo64.data_ptr()
+                        a.ld_src_lo8 = 64
+                        a.self_coef = 1.0
+                        a.out, a.ld_out = out64.data_ptr(), out64.shape[1]
+                        call("gdx_aggregate_variant", _lib.C.byref(a), v, stream_handle())
+                    extra[f"p24_pitch64_v{v}_ms"] = round(timed(run64), 4)
+                    r24 = out24[:, :w].double()
+                    extra[f"p24_pitch64_v{v}_err"] = float(((out64[:, :w].double() - r24).abs() /
+                                                            (r24.abs() + float(r24.pow(2).mean().sqrt()))).max())
+                del hi64, lo64, out64
             ref = out32[:, :w].double()
             rms = float(ref.pow(2).mean().sqrt())
             err_same = float(((out24[:, :w].double() - ref).abs() / (ref.abs() + rms)).max())
@@ -75,7 +96,7 @@ def main():
             res.append({"graph": name, "width": w, "fp32_ms": round(t32, 4), "p24_ms": round(t24, 4),
                         "speedup": round(t32 / t24, 3), "fp32_GBps": round(alg32 / t32 / 1e6, 1),
                         "p24_GBps": round(alg24 / t24 / 1e6, 1), "err_vs_same_values": err_same,
-                        "err_vs_fp32_inputs": err_fp32, "minb": os.environ.get("GDX_P24_MINB", "6")})
+                        "err_vs_fp32_inputs": err_fp32, "minb": os.environ.get("GDX_P24_MINB", "6"), **extra})
             del src, hi, lo, src24, out32, out24
         del dg, g
         torch.cuda.empty_cache()
