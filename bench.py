@@ -286,6 +286,32 @@ def probe_l2_peak(torch, dev):
     return best
 
 
+def probe_gather_ceiling(torch, dev, packed24: bool, mbytes: int = 44):
+    """Live ceiling of the aggregation's own access pattern: random row gathers from an
+    L2-resident buffer of the gathered matrix's size class (mode 2: 192-byte packed-24
+    rows, 16 B + 8 B per lane; mode 1: 256-byte fp32 rows), no CSR. Best of 4, GB/s."""
+    from paper_2311_06837_b200._lib import call
+    from paper_2311_06837_b200.device import stream_handle
+    nbytes = mbytes << 20
+    buf = torch.randn(nbytes // 4, device=dev)
+    sink = torch.zeros(4, device=dev)
+    reps, mode = 20, (2 if packed24 else 1)
+    if mode == 2:
+        per = 8 * 2048 * torch.cuda.get_device_properties(dev).multi_processor_count * 24
+        moved = -(-reps * nbytes // per) * per
+    else:
+        moved = reps * nbytes
+    best = 0.0
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        call("gdx_probe_bandwidth", buf.data_ptr(), nbytes, reps, mode, sink.data_ptr(), stream_handle())
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, moved / e0.elapsed_time(e1) / 1e6)
+    return best
+
+
 def load_traffic(config: str, key: str = "aggregate"):
     """DRAM bytes per launch of the dominant kernel for THIS config, from the committed
     ncu --set full capture summary (profiles/ncu_traffic.json); None if that config
@@ -691,6 +717,7 @@ def main():
                                   "fp32 inputs are re-sent every step"}
 
     l2_peak = probe_l2_peak(torch, dev)
+    gather_peak = probe_gather_ceiling(torch, dev, packed24)
     hbm_pass = hbm_regime_pass(torch, dev) if (rank == 0 and args.config == "reddit-sage"
                                                and not args.no_hbm_pass) else None
     edges_total = g.num_edges()
@@ -703,7 +730,7 @@ def main():
     agg_avg_ms = (agg_ms_total / agg_launches) if agg_launches else None
     achieved = (agg_bytes / agg_launches) / (agg_avg_ms * 1e-3) / 1e9 if agg_launches else None
     nrows_gather = tr.info()[3]
-    gathered_bytes = nrows_gather * max(agg_width(d, nrows_gather) for d in cfg.dims[1:]) * 4
+    gathered_bytes = nrows_gather * max(agg_width(d, nrows_gather) for d in cfg.dims[1:]) * (3 if packed24 else 4)
     l2_resident = gathered_bytes <= L2_RESIDENT_BYTES
     traffic, traffic_src = load_traffic(args.config)
 
@@ -731,7 +758,8 @@ def main():
             "avg_launch_ms": round(agg_avg_ms, 4) if agg_avg_ms else None,
             "launches_per_step": int(agg_launches / max(args.steps, 1)),
             "share_of_step": round(agg_ms_step / ms, 3) if ms else None,
-            "note": ("bytes = 4 nnz + 8 (rows+1) + 4 F nnz + 4 F rows per launch (SURVEY §8d), "
+            "note": ("bytes = 4 nnz + 8 (rows+1) + b F nnz + 4 F rows per launch (SURVEY §8d; b = 4 "
+                     "for fp32 rows, 3 for packed-24 rows), "
                      "timed on the trainer's stream over K eager epochs. "
                      + (f"The gathered matrix ({gathered_bytes / 1e6:.0f} MB) is L2-resident, so the "
                         f"binding ceiling is L2 read bandwidth (frac vs the live L2 probe); vs HBM "
@@ -743,6 +771,16 @@ def main():
                               "frac": hbm_frac,
                               "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
             "l2_probe_gbs": round(l2_peak, 1),
+            "gather_ceiling": None if not l2_resident else {
+                "achieved": round(achieved, 1) if achieved else None,
+                "peak": round(gather_peak, 1), "unit": "GB/s",
+                "frac": round(achieved / gather_peak, 4) if achieved else None,
+                "peak_source": ("live probe in this run: gdx_probe_bandwidth mode "
+                                + ("2, random 192-byte packed-24 rows (16 B + 8 B per lane, 8 lanes "
+                                   "per row)" if packed24 else "1, random 256-byte fp32 rows")
+                                + " from a 44 MiB L2-resident buffer, no CSR (best of 4)"),
+                "note": "the ceiling of the kernel's own access pattern (random whole-row "
+                        "gathers), below the coalesced-stream L2 probe"},
         }
         if hbm_pass is not None:
             roof["hbm_regime"] = hbm_pass

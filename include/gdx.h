@@ -338,7 +338,10 @@ int gdx_softmax_xent_fused_peers(const float* logits, uint64_t ld, uint32_t rows
                                  const int64_t* gs_peer_delta, gdx_stream stream);
 /* Bandwidth probe for roofline denominators: reads `bytes` of buf `reps` times,
  * mode 0 = coalesced stream, mode 1 = random 256 B row gathers (bytes moved =
- * reps * bytes in both modes).  Time it with events on `stream`. */
+ * reps * bytes in both modes), mode 2 = random 192 B packed-24 row gathers (16 B + 8 B
+ * per lane, 8 lanes per row; bytes moved = steps * 8 * T * 24 with T = 2048 * SMs
+ * threads and steps = ceil(reps * bytes / (8 * T * 24))).  Time it with events on
+ * `stream`. */
 /* L2 access-policy window (persisting) on `stream` for the matrix the next kernels gather
  * (bytes = 0 clears it); carves the device's persisting L2 set-aside on first use. */
 int gdx_set_l2_window(const void* base, uint64_t bytes, float hit_ratio, gdx_stream stream);

@@ -208,8 +208,8 @@ __global__ void splitk_reduce_kernel(const float* ws, uint32_t split_k, uint64_t
 }
 
 // Bandwidth probe (roofline denominators): mode 0 streams the buffer with 16 B
-// loads (coalesced), mode 1 gathers random 256 B rows (the aggregation's access
-// pattern without the CSR).  The buffer is L2-resident when it fits.
+// loads (coalesced), mode 1 gathers random 256 B rows (the fp32 aggregation's access
+// pattern without the CSR), mode 2 random 192 B packed-24 rows.  The buffer is L2-resident when it fits.
 __global__ void __launch_bounds__(256) probe_kernel(const float4* __restrict__ buf, uint64_t n4,
                                                     uint32_t reps, int mode, float* sink) {
     constexpr int U = 8;  // independent 16 B loads in flight per thread
@@ -227,6 +227,36 @@ __global__ void __launch_bounds__(256) probe_kernel(const float4* __restrict__ b
                     acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
                 }
             }
+    } else if (mode == 2) {
+        // packed-24 row gathers: random 192-byte rows (a 64-wide packed-24 row), 8 lanes
+        // per row, each lane a 16 B load of the u16 plane + an 8 B load of the u8 plane --
+        // the access pattern of aggregate_p24 without the CSR.  24 B per thread per load pair;
+        // steps rounded up so a thread moves >= reps * bytes / nthreads (the caller counts
+        // steps * U * nthreads * 24 bytes).
+        const uint64_t rows = n4 * 16 / 192;
+        const int lane8 = threadIdx.x & 7;
+        const char* base = reinterpret_cast<const char*>(buf);
+        uint64_t h = (tid >> 3) * 0x9e3779b97f4a7c15ULL + 1;
+        const uint64_t per = static_cast<uint64_t>(U) * nthreads * 24;
+        const uint64_t steps = (reps * n4 * 16 + per - 1) / per;
+        for (uint64_t k = 0; k < steps; ++k) {
+            uint4 v[U];
+            uint2 w[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                h = h * 6364136223846793005ULL + 1442695040888963407ULL;
+                const char* r = base + ((h >> 33) % rows) * 192;
+                v[u] = __ldcg(reinterpret_cast<const uint4*>(r + 16 * lane8));
+                w[u] = __ldcg(reinterpret_cast<const uint2*>(r + 128 + 8 * lane8));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                acc.x += __uint_as_float(v[u].x ^ w[u].x);
+                acc.y += __uint_as_float(v[u].y ^ w[u].y);
+                acc.z += __uint_as_float(v[u].z);
+                acc.w += __uint_as_float(v[u].w);
+            }
+        }
     } else {
         const uint64_t rows = n4 / 16;  // 256-byte rows, 16 lanes per row
         const int lane16 = threadIdx.x & 15;
