@@ -233,10 +233,12 @@ __global__ void __launch_bounds__(256) probe_kernel(const float4* __restrict__ b
         // the access pattern of aggregate_p24 without the CSR.  24 B per thread per load pair;
         // steps rounded up so a thread moves >= reps * bytes / nthreads (the caller counts
         // steps * U * nthreads * 24 bytes).
-        const uint64_t rows = n4 * 16 / 192;
+        // row ids: a 32-bit LCG per 8-lane group mapped onto [0, rows) by a multiply-high
+        // (no 64-bit modulo: the probe must stay load-bound, not integer-bound)
+        const uint32_t rows = static_cast<uint32_t>(n4 * 16 / 192);
         const int lane8 = threadIdx.x & 7;
         const char* base = reinterpret_cast<const char*>(buf);
-        uint64_t h = (tid >> 3) * 0x9e3779b97f4a7c15ULL + 1;
+        uint32_t h = static_cast<uint32_t>(tid >> 3) * 2654435761u + 12345u;
         const uint64_t per = static_cast<uint64_t>(U) * nthreads * 24;
         const uint64_t steps = (reps * n4 * 16 + per - 1) / per;
         for (uint64_t k = 0; k < steps; ++k) {
@@ -244,8 +246,8 @@ __global__ void __launch_bounds__(256) probe_kernel(const float4* __restrict__ b
             uint2 w[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                h = h * 6364136223846793005ULL + 1442695040888963407ULL;
-                const char* r = base + ((h >> 33) % rows) * 192;
+                h = h * 1664525u + 1013904223u;
+                const char* r = base + static_cast<uint64_t>(__umulhi(h, rows)) * 192;
                 v[u] = __ldcg(reinterpret_cast<const uint4*>(r + 16 * lane8));
                 w[u] = __ldcg(reinterpret_cast<const uint2*>(r + 128 + 8 * lane8));
             }

@@ -9,7 +9,10 @@ import re
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-SRC = os.path.join(ROOT, "gpurun_out", "prof2")
+import sys
+# usage: summarize.py [src dir under gpurun_out] [tag]   (defaults: prof2 r02)
+SRC = os.path.join(ROOT, "gpurun_out", sys.argv[1] if len(sys.argv) > 1 else "prof2")
+TAG = sys.argv[2] if len(sys.argv) > 2 else "r02"
 OUT = os.path.join(ROOT, "profiles")
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-6, "us": 1e-3, "ms": 1.0,
         "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6}
@@ -41,7 +44,7 @@ def launches():
              f"{'kernel':60s} {'launches':>8s} {'ms':>9s} {'share':>7s}"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"{k[:60]:60s} {cnt[k]:8d} {v:9.3f} {v / all_ms:7.1%}")
-    open(os.path.join(OUT, "r02_launches.txt"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(OUT, f"{TAG}_launches.txt"), "w").write("\n".join(lines) + "\n")
 
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -93,11 +96,15 @@ def full():
             sel = [a for a in agg if a[0] == top]
             traffic[t] = {"kernel": top, "launches": len(sel),
                           "dram_bytes_per_launch": int(sum(a[1] for a in sel) / len(sel) * 1e9),
-                          "source": f"profiles/r02_ncu_full.txt ({t})"}
-    open(os.path.join(OUT, "r02_ncu_full.txt"), "w").write("\n".join(lines) + "\n")
+                          "source": f"profiles/{TAG}_ncu_full.txt ({t})"}
+    open(os.path.join(OUT, f"{TAG}_ncu_full.txt"), "w").write("\n".join(lines) + "\n")
     names = {"reddit": "reddit-sage", "products": "products-gcn", "hbm": "hbm-regime-products64",
              "cobatch": "papers-cobatch"}
-    out = {names[k]: {"aggregate": v} for k, v in traffic.items()}
+    try:  # keep the configs this capture did not cover
+        out = json.load(open(os.path.join(OUT, "ncu_traffic.json")))
+    except Exception:
+        out = {}
+    out.update({names[k]: {"aggregate": v} for k, v in traffic.items()})
     json.dump(out, open(os.path.join(OUT, "ncu_traffic.json"), "w"), indent=1)
     print(json.dumps(out, indent=1))
 
