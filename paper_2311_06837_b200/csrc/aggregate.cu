@@ -772,7 +772,8 @@ int launch_p24(const AggParams& p, int variant, cudaStream_t s) {
     };
     const bool rows = variant == GDX_AGG_ROWS;
     // resident blocks per SM: GDX_P24_MINB tuning knob, default 4 (60 registers, no spills;
-    // measured: Reddit 64-wide 1.22 ms at 4, 1.69 at 6, 2.61 at 8 -- tools/agg24_bench.py)
+    // measured: Reddit 64-wide 1.22 ms at 4, 1.69 at 6, 2.61 at 8 -- tools/agg24_bench.py;
+    // 5 (48-register cap, 40 warps/SM) spills at UNROLL 4: epoch 8.8 -> 9.6 ms, 10.0 at UNROLL 2)
     static const int minb = [] {
         const char* e = std::getenv("GDX_P24_MINB");
         return e ? std::atoi(e) : 4;

@@ -256,15 +256,72 @@ extern "C" int gdx_host_partition_random(uint32_t n, uint32_t parts, uint64_t se
     return GDX_OK;
 }
 
+// Gain-bucket queue for the region growth: one two-level bitmap of vertex ids per gain
+// value.  pop() returns the unassigned frontier vertex with the largest gain, ties to
+// the lowest id -- exactly the valid top of the reference's lazy priority_queue of
+// (gain, MAX - v) (partition.cpp:95-125) -- in O(1) amortised per update instead of a
+// heap push per edge (114.6 M pushes at the Reddit shape).
+class GainBuckets {
+public:
+    explicit GainBuckets(uint32_t n) : n_(n), words_((n + 63) / 64), sums_((words_ + 63) / 64) {}
+    void set(uint32_t g, uint32_t v) {
+        Level& L = level(g);
+        const uint32_t w = v >> 6;
+        if (!L.w[w]) {
+            L.s[w >> 6] |= 1ull << (w & 63);
+            if (w >> 6 < L.lo) L.lo = w >> 6;
+        }
+        L.w[w] |= 1ull << (v & 63);
+        ++L.count;
+        if (g > top_) top_ = g;
+    }
+    void clear(uint32_t g, uint32_t v) {
+        Level& L = lv_[g];
+        const uint32_t w = v >> 6;
+        L.w[w] &= ~(1ull << (v & 63));
+        if (!L.w[w]) L.s[w >> 6] &= ~(1ull << (w & 63));
+        --L.count;
+        while (top_ > 0 && lv_[top_].count == 0) --top_;
+    }
+    // lowest id at the highest non-empty gain; n if every bucket is empty
+    uint32_t top_vertex(uint32_t* g_out) {
+        if (top_ == 0) return n_;
+        Level& L = lv_[top_];
+        while (!L.s[L.lo]) ++L.lo;
+        const uint32_t w = (L.lo << 6) + static_cast<uint32_t>(__builtin_ctzll(L.s[L.lo]));
+        *g_out = top_;
+        return (w << 6) + static_cast<uint32_t>(__builtin_ctzll(L.w[w]));
+    }
+private:
+    struct Level {
+        std::vector<uint64_t> w, s;
+        uint32_t lo = 0;
+        uint64_t count = 0;
+    };
+    Level& level(uint32_t g) {
+        if (g >= lv_.size()) lv_.resize(g + 1);
+        Level& L = lv_[g];
+        if (L.w.empty()) {
+            L.w.assign(words_, 0);
+            L.s.assign(sums_, 0);
+            L.lo = sums_;
+        }
+        return L;
+    }
+    uint32_t n_, words_, sums_, top_ = 0;
+    std::vector<Level> lv_;
+};
+
 // partition_mincut (partition.cpp:63-170): greedy region growing from high-degree
 // seeds (frontier vertex with the most edges into the region next, ties to the
 // lowest id), then <= 10 boundary-refinement passes under the size cap
-// floor(ceil(n/parts) * (1 + eps)).  Host preprocessing: deterministic and
-// sequential by construction; bit-identical assignment to the reference.
+// floor(ceil(n/parts) * (1 + eps)).  Host preprocessing, deterministic; the growth
+// order comes from GainBuckets instead of a heap, the assignment is bit-identical to
+// the reference's (tests/test_abi.py against the compiled reference).
 extern "C" int gdx_host_partition_mincut(uint32_t n, const uint64_t* ro, const uint32_t* ci,
                                          uint32_t parts, uint64_t seed, double eps,
                                          uint32_t* assignment) {
-    (void)seed;  // growth and refinement are fully deterministic (partition.cpp:67)
+    (void)seed;  // the reference ignores it: growth and refinement are deterministic
     if (parts == 0) return fail(GDX_INPUT, "partition: parts must be >= 1");
     if (parts > n)
         return fail(GDX_INPUT, "partition: parts (" + std::to_string(parts) +
@@ -280,36 +337,32 @@ extern "C" int gdx_host_partition_mincut(uint32_t n, const uint64_t* ro, const u
                      [&](uint32_t x, uint32_t y) { return deg(x) > deg(y); });
     size_t seed_scan = 0;
     std::vector<uint32_t> gain(n, 0), touched;
-    constexpr uint32_t kMax = std::numeric_limits<uint32_t>::max();
+    GainBuckets q(n);
     for (uint32_t part = 0; part < parts; ++part) {
         const uint32_t target = base + (part < rem ? 1 : 0);
-        uint32_t taken = 0;
-        std::priority_queue<std::pair<uint32_t, uint32_t>> frontier;  // (gain, MAX - v)
-        while (taken < target) {
-            uint32_t v = n;
-            while (!frontier.empty()) {
-                auto [g_at, key] = frontier.top();
-                frontier.pop();
-                const uint32_t cand = kMax - key;
-                if (a[cand] != unassigned || gain[cand] != g_at) continue;
-                v = cand;
-                break;
-            }
-            if (v == n) {
+        for (uint32_t taken = 0; taken < target; ++taken) {
+            uint32_t g = 0;
+            uint32_t v = q.top_vertex(&g);
+            if (v == n) {  // empty frontier: next unassigned vertex by degree
                 while (a[by_degree[seed_scan]] != unassigned) ++seed_scan;
                 v = by_degree[seed_scan];
+            } else {
+                q.clear(g, v);
             }
             a[v] = part;
-            ++taken;
             for (uint64_t e = ro[v]; e < ro[v + 1]; ++e) {
                 const uint32_t u = ci[e];
                 if (a[u] != unassigned) continue;
                 if (gain[u] == 0) touched.push_back(u);
-                ++gain[u];
-                frontier.push({gain[u], kMax - u});
+                else q.clear(gain[u], u);
+                q.set(++gain[u], u);
             }
         }
-        for (uint32_t u : touched) gain[u] = 0;
+        // the next region starts from an empty frontier with all gains 0
+        for (uint32_t u : touched) {
+            if (a[u] == unassigned && gain[u]) q.clear(gain[u], u);
+            gain[u] = 0;
+        }
         touched.clear();
     }
     std::vector<uint32_t> size(parts, 0);

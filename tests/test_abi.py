@@ -95,7 +95,7 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
 
 
 @pytest.mark.parametrize("n,d,seed,parts", [(120, 6.0, 2200, 2), (10000, 10.0, 7, 2), (3000, 20.0, 1, 8),
-                                            (500, 3.0, 4, 7)])
+                                            (500, 3.0, 4, 7), (20000, 30.0, 9, 4), (2000, 1.5, 3, 5)])
 def test_host_partition_mincut_and_hierarchical_bit_exact(n, d, seed, parts):
     import oracle as O
     import paper_2311_06837_b200 as G
