@@ -257,10 +257,13 @@ extern "C" int gdx_host_partition_random(uint32_t n, uint32_t parts, uint64_t se
 }
 
 // Gain-bucket queue for the region growth: one two-level bitmap of vertex ids per gain
-// value.  pop() returns the unassigned frontier vertex with the largest gain, ties to
+// value.  An increment only sets the vertex's bit at its new gain; the bits it leaves at
+// lower gains go stale and are dropped when a pop meets them (a stale bit is never the
+// answer: the vertex's valid bit sits at a higher, non-empty gain, or it is assigned).
+// pop() therefore returns the unassigned frontier vertex with the largest gain, ties to
 // the lowest id -- exactly the valid top of the reference's lazy priority_queue of
-// (gain, MAX - v) (partition.cpp:95-125) -- in O(1) amortised per update instead of a
-// heap push per edge (114.6 M pushes at the Reddit shape).
+// (gain, MAX - v) (partition.cpp:95-125) -- with one bitmap store per edge instead of a
+// heap push.
 class GainBuckets {
 public:
     explicit GainBuckets(uint32_t n) : n_(n), words_((n + 63) / 64), sums_((words_ + 63) / 64) {}
@@ -272,25 +275,38 @@ public:
             if (w >> 6 < L.lo) L.lo = w >> 6;
         }
         L.w[w] |= 1ull << (v & 63);
-        ++L.count;
+        ++L.count;  // bits set (valid + stale); a vertex's bit per gain is set at most once
         if (g > top_) top_ = g;
     }
-    void clear(uint32_t g, uint32_t v) {
-        Level& L = lv_[g];
-        const uint32_t w = v >> 6;
-        L.w[w] &= ~(1ull << (v & 63));
-        if (!L.w[w]) L.s[w >> 6] &= ~(1ull << (w & 63));
-        --L.count;
-        while (top_ > 0 && lv_[top_].count == 0) --top_;
+    // Lowest valid id at the highest gain holding one (removed); n if none.
+    template <class Valid>
+    uint32_t pop(Valid valid) {
+        while (top_ > 0) {
+            Level& L = lv_[top_];
+            if (L.count == 0) {
+                --top_;
+                continue;
+            }
+            while (!L.s[L.lo]) ++L.lo;
+            const uint32_t w = (L.lo << 6) + static_cast<uint32_t>(__builtin_ctzll(L.s[L.lo]));
+            const uint32_t v = (w << 6) + static_cast<uint32_t>(__builtin_ctzll(L.w[w]));
+            L.w[w] &= L.w[w] - 1;  // v is the lowest bit of its word
+            if (!L.w[w]) L.s[w >> 6] &= ~(1ull << (w & 63));
+            --L.count;
+            if (valid(v, top_)) return v;
+        }
+        return n_;
     }
-    // lowest id at the highest non-empty gain; n if every bucket is empty
-    uint32_t top_vertex(uint32_t* g_out) {
-        if (top_ == 0) return n_;
-        Level& L = lv_[top_];
-        while (!L.s[L.lo]) ++L.lo;
-        const uint32_t w = (L.lo << 6) + static_cast<uint32_t>(__builtin_ctzll(L.s[L.lo]));
-        *g_out = top_;
-        return (w << 6) + static_cast<uint32_t>(__builtin_ctzll(L.w[w]));
+    // empty every bucket (a new region starts with all gains 0)
+    void reset() {
+        for (Level& L : lv_)
+            if (L.count) {
+                std::fill(L.w.begin(), L.w.end(), 0ull);
+                std::fill(L.s.begin(), L.s.end(), 0ull);
+                L.count = 0;
+                L.lo = sums_;
+            }
+        top_ = 0;
     }
 private:
     struct Level {
@@ -336,41 +352,48 @@ extern "C" int gdx_host_partition_mincut(uint32_t n, const uint64_t* ro, const u
     std::stable_sort(by_degree.begin(), by_degree.end(),
                      [&](uint32_t x, uint32_t y) { return deg(x) > deg(y); });
     size_t seed_scan = 0;
-    std::vector<uint32_t> gain(n, 0), touched;
+    // st[u]: the gain of an unassigned vertex, or kAssigned | part -- one random access
+    // per edge for the "unassigned?" test and the gain update together; neighbours'
+    // entries are prefetched a few edges ahead (the growth is latency-bound at the
+    // products shape, 2.4 M vertices)
+    constexpr uint32_t kAssigned = 0x80000000u;
+    std::vector<uint32_t> st(n, 0), touched;
     GainBuckets q(n);
+    constexpr uint64_t kAhead = 16;
     for (uint32_t part = 0; part < parts; ++part) {
         const uint32_t target = base + (part < rem ? 1 : 0);
         for (uint32_t taken = 0; taken < target; ++taken) {
-            uint32_t g = 0;
-            uint32_t v = q.top_vertex(&g);
+            uint32_t v = q.pop([&](uint32_t c, uint32_t g) { return st[c] == g; });
             if (v == n) {  // empty frontier: next unassigned vertex by degree
-                while (a[by_degree[seed_scan]] != unassigned) ++seed_scan;
+                while (st[by_degree[seed_scan]] & kAssigned) ++seed_scan;
                 v = by_degree[seed_scan];
-            } else {
-                q.clear(g, v);
             }
-            a[v] = part;
-            for (uint64_t e = ro[v]; e < ro[v + 1]; ++e) {
+            st[v] = kAssigned | part;
+            const uint64_t e1 = ro[v + 1];
+            for (uint64_t e = ro[v]; e < e1; ++e) {
+                if (e + kAhead < e1) __builtin_prefetch(&st[ci[e + kAhead]], 1, 3);
                 const uint32_t u = ci[e];
-                if (a[u] != unassigned) continue;
-                if (gain[u] == 0) touched.push_back(u);
-                else q.clear(gain[u], u);
-                q.set(++gain[u], u);
+                const uint32_t g = st[u];
+                if (g & kAssigned) continue;
+                if (g == 0) touched.push_back(u);
+                st[u] = g + 1;
+                q.set(g + 1, u);
             }
         }
         // the next region starts from an empty frontier with all gains 0
-        for (uint32_t u : touched) {
-            if (a[u] == unassigned && gain[u]) q.clear(gain[u], u);
-            gain[u] = 0;
-        }
+        for (uint32_t u : touched)
+            if (!(st[u] & kAssigned)) st[u] = 0;
         touched.clear();
+        q.reset();
     }
+    for (uint32_t v = 0; v < n; ++v) a[v] = st[v] & ~kAssigned;
     std::vector<uint32_t> size(parts, 0);
     for (uint32_t v = 0; v < n; ++v) ++size[a[v]];
     uint32_t cap = static_cast<uint32_t>(
         std::floor(static_cast<double>((n + parts - 1) / parts) * (1.0 + eps)));
     cap = std::max<uint32_t>(cap, (n + parts - 1) / parts);
     std::vector<uint64_t> conn(parts, 0);
+    const uint64_t nnz = ro[n];
     std::vector<uint32_t> tparts;
     for (int pass = 0; pass < 10; ++pass) {
         bool moved = false;
@@ -378,7 +401,9 @@ extern "C" int gdx_host_partition_mincut(uint32_t n, const uint64_t* ro, const u
             const uint32_t own = a[v];
             if (size[own] <= 1) continue;
             tparts.clear();
-            for (uint64_t e = ro[v]; e < ro[v + 1]; ++e) {
+            const uint64_t e1 = ro[v + 1];
+            for (uint64_t e = ro[v]; e < e1; ++e) {
+                if (e + kAhead < nnz) __builtin_prefetch(&a[ci[e + kAhead]], 0, 3);  // across rows
                 const uint32_t q = a[ci[e]];
                 if (conn[q] == 0) tparts.push_back(q);
                 ++conn[q];
