@@ -501,3 +501,24 @@ def test_softmax_xent_fused_p24(gdx, cuda, classes, ld):
     assert np.array_equal(got[:, 2 * ld:], lo.cpu().numpy())
     assert torch.equal(sp.hi, sp24.hi) and torch.equal(sp.lo, sp24.lo)
     assert float(loss.item()) == pytest.approx(float(loss24.item()), rel=1e-12)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_bandwidth_probe_modes(gdx, cuda, mode):
+    """The roofline probes (stream, random 256-byte rows, random 192-byte packed-24 rows)
+    run on an L2-resident buffer, reject non-4 KiB sizes, and report a plausible rate."""
+    import torch
+    from paper_2311_06837_b200._lib import call
+    from paper_2311_06837_b200.errors import InputError
+    nbytes = 8 << 20
+    buf = torch.rand(nbytes // 4, device=cuda)
+    sink = torch.zeros(4, device=cuda)
+    with pytest.raises(InputError):
+        call("gdx_probe_bandwidth", buf.data_ptr(), nbytes - 4, 1, mode, sink.data_ptr(), gdx.stream_handle())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    call("gdx_probe_bandwidth", buf.data_ptr(), nbytes, 8, mode, sink.data_ptr(), gdx.stream_handle())
+    e1.record()
+    torch.cuda.synchronize()
+    gbs = 8 * nbytes / e0.elapsed_time(e1) / 1e6
+    assert 100.0 < gbs < 100000.0, gbs
