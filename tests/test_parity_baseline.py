@@ -97,6 +97,44 @@ def test_reddit_sage_configs1_ten_epochs(cuda):
     assert np.all(np.abs(lg - lo) <= 1e-3), np.c_[lg, lo]
 
 
+def test_reddit_sage_configs1_benched_trainer_packed24(cuda):
+    """The benchmarked path itself at configs[1] full size: the C-ABI trainer with
+    packed-24 gathered rows and CUDA-graph replay (bench.py's defaults), 10 epochs
+    against the fp64 oracle on identical inputs, epoch-1 weight gradients by relative
+    Frobenius norm."""
+    import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.native import NativeTrainer
+    from paper_2311_06837_b200.train import ModelConfig
+
+    n, deg, dims, lr = 232965, 491.99, [602, 64, 64, 41], 0.1
+    g = G.gen_random_graph(n, deg, 11)
+    model = O.Model(O.SAGE, dims)
+    w0 = O.stream_weights(model.weight_shapes(), 3)
+    tr = NativeTrainer(g, ModelConfig("sage", dims, lr=lr), weights=w0, packed24=True)
+    c = O.CSR(n, g.row_offsets(), g.col_indices())
+    x = O.make_features(n, dims[0], 1).astype(np.float32).astype(np.float64)
+    labels = O.make_labels(n, dims[-1], 2)
+    w = np.concatenate([a.ravel() for a in w0])
+    lg, lo = [], []
+    for e in range(10):
+        lg.append(tr.train_epoch())
+        if e == 0:
+            l_ref, grads, _, _ = O.train_epoch(c, x, labels, model, w, lr, want_state=True, nthreads=THREADS)
+            off = 0
+            for mi, gm in enumerate(tr.get_grads()):
+                ref = grads[off:off + gm.size].reshape(gm.shape)
+                off += gm.size
+                frob_close(gm, ref, what=f"dW[{mi}]")
+            lo.append(l_ref)
+        else:
+            lo.append(O.train_epoch(c, x, labels, model, w, lr, nthreads=THREADS))
+    assert tr.graph_captured
+    tr.close()
+    lg, lo = np.array(lg), np.array(lo)
+    assert np.all(np.isfinite(lg))
+    assert np.all(np.abs(lg - lo) <= 1e-3), np.c_[lg, lo]
+
+
 def test_products_gcn_configs3_epochs(cuda):
     """BASELINE configs[3] at full size: 2,449,029 vertices, 61.9 M entries, GCN
     100-64-64-47 (the HBM-regime gathers), 4 epochs."""
@@ -125,14 +163,17 @@ def _local_graph(g, sub):
     return O.CSR(m, lro, nb[keep].astype(np.uint32)), order, hop[order]
 
 
-@pytest.mark.parametrize("server", [0, 5])
-def test_gcn56_eas_configs2_reduced(cuda, server):
+@pytest.mark.parametrize("server,trainer", [(0, "torch"), (5, "torch"), (0, "native-p24")])
+def test_gcn56_eas_configs2_reduced(cuda, server, trainer):
     """BASELINE configs[2] semantics at reduced V: 56-layer normalised GCN (He-uniform
     init, lr 1.0 as bench.py), EAS(m=1, k=15, seed 3) on an 8-server random partition
     (N_s = 8 emulated servers), one server's preloaded subgraph on the GPU, loss on
     its inner vertices, 10 epochs.  V and the degree are Reddit's / 10 (same edge
-    density p = deg / V); every layer's gradient is checked after epoch 1."""
+    density p = deg / V); every layer's gradient is checked after epoch 1.  trainer
+    "native-p24": the benchmarked C-ABI trainer with packed-24 gathered rows (bench.py's
+    configs[2] setting)."""
     import paper_2311_06837_b200 as G
+    from paper_2311_06837_b200.native import NativeTrainer
     from paper_2311_06837_b200.train import FullGraphTrainer, ModelConfig
 
     n, deg, dims, lr = 23297, 49.2, [602] + [64] * 55 + [41], 1.0
@@ -142,7 +183,10 @@ def test_gcn56_eas_configs2_reduced(cuda, server):
     cfg = ModelConfig("gcn", dims, lr=lr, init="he")
     model = O.Model(O.GCN, dims)
     w0 = O.stream_weights(model.weight_shapes(), 3, init="he")
-    tr = FullGraphTrainer(g, cfg, weights=w0, subgraph=sub)
+    if trainer == "torch":
+        tr = FullGraphTrainer(g, cfg, weights=w0, subgraph=sub)
+    else:
+        tr = NativeTrainer(g, cfg, weights=w0, subgraph=sub, packed24=True)
     lc, order, hop_sorted = _local_graph(g, sub)
     x = O.make_features(n, dims[0], 1).astype(np.float32).astype(np.float64)[order]
     lab = O.make_labels(n, dims[-1], 2)[order]
