@@ -598,7 +598,7 @@ __device__ __forceinline__ void epilogue8(const AggParams& p, uint32_t row, uint
 
 // Warp per destination row over packed-24 sources: LPE lanes x 8 values cover a row,
 // EPW rows in flight per warp step, UNROLL steps unrolled.
-template <int LPE, int UNROLL, int MINB>
+template <int LPE, int UNROLL, int MINB, bool HOLE = false>
 __global__ void __launch_bounds__(256, MINB) aggregate_p24(const AggParams p) {
     constexpr int EPW = pow2_floor(32 / LPE);
     constexpr int STEP = EPW * UNROLL;
@@ -618,18 +618,32 @@ __global__ void __launch_bounds__(256, MINB) aggregate_p24(const AggParams p) {
         const uint64_t beg = p.row_ptr[row];
         const uint64_t end = p.row_end ? p.row_end[row] : p.row_ptr[row + 1];
         float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-        const int nseg = p.skip_lo ? 2 : 1;
+        // HOLE (the exchange's remote-source pass, skip range [skip_lo, skip_hi) given):
+        // both sides of the hole are walked as ONE logical edge stream, so 32-edge chunks
+        // run across it and a row pays one partial chunk instead of two.  Otherwise the
+        // row (or each side of a skip range) is its own segment.
+        const int nseg = (!HOLE && p.skip_lo) ? 2 : 1;
         for (int seg = 0; seg < nseg; ++seg) {
-            uint64_t sbeg = beg, send = end;
-            if (p.skip_lo) {
+            uint64_t sbeg = beg, send = end, n0 = ~0ull, hole = 0;
+            if (HOLE) {
+                const uint64_t slo = p.skip_lo[row], shi = p.skip_hi[row];
+                n0 = slo;
+                hole = shi - slo;
+                send = end - hole;
+            } else if (p.skip_lo) {
                 if (seg == 0) send = p.skip_lo[row];
                 else sbeg = p.skip_hi[row];
             }
-            uint32_t my = (sbeg + lane < send) ? ld_stream_u32(p.col + sbeg + lane, pol_stream) : 0u;
+            // logical edge e -> physical e (+ hole past skip_lo)
+            uint32_t my = (sbeg + lane < send)
+                              ? ld_stream_u32(p.col + sbeg + lane + (HOLE && sbeg + lane >= n0 ? hole : 0), pol_stream)
+                              : 0u;
             for (uint64_t e0 = sbeg; e0 < send; e0 += 32) {
                 const uint32_t cnt = static_cast<uint32_t>((send - e0) < 32 ? (send - e0) : 32);
                 const uint64_t e1 = e0 + 32;
-                const uint32_t nxt = (e1 + lane < send) ? ld_stream_u32(p.col + e1 + lane, pol_stream) : 0u;
+                const uint32_t nxt = (e1 + lane < send)
+                                         ? ld_stream_u32(p.col + e1 + lane + (HOLE && e1 + lane >= n0 ? hole : 0), pol_stream)
+                                         : 0u;
                 uint32_t j = 0;
                 for (; j + STEP <= cnt; j += STEP) {
                     uint4 h[UNROLL];
@@ -795,9 +809,17 @@ int launch_p24(const AggParams& p, int variant, cudaStream_t s) {
     // a quarter of the warp idle); columns >= width are summed but never stored.
     // Measured (Reddit, tools/agg24_bench.py): 6-lane row groups 1.38 ms, 6-lane warp per
     // row 1.66 ms.
+    // the exchange's remote-source pass (skip range): one edge stream across the hole
+    // (N=2: 4.95 -> 4.88 ms, N=4: 2.66 -> 2.63 ms per Reddit epoch, tools/r02/hole_ab.sh)
+    const bool hole = p.skip_lo && minb < 6 && !un2 && !rows;
     if (variant == GDX_AGG_P24_WIDE && c8 == 6) {
         if (minb >= 6) vec(aggregate_p24<8, 4, 6>, 4);
+        else if (hole) vec(aggregate_p24<8, 4, 4, true>, 4);
         else vec(aggregate_p24<8, 4, 4>, 4);
+        return 0;
+    }
+    if (c8 == 8 && hole) {
+        vec(aggregate_p24<8, 4, 4, true>, 4);
         return 0;
     }
     if (c8 == 8 && un2 && !rows) {
