@@ -689,6 +689,17 @@ def main():
     e2e = None
     if not args.no_e2e:
         xh, lh = host_inputs(torch, dev, tr, g, C)
+        # this box's pinned H2D rate for the same bytes, measured alone (the e2e floor)
+        probe = torch.empty(xh.numel(), dtype=torch.float32, device=dev)
+        h2d_alone_ms = float("inf")
+        for _ in range(3):
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record()
+            probe.copy_(xh.reshape(-1), non_blocking=True)
+            p1.record()
+            torch.cuda.synchronize()
+            h2d_alone_ms = min(h2d_alone_ms, p0.elapsed_time(p1))
+        del probe
         for _ in range(2):   # untimed warm-up of the staged path (staging buffers, copy stream)
             tr.stage_inputs(None, x_ptr=xh.data_ptr(), labels_ptr=lh.data_ptr())
             tr.step_staged(with_labels=True, sync_loss=True)
@@ -711,10 +722,12 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * world,
                "api": "gdx_trainer_stage_inputs + gdx_trainer_step_staged (C ABI), pinned host buffers",
                "pipelining": "step i+1's feature H2D overlaps step i's compute (double buffer)",
-               "pcie_floor_ms": round(h2d / world / 55e9 * 1e3, 2),
-               "pcie_floor_note": "each rank's H2D at the ~55 GB/s pinned PCIe rate measured alone "
-                                  "(tools/h2d_probe.py): e2e cannot go below this while the "
-                                  "fp32 inputs are re-sent every step"}
+               "pcie_floor_ms": round(h2d_alone_ms, 2),
+               "h2d_alone_gbs": round(xh.numel() * 4 / h2d_alone_ms / 1e6, 1),
+               "pcie_floor_note": "this rank's feature block copied alone from the same pinned buffer "
+                                  "in this run (best of 3, CUDA events); e2e cannot go below it while "
+                                  "the fp32 inputs are re-sent every step (tools/h2d_probe.py "
+                                  "sweeps sizes)"}
 
     l2_peak = probe_l2_peak(torch, dev)
     gather_peak = probe_gather_ceiling(torch, dev, packed24)
